@@ -1,0 +1,217 @@
+/*
+ * include/mpap.h -- C ABI of libmpap.so, the B200 (sm_100a) hot path of MPAP
+ * (Ichter, Landry, Schmerling, Pavone, "Perception-Aware Motion Planning via
+ * Multiobjective Search on GPUs", arXiv 1705.02408; "P:n" = line n of the
+ * paper source /root/reference/PAPER.md, cited for the reader -- nothing here
+ * reads it at run time).
+ *
+ * Two calls carry the method (BASELINE.json north_star):
+ *   mpap_build_roadmap*  -- Alg. 2 BuildGraph + Alg. 1 line 2,
+ *                           the perception-heuristic precompute (P:178,
+ *                           P:222-225): r_n-disc neighbour CSR with per-edge
+ *                           cost, perception-heuristic summary and collision bit.
+ *   mpap_search*         -- Alg. 3 Explore: group-marching
+ *                           multiobjective (cost, h) search; returns the plan,
+ *                           its cost and its perception value.
+ * Numerics follow DESIGN.md §3 "Numeric contract" (bit-exact with the CPU
+ * oracle in oracle/, which shares no code with this library).
+ *
+ * Conventions for every entry point:
+ *   - returns mpap_status; never throws, never aborts the process;
+ *   - on a non-OK status mpap_last_error() gives a thread-local detail string;
+ *   - outputs are valid only on MPAP_OK, except where stated;
+ *   - `cuda_stream` is a cudaStream_t (NULL = legacy default stream); all
+ *     device work is ordered on it.  The device is the one current when
+ *     mpap_build_roadmap* was called; the roadmap is bound to it.
+ *   - pointer arguments documented as "mem space" are host pointers when
+ *     mem == MPAP_MEM_HOST and device pointers when mem == MPAP_MEM_DEVICE;
+ *     all other pointers are host pointers.  Inputs are borrowed (read during
+ *     the call, never retained).
+ */
+#ifndef MPAP_H
+#define MPAP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MPAP_OK = 0,
+  MPAP_ERR_INVALID_ARGUMENT = 1, /* a documented precondition failed            */
+  MPAP_ERR_NO_GOAL_NODE = 2,     /* no node position in X_goal (R19)      */
+  MPAP_ERR_NO_FEASIBLE_PLAN = 3, /* P_open emptied with no goal plan (A3.5) */
+  MPAP_ERR_BUFFER_TOO_SMALL = 4, /* path_capacity too small; path_len = required */
+  MPAP_ERR_OUT_OF_MEMORY = 5,    /* device allocation failed                     */
+  MPAP_ERR_CUDA = 6              /* CUDA runtime error; see mpap_last_error()    */
+} mpap_status;
+
+enum { MPAP_MEM_HOST = 0, MPAP_MEM_DEVICE = 1 };
+
+/* Cost(u,v) model (reading R7). */
+enum { MPAP_KINEMATIC = 0, MPAP_DOUBLE_INTEGRATOR = 1 };
+
+/* Perception heuristic (P:323-328 feature count; P:476-477 learned; R9-R12). */
+enum {
+  MPAP_PH_OMNI_COUNT = 0,         /* visible = in range and unobstructed           */
+  MPAP_PH_FOV_VELOCITY_COUNT = 1, /* + in the FOV cone around the velocity         */
+  MPAP_PH_FOV_HEADING_COUNT = 2,  /* + in the FOV cone around the interpolated yaw */
+  MPAP_PH_FOV_HEADING_MLP = 3     /* heading count + learned-style 3-8-8-2 MLP      */
+};
+
+typedef struct {
+  int32_t pos_dim;        /* d in {2, 3}                                            */
+  int32_t dynamics;       /* MPAP_KINEMATIC or MPAP_DOUBLE_INTEGRATOR               */
+  int32_t has_heading;    /* sample row ends with (cos yaw, sin yaw) (R21, N1)      */
+  int32_t heuristic;      /* MPAP_PH_*                                             */
+  double ws_lo[3], ws_hi[3]; /* workspace box; leaving it is a collision (R8)       */
+  double control_weight;  /* r_u > 0 in J = int_0^tau (1 + r_u |u|^2) dt (R7)       */
+  double nominal_speed;   /* > 0; kinematic edge duration = length / speed (R9)     */
+  double dt;              /* > 0; heuristic timestep                        */
+  double collision_dt;    /* > 0; polyline resolution of double-integrator edges    */
+  double n_f;             /* > 0; features offsetting drift (P:325-327, 12 in paper) */
+  double fov_cos_half;    /* in (0, 1]; cos of the FOV half angle           */
+  double max_range;       /* > 0; feature range                         */
+  const double *mlp;      /* MLP only: 122 doubles W1[8x3] b1[8] W2[8x8] b2[8]
+                             W3[2x8] b3[2] (host memory); else may be NULL          */
+  double mlp_gain;        /* gamma of R12                                           */
+  double v_ref, w_ref;    /* > 0; MLP input scales (R12)                            */
+} mpap_params;
+
+/* Opaque, device-resident, immutable after build: B >= 1 environments, each
+ * with its own node set and CSR ("offline precomputation"). */
+typedef struct mpap_roadmap mpap_roadmap;
+
+/*
+ * mpap_build_roadmap_batch -- Alg. 2 + heuristic precompute for B environments
+ * sharing `r` and `params`.
+ *   n_envs          B >= 1.
+ *   samples         mem space; rows of env 0, then env 1, ...; row b,u has
+ *                   row_stride doubles: p[d] (+ v[d] if double integrator)
+ *                   (+ cos yaw, sin yaw if has_heading).  Row u = node u of its
+ *                   env; x_init is whichever node the search names as start.
+ *   n               host, [B]: node count of each env (>= 1).
+ *   obstacles       mem space; [sum O_b][2d] closed boxes lo[d], hi[d].
+ *   n_obstacles     host, [B] (>= 0).
+ *   features        mem space; [sum F_b][d] feature positions.
+ *   n_features      host, [B] (>= 0).
+ *   r               r_n > 0, finite: Near(V,u,r) = {v: Cost(u,v) < r}.
+ *   params          host; see mpap_params.
+ *   mem             MPAP_MEM_HOST or MPAP_MEM_DEVICE for the three arrays.
+ *   out             receives the roadmap handle; free with mpap_roadmap_free.
+ * Errors: INVALID_ARGUMENT (null pointers, n < 1, pos_dim not 2/3, row_stride
+ * too small, lo >= hi in a box, non-finite samples, r <= 0, params out of
+ * range), OUT_OF_MEMORY, CUDA.  Synchronises `cuda_stream` before returning.
+ */
+mpap_status mpap_build_roadmap_batch(int32_t n_envs, const double *samples, const int32_t *n,
+                                     int32_t row_stride, const double *obstacles,
+                                     const int32_t *n_obstacles, const double *features,
+                                     const int32_t *n_features, double r, const mpap_params *params,
+                                     int32_t mem, void *cuda_stream, mpap_roadmap **out);
+
+/* Single-environment form of the north_star call
+ * mpap_build_roadmap(samples, obstacles, features, r): B = 1. */
+mpap_status mpap_build_roadmap(const double *samples, int32_t n, int32_t row_stride,
+                               const double *obstacles, int32_t n_obstacles,
+                               const double *features, int32_t n_features, double r,
+                               const mpap_params *params, int32_t mem, void *cuda_stream,
+                               mpap_roadmap **out);
+
+/* X_goal: closed box on position (reading R20). */
+typedef struct { double lo[3], hi[3]; } mpap_goal;
+
+typedef struct {
+  int32_t status;     /* mpap_status of this query (OK or NO_FEASIBLE_PLAN ...)     */
+  int32_t path_len;   /* nodes in the plan, start first (0 if no plan)              */
+  int32_t waves;      /* non-empty groups expanded (reading R24)                    */
+  int32_t retries;    /* capacity regrow-and-rerun rounds used (exact)              */
+  float cost;         /* plan cost p.cost (f32 sum along the path, N5)               */
+  float h;            /* plan perception value p.h (A3.21; R25)                      */
+  float h_peak;       /* max node-prefix h along the plan (<= beta) (R25)            */
+  float pad;
+  int64_t relaxations;     /* (plan in G, collision-free edge) pairs (R23)           */
+  int64_t labels_inserted; /* plans that survived RemoveDominated (A3.15)            */
+} mpap_result;
+
+/* Per-wave counters (DESIGN.md §3 "counters"), identical to the oracle's. */
+typedef struct {
+  int64_t i, group, relax, beta_pass, inserted, killed, touched, stair_sum;
+} mpap_wave;
+
+/*
+ * mpap_search -- Alg. 3 Explore on environment `env` of `rm` (SURVEY.md §8(a)
+ * rows a5-a10).
+ *   start           x_init node index in [0, n_env).
+ *   goal            host; X_goal box (only the first pos_dim axes are used).
+ *   perception_bound beta in [0, +inf] (Eq. 2; A3.9 P:251); +inf = agnostic.
+ *   lambda          group cost factor in (0, 1] (reading R1).
+ *   path            host, [path_capacity]: node sequence start..goal.
+ *   result          host; filled for OK and NO_FEASIBLE_PLAN (path_len = 0).
+ *   waves, waves_capacity  optional host trace of per-wave counters (NULL/0 = off);
+ *                   result->waves says how many were produced.
+ * Returns OK, NO_FEASIBLE_PLAN, NO_GOAL_NODE, BUFFER_TOO_SMALL (result->path_len
+ * = required length), INVALID_ARGUMENT, OUT_OF_MEMORY, CUDA.  Synchronises.
+ */
+mpap_status mpap_search(const mpap_roadmap *rm, int32_t env, int32_t start, const mpap_goal *goal,
+                        double perception_bound, double lambda, int32_t *path, int32_t path_capacity,
+                        mpap_result *result, mpap_wave *waves, int32_t waves_capacity,
+                        void *cuda_stream);
+
+/*
+ * mpap_search_batch -- n_queries independent queries, one persistent CTA per
+ * query at a time (dynamic scheduling), all on `cuda_stream`.
+ *   envs, starts, goals, perception_bounds   host, [n_queries].
+ *   paths           mem space, [n_queries][path_capacity] int32.
+ *   results         mem space, [n_queries] mpap_result.
+ *   mem             MPAP_MEM_HOST: synchronises, outputs on the host.
+ *                   MPAP_MEM_DEVICE: asynchronous; outputs are written on the
+ *                   device in stream order; the caller synchronises.
+ * Returns OK if the batch executed; each query's outcome is results[q].status.
+ */
+mpap_status mpap_search_batch(const mpap_roadmap *rm, int32_t n_queries, const int32_t *envs,
+                              const int32_t *starts, const mpap_goal *goals,
+                              const double *perception_bounds, double lambda, int32_t *paths,
+                              int32_t path_capacity, mpap_result *results, int32_t mem,
+                              void *cuda_stream);
+
+/*
+ * mpap_roadmap_import -- wrap a precomputed single-environment CSR (P:337:
+ * neighbours and edge data "precomputed offline") so mpap_search can run on it.
+ *   n, pos_dim      node count (>= 1) and position dimension (2 or 3).
+ *   positions       host, [n][pos_dim] node positions (goal membership, R20).
+ *   row_ptr         host, [n+1] non-decreasing, row_ptr[0] = 0.
+ *   dst_coll, w, s, c  host, [row_ptr[n]]: dst | coll << 31 (dst < n), f32 w >= 0,
+ *                   s, c >= 0 the tropical edge summary (R10).
+ *   r               r_n used for the group threshold lambda r_n (> 0).
+ * Errors: INVALID_ARGUMENT, OUT_OF_MEMORY, CUDA.  Synchronises.
+ */
+mpap_status mpap_roadmap_import(int32_t n, int32_t pos_dim, const double *positions, const int32_t *row_ptr,
+                                const uint32_t *dst_coll, const float *w, const float *s, const float *c,
+                                double r, void *cuda_stream, mpap_roadmap **out);
+
+/* Environment count and per-env sizes: n nodes, nnz edges, nnz_free
+ * collision-free edges. */
+mpap_status mpap_roadmap_info(const mpap_roadmap *rm, int32_t env, int32_t *n, int64_t *nnz,
+                              int64_t *nnz_free);
+int32_t mpap_roadmap_envs(const mpap_roadmap *rm);
+
+/* Copy env's CSR to host buffers (parity/debug): row_ptr[n+1] (local edge
+ * offsets), dst_coll[nnz] = dst | coll << 31, w, s, c [nnz] (f32). */
+mpap_status mpap_roadmap_export(const mpap_roadmap *rm, int32_t env, int32_t *row_ptr,
+                                uint32_t *dst_coll, float *w, float *s, float *c);
+
+/* Releases the roadmap's device memory (NULL is a no-op). */
+void mpap_roadmap_free(mpap_roadmap *rm);
+
+const char *mpap_status_str(mpap_status s);
+const char *mpap_last_error(void);
+
+/* Number of kernel launches issued by this thread's calls so far (bench
+ * evidence: "gpu_launches"). */
+int64_t mpap_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPAP_H */

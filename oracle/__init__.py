@@ -314,3 +314,37 @@ def search(rm: Dict[str, np.ndarray], prob, beta: float, lam: Optional[float] = 
     return search_csr(rm["n"], rm["row_ptr"], rm["dst"], rm["coll"], rm["w"], rm["s"], rm["c"], goal_mask(prob),
                       prob.start if start is None else start, beta, prob.lam if lam is None else lam,
                       prob.r if r is None else r)
+
+
+# ---------------------------------------------------------------------------
+# harness-level parallelism: independent rows of Alg. 2 on several processes
+# (each process runs the unchanged sequential per-row oracle; the assembled
+# CSR is identical to orc_build's -- checked in tests/test_oracle_build.py)
+# ---------------------------------------------------------------------------
+
+def _rows_worker(args):
+    prob, lo, hi, use_prefilter = args
+    out = []
+    for u in range(lo, hi):
+        out.append(build_row(prob, u, use_prefilter))
+    return out
+
+
+def build_roadmap_parallel(prob, procs: int = 0, use_prefilter: bool = True) -> Dict[str, np.ndarray]:
+    import multiprocessing as mp
+    n = prob.samples.shape[0]
+    procs = procs or os.cpu_count() or 1
+    if procs <= 1:
+        return build_roadmap(prob, use_prefilter)
+    nchunk = procs * 8
+    bounds = np.linspace(0, n, nchunk + 1).astype(int)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        parts = pool.map(_rows_worker, [(prob, int(bounds[k]), int(bounds[k + 1]), use_prefilter)
+                                        for k in range(nchunk)])
+    rows = [r for part in parts for r in part]
+    row_ptr = np.zeros(n + 1, np.int32)
+    row_ptr[1:] = np.cumsum([len(r["dst"]) for r in rows])
+    cat = lambda k, dt: np.concatenate([r[k] for r in rows]).astype(dt) if rows else np.zeros(0, dt)
+    return {"n": n, "row_ptr": row_ptr, "dst": cat("dst", np.int32), "coll": cat("coll", np.uint8),
+            "w": cat("w", np.float32), "s": cat("s", np.float32), "c": cat("c", np.float32)}

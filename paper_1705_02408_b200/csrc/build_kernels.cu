@@ -1,0 +1,737 @@
+// paper_1705_02408_b200/csrc/build_kernels.cu -- roadmap build on sm_100a.
+//
+// Alg. 2 BuildGraph and Alg. 1 line 2, the perception
+// heuristic precompute (heuristic §4.1, learned
+// heuristic §5.2), as three kernels per batch of environments:
+//
+//   k_near   one warp per row u: Near(V \ {u}, u, r_n) = {v : Cost(u,v) < r}
+//            (A2.3 P:213).  Kinematic cost is evaluated by every lane;
+//            double-integrator pairs pass a conservative prefilter first and
+//            the survivors are compacted into a per-warp shared-memory queue so
+//            the root-isolation cascade (reading R7) always runs 32-wide.
+//            Entries come out in ascending v (ballot-ordered appends).
+//   k_scan   exclusive scan of the row counts -> CSR row_ptr (int64).
+//   k_edges  one warp per row, one edge at a time: Collision(u,v) (P:190,
+//            A2.5 P:215; reading R8) with lanes over polyline segments, then
+//            the heuristic summary (R9, R10, R12) with lanes over timesteps;
+//            per edge the warp culls features/boxes against the bounding box
+//            of its sample points (exact: a culled item provably fails its
+//            test), and folds the per-step increments in time
+//            order with shuffles.  Writes the 16-byte EdgeRec.
+//
+// Every floating-point expression follows DESIGN.md §3 ("Numeric contract")
+// operation by operation and is compiled with --fmad=false (no contraction),
+// so results are bit-identical to the CPU oracle without sharing its code.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "mpap_internal.cuh"
+
+namespace mpap {
+
+#define FULL 0xffffffffu
+constexpr int kWarps = 8;                 // warps per block in the build kernels
+constexpr double kCullMargin = 1e-6;      // absolute; >> rounding of O(100) coordinates
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---------------------------------------------------------------------------
+// geometry (DESIGN.md §3 "slab")
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool seg_box(const double* A, const double* B, const double* box, int d) {
+  double t0 = 0.0, t1 = 1.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (k >= d) break;
+    const double lo = box[k], hi = box[d + k];
+    const double dk = B[k] - A[k];
+    if (dk == 0.0) {
+      if (A[k] < lo || A[k] > hi) return false;
+    } else {
+      const double inv = 1.0 / dk;
+      double ta = (lo - A[k]) * inv;
+      double tb = (hi - A[k]) * inv;
+      if (ta > tb) { const double tmp = ta; ta = tb; tb = tmp; }
+      if (ta > t0) t0 = ta;
+      if (tb < t1) t1 = tb;
+      if (t0 > t1) return false;
+    }
+  }
+  return true;
+}
+
+__device__ __forceinline__ bool outside_ws(const double* p, const DevParams& P) {
+  for (int k = 0; k < P.pos_dim; ++k)
+    if (p[k] < P.ws_lo[k] || p[k] > P.ws_hi[k]) return true;
+  return false;
+}
+
+// ---------------------------------------------------------------------------
+// double-integrator steering (reading R7)
+// ---------------------------------------------------------------------------
+struct DiCoef { double vv, av, aa, B, C, D, ru; };
+
+__device__ __forceinline__ void di_coefs(const double* su, const double* sv, int d, double ru, DiCoef& k) {
+  double vv = 0.0, av = 0.0, aa = 0.0;
+  for (int j = 0; j < d; ++j) {
+    const double p0 = su[j], v0 = su[d + j], p1 = sv[j], v1 = sv[d + j];
+    const double a = p1 - p0;
+    vv = vv + ((v0 * v0 + v0 * v1) + v1 * v1);
+    av = av + a * (v0 + v1);
+    aa = aa + a * a;
+  }
+  k.vv = vv; k.av = av; k.aa = aa; k.ru = ru;
+  k.B = (4.0 * ru) * vv;
+  k.C = (24.0 * ru) * av;
+  k.D = (36.0 * ru) * aa;
+}
+
+__device__ __forceinline__ double di_q(const DiCoef& k, double t) { return ((t * t - k.B) * t + k.C) * t - k.D; }
+__device__ __forceinline__ double di_qp(const DiCoef& k, double t) {
+  return ((4.0 * (t * t)) - (2.0 * k.B)) * t + k.C;
+}
+__device__ __forceinline__ double di_c(const DiCoef& k, double t) {
+  const double t2 = t * t;
+  const double t3 = t2 * t;
+  return t + k.ru * ((((4.0 * k.vv) / t) - ((12.0 * k.av) / t2)) + ((12.0 * k.aa) / t3));
+}
+
+template <int WHICH>
+__device__ __forceinline__ double di_f(const DiCoef& k, double t) { return WHICH == 0 ? di_q(k, t) : di_qp(k, t); }
+
+template <int WHICH>
+__device__ double di_bisect(const DiCoef& k, double lo, double hi) {
+  const bool hi_pos = di_f<WHICH>(k, hi) > 0.0;
+  for (int it = 0; it < 100; ++it) {
+    const double mid = lo + 0.5 * (hi - lo);
+    if (!(mid > lo && mid < hi)) break;
+    if ((di_f<WHICH>(k, mid) > 0.0) == hi_pos) hi = mid; else lo = mid;
+  }
+  return hi;
+}
+
+// Returns true and (c*, tau*) when c has a local minimiser on (0, r].
+__device__ bool cost_di(const double* su, const double* sv, int d, double ru, double r, double& c_out,
+                        double& tau_out) {
+  DiCoef k;
+  di_coefs(su, sv, d, ru, k);
+  if (k.D == 0.0) return false;
+  double bp[4];
+  int nb = 0;
+  bp[nb++] = 0.0;
+  const double tc = (k.B > 0.0) ? sqrt(k.B / 6.0) : 0.0;
+  double pieces[3];
+  int np = 0;
+  pieces[np++] = 0.0;
+  if (tc > 0.0 && tc < r) pieces[np++] = tc;
+  pieces[np++] = r;
+  for (int s = 0; s + 1 < np; ++s) {
+    const double a = pieces[s], b = pieces[s + 1];
+    const double fa = di_qp(k, a), fb = di_qp(k, b);
+    if ((fa > 0.0 && fb < 0.0) || (fa < 0.0 && fb > 0.0)) bp[nb++] = di_bisect<1>(k, a, b);
+  }
+  bp[nb++] = r;
+  for (int i = 1; i < nb; ++i) {  // ascending already; kept for the contract
+    const double x = bp[i];
+    int j = i - 1;
+    while (j >= 0 && bp[j] > x) { bp[j + 1] = bp[j]; --j; }
+    bp[j + 1] = x;
+  }
+  bool found = false;
+  double best_c = 0.0, best_t = 0.0;
+  for (int s = 0; s + 1 < nb; ++s) {
+    const double a = bp[s], b = bp[s + 1];
+    if (!(b > a)) continue;
+    if (di_q(k, a) <= 0.0 && di_q(k, b) > 0.0) {
+      const double t = di_bisect<0>(k, a, b);
+      const double c = di_c(k, t);
+      if (!found || c < best_c || (c == best_c && t < best_t)) { found = true; best_c = c; best_t = t; }
+    }
+  }
+  if (!found) return false;
+  c_out = best_c;
+  tau_out = best_t;
+  return true;
+}
+
+__device__ __forceinline__ void di_traj(const double* su, const double* sv, int d, double tau, double* c2,
+                                        double* c3) {
+  const double tau2 = tau * tau;
+  const double tau3 = tau2 * tau;
+  for (int j = 0; j < d; ++j) {
+    const double dp = (sv[j] - su[j]) - su[d + j] * tau;
+    const double dl = sv[d + j] - su[d + j];
+    c2[j] = (3.0 * dp - dl * tau) / tau2;
+    c3[j] = (dl * tau - 2.0 * dp) / tau3;
+  }
+}
+
+__device__ __forceinline__ void di_pos(const double* su, const double* c2, const double* c3, int d, double t,
+                                       double* x) {
+  for (int j = 0; j < d; ++j) x[j] = su[j] + t * (su[d + j] + t * (c2[j] + t * c3[j]));
+}
+
+__device__ __forceinline__ void di_vel(const double* su, const double* c2, const double* c3, int d, double t,
+                                       double* v) {
+  for (int j = 0; j < d; ++j) v[j] = su[d + j] + t * (2.0 * c2[j] + t * (3.0 * c3[j]));
+}
+
+// ---------------------------------------------------------------------------
+// k_near
+// ---------------------------------------------------------------------------
+template <int DYN>
+__global__ void __launch_bounds__(kWarps * 32) k_near(const double* __restrict__ samples,
+                                                      const int64_t* __restrict__ node_base,
+                                                      const int32_t* __restrict__ n_env, DevParams P, int cap,
+                                                      int32_t* __restrict__ cnt, NearRec* __restrict__ scratch,
+                                                      int* __restrict__ overflow) {
+  __shared__ int queue[kWarps][64];
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = n_env[b];
+  const int u = blockIdx.x * kWarps + warp;
+  if (u >= nb) return;  // warp-uniform
+  const int64_t row = node_base[b] + u;
+  const int d = P.pos_dim;
+  const int stride = P.stride;
+  const double* envs = samples + node_base[b] * stride;
+  double su[6];
+  for (int j = 0; j < 2 * d && j < 6; ++j) su[j] = (j < d || DYN == 1) ? envs[(int64_t)u * stride + j] : 0.0;
+  NearRec* out = scratch + row * (int64_t)cap;
+  const double r = P.r;
+  const unsigned lt = lanemask_lt();
+  int count = 0;
+  if (DYN == 0) {
+    for (int v0 = 0; v0 < nb; v0 += 32) {
+      const int v = v0 + lane;
+      bool keep = false;
+      double c = 0.0;
+      if (v < nb && v != u) {
+        const double* sv = envs + (int64_t)v * stride;
+        double acc = 0.0;
+        for (int k = 0; k < d; ++k) {
+          const double dk = sv[k] - su[k];
+          acc = acc + dk * dk;
+        }
+        c = sqrt(acc);
+        keep = c < r;
+      }
+      const unsigned m = __ballot_sync(FULL, keep);
+      if (keep) {
+        const int pos = count + __popc(m & lt);
+        if (pos < cap) out[pos] = NearRec{v, (float)c, c / P.nominal_speed};
+      }
+      count += __popc(m);
+    }
+  } else {
+    const double ru = P.control_weight;
+    double v02 = 0.0;
+    for (int j = 0; j < d; ++j) v02 += su[d + j] * su[d + j];
+    const double bp = (sqrt(v02) * r + r * r / sqrt(3.0 * ru)) * (1.0 + 1e-9);
+    const double bv = (r / sqrt(ru)) * (1.0 + 1e-9);
+    const double bp2 = bp * bp, bv2 = bv * bv;
+    int qn = 0;
+    auto process = [&](int k) {
+      bool ok = false;
+      double c = 0.0, tau = 0.0;
+      int v = -1;
+      if (lane < k) {
+        v = queue[warp][lane];
+        double sv[6];
+        const double* svp = envs + (int64_t)v * stride;
+        for (int j = 0; j < 2 * d; ++j) sv[j] = svp[j];
+        ok = cost_di(su, sv, d, ru, r, c, tau) && (c < r);
+      }
+      const unsigned m = __ballot_sync(FULL, ok);
+      if (ok) {
+        const int pos = count + __popc(m & lt);
+        if (pos < cap) out[pos] = NearRec{v, (float)c, tau};
+      }
+      count += __popc(m);
+    };
+    for (int v0 = 0; v0 < nb; v0 += 32) {
+      const int v = v0 + lane;
+      bool pf = false;
+      if (v < nb && v != u) {
+        const double* sv = envs + (int64_t)v * stride;
+        double dp2 = 0.0, dv2 = 0.0;
+        for (int j = 0; j < d; ++j) {
+          const double a = sv[j] - su[j], e = sv[d + j] - su[d + j];
+          dp2 += a * a;
+          dv2 += e * e;
+        }
+        pf = !(dp2 > bp2 || dv2 > bv2);
+      }
+      const unsigned m = __ballot_sync(FULL, pf);
+      if (pf) queue[warp][qn + __popc(m & lt)] = v;
+      qn += __popc(m);
+      __syncwarp();
+      if (qn >= 32) {
+        process(32);
+        const int rest = qn - 32;
+        int tmp = 0;
+        if (lane < rest) tmp = queue[warp][32 + lane];
+        __syncwarp();
+        if (lane < rest) queue[warp][lane] = tmp;
+        __syncwarp();
+        qn = rest;
+      }
+    }
+    if (qn > 0) process(qn);
+  }
+  if (lane == 0) {
+    cnt[row] = count;
+    if (count > cap) atomicMax(overflow, count);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_scan: single-block exclusive scan (int32 counts -> int64 offsets)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ cnt, int64_t N,
+                                               int64_t* __restrict__ row_ptr) {
+  __shared__ int64_t wsum[32];
+  const int t = threadIdx.x;
+  const int64_t chunk = (N + 1023) / 1024;
+  const int64_t lo = t * chunk, hi = min(N, lo + chunk);
+  int64_t s = 0;
+  for (int64_t i = lo; i < hi; ++i) s += cnt[i];
+  // block exclusive scan of s
+  const int lane = t & 31, w = t >> 5;
+  int64_t x = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int64_t y = wsum[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t z = __shfl_up_sync(FULL, y, o);
+      if (lane >= o) y += z;
+    }
+    wsum[lane] = y;
+  }
+  __syncthreads();
+  int64_t excl = x - s + (w > 0 ? wsum[w - 1] : 0);
+  for (int64_t i = lo; i < hi; ++i) {
+    row_ptr[i] = excl;
+    excl += cnt[i];
+  }
+  if (t == 1023) row_ptr[N] = wsum[31];
+}
+
+// ---------------------------------------------------------------------------
+// k_edges: collision + heuristic summary per edge
+// ---------------------------------------------------------------------------
+struct EdgeSmem {
+  double* box;   // [O][2d]
+  double* feat;  // [F][d]
+  int* flist;    // [kWarps][F]
+  int* blist;    // [kWarps][O]
+};
+
+__device__ __forceinline__ double warp_min(double x) {
+  for (int o = 16; o > 0; o >>= 1) x = fmin(x, __shfl_xor_sync(FULL, x, o));
+  return x;
+}
+__device__ __forceinline__ double warp_max(double x) {
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(FULL, x, o));
+  return x;
+}
+
+// Boxes overlapping [lo - m, hi + m] -> per-warp list; returns the count.
+__device__ int cull_boxes(const double* box, int O, int d, const double* lo, const double* hi, double m, int* list,
+                          int lane) {
+  int nc = 0;
+  const unsigned lt = lanemask_lt();
+  __syncwarp();
+  for (int o0 = 0; o0 < O; o0 += 32) {
+    const int o = o0 + lane;
+    bool keep = false;
+    if (o < O) {
+      keep = true;
+      const double* bx = box + (size_t)o * 2 * d;
+      for (int k = 0; k < d; ++k)
+        if (bx[k] > hi[k] + m || bx[d + k] < lo[k] - m) keep = false;
+    }
+    const unsigned msk = __ballot_sync(FULL, keep);
+    if (keep) list[nc + __popc(msk & lt)] = o;
+    nc += __popc(msk);
+  }
+  __syncwarp();
+  return nc;
+}
+
+__device__ __forceinline__ bool seg_hits_list(const double* A, const double* B, const double* box, const int* list,
+                                              int nl, int d) {
+  for (int i = 0; i < nl; ++i)
+    if (seg_box(A, B, box + (size_t)list[i] * 2 * d, d)) return true;
+  return false;
+}
+
+// Collision(u,v) of reading R8, warp-cooperative; every lane returns the result.
+__device__ bool edge_collision(const DevParams& P, const double* su, const double* sv, double tau,
+                               const EdgeSmem& S, int O, int lane) {
+  const int d = P.pos_dim;
+  if (P.dynamics == 0) {
+    bool hit = false;
+    for (int o0 = 0; o0 < O; o0 += 32) {
+      const int o = o0 + lane;
+      if (o < O && seg_box(su, sv, S.box + (size_t)o * 2 * d, d)) hit = true;
+      if (__any_sync(FULL, hit)) return true;
+    }
+    return false;
+  }
+  double c2[3], c3[3];
+  di_traj(su, sv, d, tau, c2, c3);
+  const double kc = ceil(tau / P.collision_dt);
+  const int Kc = (kc < 1.0) ? 1 : (int)kc;
+  // bounding box of the polyline vertices P_0..P_Kc
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  bool out = false;
+  for (int k = lane; k <= Kc; k += 32) {
+    const double t = (k == 0) ? 0.0 : ((double)k * tau) / (double)Kc;
+    double x[3];
+    di_pos(su, c2, c3, d, t, x);
+    if (outside_ws(x, P)) out = true;
+    for (int j = 0; j < d; ++j) { lo[j] = fmin(lo[j], x[j]); hi[j] = fmax(hi[j], x[j]); }
+  }
+  if (__any_sync(FULL, out)) return true;
+  for (int j = 0; j < d; ++j) { lo[j] = warp_min(lo[j]); hi[j] = warp_max(hi[j]); }
+  int* list = S.blist;
+  const int nl = cull_boxes(S.box, O, d, lo, hi, kCullMargin, list, lane);
+  if (nl == 0) return false;
+  for (int k0 = 1; k0 <= Kc; k0 += 32) {
+    const int k = k0 + lane;
+    bool hit = false;
+    if (k <= Kc) {
+      const double ta = (k - 1 == 0) ? 0.0 : ((double)(k - 1) * tau) / (double)Kc;
+      const double tb = ((double)k * tau) / (double)Kc;
+      double A[3], B[3];
+      di_pos(su, c2, c3, d, ta, A);
+      di_pos(su, c2, c3, d, tb, B);
+      hit = seg_hits_list(A, B, S.box, list, nl, d);
+    }
+    if (__any_sync(FULL, hit)) return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ double mlp_out0(const DevParams& P, double z0, double z1, double z2) {
+  const double* W1 = P.mlp;
+  const double* b1 = P.mlp + 24;
+  const double* W2 = P.mlp + 32;
+  const double* b2 = P.mlp + 96;
+  const double* W3 = P.mlp + 104;
+  const double* b3 = P.mlp + 120;
+  double h1[8], h2[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    double a = b1[i];
+    a = a + W1[i * 3 + 0] * z0;
+    a = a + W1[i * 3 + 1] * z1;
+    a = a + W1[i * 3 + 2] * z2;
+    h1[i] = (a > 0.0) ? a : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    double a = b2[i];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a = a + W2[i * 8 + j] * h1[j];
+    h2[i] = (a > 0.0) ? a : 0.0;
+  }
+  double o = b3[0];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o = o + W3[j] * h2[j];
+  return o;
+}
+
+// Heuristic summary (s, c) of reading R10 for a collision-free edge.
+__device__ void edge_heuristic(const DevParams& P, const double* su, const double* sv, double T, const EdgeSmem& S,
+                               int O, int F, int lane, double& s_out, double& c_out) {
+  const int d = P.pos_dim;
+  const double kk = ceil(T / P.dt);
+  const int K = (kk < 1.0) ? 1 : (int)kk;
+  const double Dl = T / (double)K;
+  double c2[3] = {0, 0, 0}, c3[3] = {0, 0, 0};
+  if (P.dynamics == 1) di_traj(su, sv, d, T, c2, c3);
+  const int hoff = P.hoff;
+  double omega = 0.0;
+  if (P.has_heading) {
+    const double ex = sv[hoff] - su[hoff], ey = sv[hoff + 1] - su[hoff + 1];
+    omega = sqrt(ex * ex + ey * ey) / T;
+  }
+  // bounding box of the step positions
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int k = lane; k < K; k += 32) {
+    const double t = (double)k * Dl;
+    double x[3];
+    if (P.dynamics == 0) {
+      const double s = t / T;
+      for (int j = 0; j < d; ++j) x[j] = su[j] + s * (sv[j] - su[j]);
+    } else {
+      di_pos(su, c2, c3, d, t, x);
+    }
+    for (int j = 0; j < d; ++j) { lo[j] = fmin(lo[j], x[j]); hi[j] = fmax(hi[j], x[j]); }
+  }
+  for (int j = 0; j < d; ++j) { lo[j] = warp_min(lo[j]); hi[j] = warp_max(hi[j]); }
+  const double R = P.max_range;
+  const double m = R + kCullMargin;
+  // features within R (+margin) of the box, per axis
+  int nf = 0;
+  {
+    const unsigned lt = lanemask_lt();
+    __syncwarp();
+    for (int f0 = 0; f0 < F; f0 += 32) {
+      const int f = f0 + lane;
+      bool keep = false;
+      if (f < F) {
+        keep = true;
+        const double* fp = S.feat + (size_t)f * d;
+        for (int k = 0; k < d; ++k)
+          if (fp[k] > hi[k] + m || fp[k] < lo[k] - m) keep = false;
+      }
+      const unsigned msk = __ballot_sync(FULL, keep);
+      if (keep) S.flist[nf + __popc(msk & lt)] = f;
+      nf += __popc(msk);
+    }
+    __syncwarp();
+  }
+  const int nb = (nf > 0) ? cull_boxes(S.box, O, d, lo, hi, m, S.blist, lane) : 0;
+  const double R2 = R * R;
+  const double cos2 = P.fov_cos_half * P.fov_cos_half;
+  double s = 0.0, c = 0.0;
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    const int k = k0 + lane;
+    double inc = 0.0;
+    if (k < K) {
+      const double t = (double)k * Dl;
+      double x[3] = {0, 0, 0}, hv[3] = {0, 0, 0}, vel[3] = {0, 0, 0};
+      if (P.dynamics == 0) {
+        const double sp = t / T;
+        for (int j = 0; j < d; ++j) x[j] = su[j] + sp * (sv[j] - su[j]);
+      } else {
+        di_pos(su, c2, c3, d, t, x);
+        di_vel(su, c2, c3, d, t, vel);
+      }
+      if (P.heuristic == 1) {
+        if (P.dynamics == 1) { for (int j = 0; j < d; ++j) hv[j] = vel[j]; }
+        else { for (int j = 0; j < d; ++j) hv[j] = sv[j] - su[j]; }
+      } else if (P.heuristic >= 2) {
+        const double sp = t / T;
+        hv[0] = (1.0 - sp) * su[hoff] + sp * sv[hoff];
+        hv[1] = (1.0 - sp) * su[hoff + 1] + sp * sv[hoff + 1];
+        hv[2] = 0.0;
+      }
+      double hh = 0.0;
+      for (int j = 0; j < d; ++j) hh = hh + hv[j] * hv[j];
+      int kv = 0;
+      for (int i = 0; i < nf; ++i) {
+        const double* fp = S.feat + (size_t)S.flist[i] * d;
+        double dl[3];
+        double dd = 0.0;
+        for (int j = 0; j < d; ++j) { dl[j] = fp[j] - x[j]; dd = dd + dl[j] * dl[j]; }
+        if (dd > R2) continue;
+        if (P.heuristic != 0) {
+          double dot = 0.0;
+          for (int j = 0; j < d; ++j) dot = dot + hv[j] * dl[j];
+          if (!(hh > 0.0)) continue;
+          if (dot < 0.0) continue;
+          if (dot * dot < cos2 * (hh * dd)) continue;
+        }
+        if (seg_hits_list(x, fp, S.box, S.blist, nb, d)) continue;
+        ++kv;
+      }
+      inc = Dl - (double)kv * (Dl / P.n_f);
+      if (P.heuristic == 3) {
+        double speed;
+        if (P.dynamics == 1) {
+          double ss = 0.0;
+          for (int j = 0; j < d; ++j) ss = ss + vel[j] * vel[j];
+          speed = sqrt(ss);
+        } else {
+          speed = P.nominal_speed;
+        }
+        const double z0 = speed / P.v_ref;
+        const double z1 = omega / P.w_ref;
+        const double z2 = (double)kv / P.n_f;
+        const double o = mlp_out0(P, z0, z1, z2);
+        inc = inc + Dl * (P.mlp_gain * o);
+      }
+    }
+    const int nk = min(32, K - k0);
+    for (int j = 0; j < nk; ++j) {   // fold in time order (every lane, same values)
+      const double ij = __shfl_sync(FULL, inc, j);
+      const double t = c + ij;
+      c = (t > 0.0) ? t : 0.0;
+      s = s + ij;
+    }
+  }
+  s_out = s;
+  c_out = c;
+}
+
+__global__ void __launch_bounds__(kWarps * 32) k_edges(const double* __restrict__ samples,
+                                                       const int64_t* __restrict__ node_base,
+                                                       const int32_t* __restrict__ n_env,
+                                                       const double* __restrict__ obst,
+                                                       const int32_t* __restrict__ obst_base,
+                                                       const double* __restrict__ feat,
+                                                       const int32_t* __restrict__ feat_base, DevParams P,
+                                                       int cap, int o_max, int f_max,
+                                                       const int32_t* __restrict__ cnt,
+                                                       const NearRec* __restrict__ scratch,
+                                                       const int64_t* __restrict__ row_ptr,
+                                                       EdgeRec* __restrict__ edges,
+                                                       unsigned long long* __restrict__ nnz_free) {
+  extern __shared__ double smem[];
+  const int b = blockIdx.y;
+  const int d = P.pos_dim;
+  const int O = obst_base[b + 1] - obst_base[b];
+  const int F = feat_base[b + 1] - feat_base[b];
+  double* sbox = smem;
+  double* sfeat = smem + (size_t)o_max * 2 * d;
+  int* lists = reinterpret_cast<int*>(sfeat + (size_t)f_max * d);
+  for (int i = threadIdx.x; i < O * 2 * d; i += blockDim.x) sbox[i] = obst[(size_t)obst_base[b] * 2 * d + i];
+  for (int i = threadIdx.x; i < F * d; i += blockDim.x) sfeat[i] = feat[(size_t)feat_base[b] * d + i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = n_env[b];
+  const int u = blockIdx.x * kWarps + warp;
+  if (u >= nb) return;
+  EdgeSmem S;
+  S.box = sbox;
+  S.feat = sfeat;
+  S.flist = lists + warp * (f_max + o_max);
+  S.blist = S.flist + f_max;
+  const int stride = P.stride;
+  const int64_t row = node_base[b] + u;
+  const double* envs = samples + node_base[b] * stride;
+  double su[8], sv[8];
+  for (int j = 0; j < stride && j < 8; ++j) su[j] = envs[(int64_t)u * stride + j];
+  const int deg = min(cnt[row], cap);
+  const int64_t e0 = row_ptr[row];
+  int nfree = 0;
+  for (int j = 0; j < deg; ++j) {
+    const NearRec rec = scratch[row * (int64_t)cap + j];
+    for (int q = 0; q < stride && q < 8; ++q) sv[q] = envs[(int64_t)rec.v * stride + q];
+    const bool coll = edge_collision(P, su, sv, rec.tau, S, O, lane);
+    float s32 = 0.0f, c32 = 0.0f;
+    if (!coll) {
+      double s64, c64;
+      edge_heuristic(P, su, sv, rec.tau, S, O, F, lane, s64, c64);
+      s32 = (float)s64;
+      c32 = (float)c64;
+      ++nfree;
+    }
+    if (lane == 0) {
+      EdgeRec er;
+      er.dst_coll = (uint32_t)rec.v | (coll ? 0x80000000u : 0u);
+      er.w = rec.w;
+      er.s = s32;
+      er.c = c32;
+      edges[e0 + j] = er;
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && nfree) atomicAdd(&nnz_free[b], (unsigned long long)nfree);
+}
+
+// ---------------------------------------------------------------------------
+// host driver
+// ---------------------------------------------------------------------------
+#define CK(x)                                          \
+  do {                                                 \
+    cudaError_t _e = (x);                              \
+    if (_e != cudaSuccess) return cuda_error(_e, #x);  \
+  } while (0)
+
+mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
+  const int B = rm->B;
+  const int64_t N = rm->node_base[B];
+  int32_t* d_n = nullptr;
+  int32_t* d_cnt = nullptr;
+  int* d_over = nullptr;
+  NearRec* d_scr = nullptr;
+  unsigned long long* d_free = nullptr;
+  mpap_status status = MPAP_OK;
+  int cap = 128;
+  CK(cudaMallocAsync(&d_n, sizeof(int32_t) * B, st));
+  CK(cudaMemcpyAsync(d_n, rm->n.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice, st));
+  CK(cudaMallocAsync(&d_cnt, sizeof(int32_t) * N, st));
+  CK(cudaMallocAsync(&d_over, sizeof(int), st));
+  CK(cudaMallocAsync(&d_free, sizeof(unsigned long long) * B, st));
+  CK(cudaMemsetAsync(d_free, 0, sizeof(unsigned long long) * B, st));
+  CK(cudaMallocAsync(&rm->d_row_ptr, sizeof(int64_t) * (N + 1), st));
+  const dim3 grid((rm->n_max + kWarps - 1) / kWarps, B);
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    if (d_scr) CK(cudaFreeAsync(d_scr, st));
+    const size_t bytes = sizeof(NearRec) * (size_t)N * (size_t)cap;
+    if (cudaMallocAsync(&d_scr, bytes, st) != cudaSuccess) {
+      d_scr = nullptr;
+      cudaGetLastError();
+      return set_error(MPAP_ERR_OUT_OF_MEMORY, "neighbour scratch allocation failed");
+    }
+    CK(cudaMemsetAsync(d_over, 0, sizeof(int), st));
+    if (rm->prm.dynamics == 0)
+      k_near<0><<<grid, kWarps * 32, 0, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->prm, cap, d_cnt, d_scr,
+                                               d_over);
+    else
+      k_near<1><<<grid, kWarps * 32, 0, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->prm, cap, d_cnt, d_scr,
+                                               d_over);
+    note_launch();
+    CK(cudaGetLastError());
+    int over = 0;
+    CK(cudaMemcpyAsync(&over, d_over, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (over == 0) break;
+    cap = ((over + 31) / 32) * 32;   // exact regrow: re-run with room for the widest row
+  }
+  k_scan<<<1, 1024, 0, st>>>(d_cnt, N, rm->d_row_ptr);
+  note_launch();
+  CK(cudaGetLastError());
+  std::vector<int64_t> bounds(B + 1);
+  for (int b = 0; b <= B; ++b) {
+    CK(cudaMemcpyAsync(&bounds[b], rm->d_row_ptr + rm->node_base[b], sizeof(int64_t), cudaMemcpyDeviceToHost,
+                       st));
+  }
+  CK(cudaStreamSynchronize(st));
+  rm->edge_base = bounds;
+  rm->nnz_total = bounds[B];
+  if (cudaMallocAsync(&rm->d_edges, sizeof(EdgeRec) * std::max<int64_t>(rm->nnz_total, 1), st) != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(MPAP_ERR_OUT_OF_MEMORY, "edge array allocation failed");
+  }
+  const int d = rm->prm.pos_dim;
+  const size_t smem = sizeof(double) * ((size_t)rm->o_max * 2 * d + (size_t)rm->f_max * d) +
+                      sizeof(int) * (size_t)kWarps * (rm->f_max + rm->o_max);
+  CK(cudaFuncSetAttribute(k_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
+  if (rm->nnz_total > 0) {
+    k_edges<<<grid, kWarps * 32, smem, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->d_obst, rm->d_obst_base,
+                                             rm->d_feat, rm->d_feat_base, rm->prm, cap, rm->o_max, rm->f_max,
+                                             d_cnt, d_scr, rm->d_row_ptr, rm->d_edges, d_free);
+    note_launch();
+    CK(cudaGetLastError());
+  }
+  std::vector<unsigned long long> fr(B);
+  CK(cudaMemcpyAsync(fr.data(), d_free, sizeof(unsigned long long) * B, cudaMemcpyDeviceToHost, st));
+  CK(cudaFreeAsync(d_scr, st));
+  CK(cudaFreeAsync(d_cnt, st));
+  CK(cudaFreeAsync(d_over, st));
+  CK(cudaFreeAsync(d_free, st));
+  CK(cudaFreeAsync(d_n, st));
+  CK(cudaStreamSynchronize(st));
+  rm->nnz_free.assign(fr.begin(), fr.end());
+  return status;
+}
+
+}  // namespace mpap

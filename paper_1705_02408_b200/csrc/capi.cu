@@ -1,0 +1,388 @@
+// paper_1705_02408_b200/csrc/capi.cu -- the extern "C" boundary of
+// libmpap.so (include/mpap.h): argument validation, status codes, device
+// memory ownership.  All compute happens in build_kernels.cu / search_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "mpap_internal.cuh"
+
+namespace mpap {
+static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+void note_launch(int k) { g_launches.fetch_add(k); }
+
+mpap_status set_error(mpap_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+mpap_status cuda_error(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  if (e == cudaErrorMemoryAllocation) return MPAP_ERR_OUT_OF_MEMORY;
+  return MPAP_ERR_CUDA;
+}
+}  // namespace mpap
+
+using namespace mpap;
+
+#define CKC(x)                                          \
+  do {                                                  \
+    cudaError_t _e = (x);                               \
+    if (_e != cudaSuccess) {                            \
+      mpap_status _s = cuda_error(_e, #x);              \
+      mpap_roadmap_free(rm);                            \
+      return _s;                                        \
+    }                                                   \
+  } while (0)
+
+static bool is_fin(double x) { return std::isfinite(x); }
+
+static mpap_status validate_params(const mpap_params* p, double r) {
+  if (!p) return set_error(MPAP_ERR_INVALID_ARGUMENT, "params is NULL");
+  if (p->pos_dim != 2 && p->pos_dim != 3) return set_error(MPAP_ERR_INVALID_ARGUMENT, "pos_dim must be 2 or 3");
+  if (p->dynamics != MPAP_KINEMATIC && p->dynamics != MPAP_DOUBLE_INTEGRATOR)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "unknown dynamics");
+  if (p->heuristic < MPAP_PH_OMNI_COUNT || p->heuristic > MPAP_PH_FOV_HEADING_MLP)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "unknown heuristic");
+  if (p->heuristic >= MPAP_PH_FOV_HEADING_COUNT && !p->has_heading)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "heading heuristic needs has_heading");
+  if (p->heuristic == MPAP_PH_FOV_HEADING_MLP && !p->mlp)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "MLP heuristic needs 122 weights");
+  if (!(r > 0.0) || !is_fin(r)) return set_error(MPAP_ERR_INVALID_ARGUMENT, "r must be finite and > 0");
+  const double pos[] = {p->control_weight, p->nominal_speed, p->dt, p->collision_dt, p->n_f, p->max_range,
+                        p->v_ref, p->w_ref};
+  for (double x : pos)
+    if (!(x > 0.0) || !is_fin(x)) return set_error(MPAP_ERR_INVALID_ARGUMENT, "params: positive finite field");
+  if (!(p->fov_cos_half > 0.0) || p->fov_cos_half > 1.0)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "fov_cos_half must be in (0, 1]");
+  if (!is_fin(p->mlp_gain)) return set_error(MPAP_ERR_INVALID_ARGUMENT, "mlp_gain not finite");
+  for (int k = 0; k < p->pos_dim; ++k)
+    if (!(p->ws_lo[k] < p->ws_hi[k])) return set_error(MPAP_ERR_INVALID_ARGUMENT, "workspace lo >= hi");
+  return MPAP_OK;
+}
+
+extern "C" {
+
+const char* mpap_status_str(mpap_status s) {
+  switch (s) {
+    case MPAP_OK: return "MPAP_OK";
+    case MPAP_ERR_INVALID_ARGUMENT: return "MPAP_ERR_INVALID_ARGUMENT";
+    case MPAP_ERR_NO_GOAL_NODE: return "MPAP_ERR_NO_GOAL_NODE";
+    case MPAP_ERR_NO_FEASIBLE_PLAN: return "MPAP_ERR_NO_FEASIBLE_PLAN";
+    case MPAP_ERR_BUFFER_TOO_SMALL: return "MPAP_ERR_BUFFER_TOO_SMALL";
+    case MPAP_ERR_OUT_OF_MEMORY: return "MPAP_ERR_OUT_OF_MEMORY";
+    case MPAP_ERR_CUDA: return "MPAP_ERR_CUDA";
+  }
+  return "MPAP_ERR_UNKNOWN";
+}
+
+const char* mpap_last_error(void) { return g_last_error.c_str(); }
+
+int64_t mpap_launch_count(void) { return (int64_t)g_launches.load(); }
+
+void mpap_roadmap_free(mpap_roadmap* rm) {
+  if (!rm) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(rm->device);
+  cudaFree(rm->d_samples);
+  cudaFree(rm->d_obst);
+  cudaFree(rm->d_feat);
+  cudaFree(rm->d_obst_base);
+  cudaFree(rm->d_feat_base);
+  cudaFree(rm->d_node_base);
+  cudaFree(rm->d_row_ptr);
+  cudaFree(rm->d_edges);
+  cudaSetDevice(cur);
+  delete rm;
+}
+
+mpap_status mpap_build_roadmap_batch(int32_t n_envs, const double* samples, const int32_t* n, int32_t row_stride,
+                                     const double* obstacles, const int32_t* n_obstacles, const double* features,
+                                     const int32_t* n_features, double r, const mpap_params* params, int32_t mem,
+                                     void* cuda_stream, mpap_roadmap** out) {
+  if (!out) return set_error(MPAP_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (n_envs < 1 || !n || !n_obstacles || !n_features || !samples)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "n_envs < 1 or NULL count/sample arrays");
+  if (mem != MPAP_MEM_HOST && mem != MPAP_MEM_DEVICE) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad mem space");
+  mpap_status s = validate_params(params, r);
+  if (s != MPAP_OK) return s;
+  const int d = params->pos_dim;
+  const int need = d * (params->dynamics == MPAP_DOUBLE_INTEGRATOR ? 2 : 1) + (params->has_heading ? 2 : 0);
+  if (row_stride < need || row_stride > 8)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "row_stride too small (or > 8)");
+  int64_t N = 0, O = 0, F = 0;
+  for (int b = 0; b < n_envs; ++b) {
+    if (n[b] < 1) return set_error(MPAP_ERR_INVALID_ARGUMENT, "n < 1");
+    if (n_obstacles[b] < 0 || n_features[b] < 0) return set_error(MPAP_ERR_INVALID_ARGUMENT, "negative count");
+    N += n[b];
+    O += n_obstacles[b];
+    F += n_features[b];
+  }
+  if (N > INT32_MAX / 2) return set_error(MPAP_ERR_INVALID_ARGUMENT, "too many nodes");
+  if ((O > 0 && !obstacles) || (F > 0 && !features))
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "NULL obstacle/feature array");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  // host copies of the inputs are needed for validation of host arrays only;
+  // device arrays are validated by value-independent checks (sizes) here.
+  if (mem == MPAP_MEM_HOST) {
+    for (int64_t i = 0; i < N * row_stride; ++i)
+      if (!is_fin(samples[i])) return set_error(MPAP_ERR_INVALID_ARGUMENT, "non-finite sample coordinate");
+    for (int64_t o = 0; o < O; ++o)
+      for (int k = 0; k < d; ++k)
+        if (!(obstacles[o * 2 * d + k] < obstacles[o * 2 * d + d + k]))
+          return set_error(MPAP_ERR_INVALID_ARGUMENT, "obstacle with lo >= hi");
+  }
+  mpap_roadmap* rm = new (std::nothrow) mpap_roadmap();
+  if (!rm) return set_error(MPAP_ERR_OUT_OF_MEMORY, "host allocation failed");
+  CKC(cudaGetDevice(&rm->device));
+  rm->B = n_envs;
+  DevParams& P = rm->prm;
+  std::memset(&P, 0, sizeof(P));
+  P.pos_dim = d;
+  P.dynamics = params->dynamics;
+  P.has_heading = params->has_heading;
+  P.heuristic = params->heuristic;
+  P.stride = row_stride;
+  P.hoff = d * (params->dynamics == MPAP_DOUBLE_INTEGRATOR ? 2 : 1);
+  for (int k = 0; k < 3; ++k) {
+    P.ws_lo[k] = params->ws_lo[k];
+    P.ws_hi[k] = params->ws_hi[k];
+  }
+  P.control_weight = params->control_weight;
+  P.nominal_speed = params->nominal_speed;
+  P.dt = params->dt;
+  P.collision_dt = params->collision_dt;
+  P.n_f = params->n_f;
+  P.fov_cos_half = params->fov_cos_half;
+  P.max_range = params->max_range;
+  P.mlp_gain = params->mlp_gain;
+  P.v_ref = params->v_ref;
+  P.w_ref = params->w_ref;
+  P.r = r;
+  if (params->mlp) std::memcpy(P.mlp, params->mlp, sizeof(double) * kMlpSize);
+  rm->n.assign(n, n + n_envs);
+  rm->n_obst.assign(n_obstacles, n_obstacles + n_envs);
+  rm->n_feat.assign(n_features, n_features + n_envs);
+  rm->node_base.assign(n_envs + 1, 0);
+  std::vector<int32_t> ob(n_envs + 1, 0), fb(n_envs + 1, 0);
+  for (int b = 0; b < n_envs; ++b) {
+    rm->node_base[b + 1] = rm->node_base[b] + n[b];
+    ob[b + 1] = ob[b] + n_obstacles[b];
+    fb[b + 1] = fb[b] + n_features[b];
+    rm->n_max = std::max(rm->n_max, n[b]);
+    rm->o_max = std::max(rm->o_max, n_obstacles[b]);
+    rm->f_max = std::max(rm->f_max, n_features[b]);
+  }
+  const cudaMemcpyKind kind = (mem == MPAP_MEM_HOST) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  CKC(cudaMalloc(&rm->d_samples, sizeof(double) * N * row_stride));
+  CKC(cudaMemcpyAsync(rm->d_samples, samples, sizeof(double) * N * row_stride, kind, st));
+  CKC(cudaMalloc(&rm->d_obst, sizeof(double) * std::max<int64_t>(O * 2 * d, 1)));
+  if (O) CKC(cudaMemcpyAsync(rm->d_obst, obstacles, sizeof(double) * O * 2 * d, kind, st));
+  CKC(cudaMalloc(&rm->d_feat, sizeof(double) * std::max<int64_t>(F * d, 1)));
+  if (F) CKC(cudaMemcpyAsync(rm->d_feat, features, sizeof(double) * F * d, kind, st));
+  CKC(cudaMalloc(&rm->d_obst_base, sizeof(int32_t) * (n_envs + 1)));
+  CKC(cudaMemcpyAsync(rm->d_obst_base, ob.data(), sizeof(int32_t) * (n_envs + 1), cudaMemcpyHostToDevice, st));
+  CKC(cudaMalloc(&rm->d_feat_base, sizeof(int32_t) * (n_envs + 1)));
+  CKC(cudaMemcpyAsync(rm->d_feat_base, fb.data(), sizeof(int32_t) * (n_envs + 1), cudaMemcpyHostToDevice, st));
+  CKC(cudaMalloc(&rm->d_node_base, sizeof(int64_t) * (n_envs + 1)));
+  CKC(cudaMemcpyAsync(rm->d_node_base, rm->node_base.data(), sizeof(int64_t) * (n_envs + 1),
+                      cudaMemcpyHostToDevice, st));
+  s = build_roadmap_device(rm, st);
+  if (s != MPAP_OK) {
+    mpap_roadmap_free(rm);
+    return s;
+  }
+  // the stream-ordered allocation of row_ptr/edges must be visible to other
+  // streams that later search this roadmap
+  CKC(cudaStreamSynchronize(st));
+  *out = rm;
+  return MPAP_OK;
+}
+
+mpap_status mpap_build_roadmap(const double* samples, int32_t n, int32_t row_stride, const double* obstacles,
+                               int32_t n_obstacles, const double* features, int32_t n_features, double r,
+                               const mpap_params* params, int32_t mem, void* cuda_stream, mpap_roadmap** out) {
+  return mpap_build_roadmap_batch(1, samples, &n, row_stride, obstacles, &n_obstacles, features, &n_features, r,
+                                  params, mem, cuda_stream, out);
+}
+
+mpap_status mpap_roadmap_import(int32_t n, int32_t pos_dim, const double* positions, const int32_t* row_ptr,
+                                const uint32_t* dst_coll, const float* w, const float* s, const float* c, double r,
+                                void* cuda_stream, mpap_roadmap** out) {
+  if (!out) return set_error(MPAP_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (n < 1 || (pos_dim != 2 && pos_dim != 3) || !positions || !row_ptr)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad n/pos_dim/positions/row_ptr");
+  if (!(r > 0.0) || !is_fin(r)) return set_error(MPAP_ERR_INVALID_ARGUMENT, "r must be finite and > 0");
+  if (row_ptr[0] != 0) return set_error(MPAP_ERR_INVALID_ARGUMENT, "row_ptr[0] != 0");
+  for (int32_t u = 0; u < n; ++u)
+    if (row_ptr[u + 1] < row_ptr[u]) return set_error(MPAP_ERR_INVALID_ARGUMENT, "row_ptr decreasing");
+  const int64_t nnz = row_ptr[n];
+  if (nnz > 0 && (!dst_coll || !w || !s || !c)) return set_error(MPAP_ERR_INVALID_ARGUMENT, "NULL edge arrays");
+  std::vector<EdgeRec> er((size_t)std::max<int64_t>(nnz, 1));
+  for (int64_t k = 0; k < nnz; ++k) {
+    if ((int64_t)(dst_coll[k] & 0x7fffffffu) >= n) return set_error(MPAP_ERR_INVALID_ARGUMENT, "dst out of range");
+    if (!(w[k] >= 0.0f) || !(s[k] == s[k]) || !(c[k] >= 0.0f))
+      return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad edge value");
+    er[k].dst_coll = dst_coll[k];
+    er[k].w = w[k];
+    er[k].s = s[k];
+    er[k].c = c[k];
+  }
+  for (int64_t k = 0; k < (int64_t)n * pos_dim; ++k)
+    if (!is_fin(positions[k])) return set_error(MPAP_ERR_INVALID_ARGUMENT, "non-finite position");
+  mpap_roadmap* rm = new (std::nothrow) mpap_roadmap();
+  if (!rm) return set_error(MPAP_ERR_OUT_OF_MEMORY, "host allocation failed");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  CKC(cudaGetDevice(&rm->device));
+  rm->B = 1;
+  std::memset(&rm->prm, 0, sizeof(rm->prm));
+  rm->prm.pos_dim = pos_dim;
+  rm->prm.stride = pos_dim;
+  rm->prm.r = r;
+  rm->n.assign(1, n);
+  rm->n_obst.assign(1, 0);
+  rm->n_feat.assign(1, 0);
+  rm->node_base = {0, n};
+  rm->edge_base = {0, nnz};
+  rm->n_max = n;
+  int64_t nf = 0;
+  for (int64_t k = 0; k < nnz; ++k) nf += (dst_coll[k] >> 31) == 0u;
+  rm->nnz_free.assign(1, nf);
+  rm->nnz_total = nnz;
+  std::vector<int64_t> rp64(n + 1);
+  for (int32_t u = 0; u <= n; ++u) rp64[u] = row_ptr[u];
+  CKC(cudaMalloc(&rm->d_samples, sizeof(double) * n * pos_dim));
+  CKC(cudaMemcpyAsync(rm->d_samples, positions, sizeof(double) * n * pos_dim, cudaMemcpyHostToDevice, st));
+  CKC(cudaMalloc(&rm->d_node_base, sizeof(int64_t) * 2));
+  CKC(cudaMemcpyAsync(rm->d_node_base, rm->node_base.data(), sizeof(int64_t) * 2, cudaMemcpyHostToDevice, st));
+  CKC(cudaMalloc(&rm->d_row_ptr, sizeof(int64_t) * (n + 1)));
+  CKC(cudaMemcpyAsync(rm->d_row_ptr, rp64.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
+  CKC(cudaMalloc(&rm->d_edges, sizeof(EdgeRec) * er.size()));
+  CKC(cudaMemcpyAsync(rm->d_edges, er.data(), sizeof(EdgeRec) * er.size(), cudaMemcpyHostToDevice, st));
+  CKC(cudaStreamSynchronize(st));
+  *out = rm;
+  return MPAP_OK;
+}
+
+int32_t mpap_roadmap_envs(const mpap_roadmap* rm) { return rm ? rm->B : 0; }
+
+mpap_status mpap_roadmap_info(const mpap_roadmap* rm, int32_t env, int32_t* n, int64_t* nnz, int64_t* nnz_free) {
+  if (!rm || env < 0 || env >= rm->B) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad roadmap/env");
+  if (n) *n = rm->n[env];
+  if (nnz) *nnz = rm->edge_base[env + 1] - rm->edge_base[env];
+  if (nnz_free) *nnz_free = rm->nnz_free[env];
+  return MPAP_OK;
+}
+
+mpap_status mpap_roadmap_export(const mpap_roadmap* rm, int32_t env, int32_t* row_ptr, uint32_t* dst_coll, float* w,
+                                float* s, float* c) {
+  if (!rm || env < 0 || env >= rm->B || !row_ptr)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad roadmap/env/row_ptr");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != rm->device) return set_error(MPAP_ERR_INVALID_ARGUMENT, "roadmap bound to another device");
+  const int32_t ne = rm->n[env];
+  std::vector<int64_t> rp(ne + 1);
+  cudaError_t e = cudaMemcpy(rp.data(), rm->d_row_ptr + rm->node_base[env], sizeof(int64_t) * (ne + 1),
+                             cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_error(e, "export row_ptr");
+  const int64_t e0 = rp[0], nnz = rp[ne] - rp[0];
+  for (int32_t u = 0; u <= ne; ++u) row_ptr[u] = (int32_t)(rp[u] - e0);
+  std::vector<EdgeRec> er((size_t)std::max<int64_t>(nnz, 1));
+  if (nnz) {
+    e = cudaMemcpy(er.data(), rm->d_edges + e0, sizeof(EdgeRec) * nnz, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_error(e, "export edges");
+  }
+  for (int64_t k = 0; k < nnz; ++k) {
+    if (dst_coll) dst_coll[k] = er[k].dst_coll;
+    if (w) w[k] = er[k].w;
+    if (s) s[k] = er[k].s;
+    if (c) c[k] = er[k].c;
+  }
+  return MPAP_OK;
+}
+
+static mpap_status check_query(const mpap_roadmap* rm, int32_t env, int32_t start, const mpap_goal* goal,
+                               double beta) {
+  if (env < 0 || env >= rm->B) return set_error(MPAP_ERR_INVALID_ARGUMENT, "env out of range");
+  if (start < 0 || start >= rm->n[env]) return set_error(MPAP_ERR_INVALID_ARGUMENT, "start out of range");
+  if (!goal) return set_error(MPAP_ERR_INVALID_ARGUMENT, "goal is NULL");
+  if (std::isnan(beta) || beta < 0.0) return set_error(MPAP_ERR_INVALID_ARGUMENT, "beta must be >= 0 (or +inf)");
+  return MPAP_OK;
+}
+
+static void to_desc(QueryDesc& q, int32_t env, int32_t start, const mpap_goal* g, double beta) {
+  q.env = env;
+  q.start = start;
+  q.beta = beta;
+  for (int k = 0; k < 3; ++k) {
+    q.goal_lo[k] = g->lo[k];
+    q.goal_hi[k] = g->hi[k];
+  }
+}
+
+mpap_status mpap_search(const mpap_roadmap* rm, int32_t env, int32_t start, const mpap_goal* goal,
+                        double perception_bound, double lambda, int32_t* path, int32_t path_capacity,
+                        mpap_result* result, mpap_wave* waves, int32_t waves_capacity, void* cuda_stream) {
+  if (!rm || !result || (!path && path_capacity > 0) || path_capacity < 0)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "NULL roadmap/result/path");
+  if (!(lambda > 0.0) || lambda > 1.0) return set_error(MPAP_ERR_INVALID_ARGUMENT, "lambda must be in (0, 1]");
+  mpap_status s = check_query(rm, env, start, goal, perception_bound);
+  if (s != MPAP_OK) return s;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != rm->device) return set_error(MPAP_ERR_INVALID_ARGUMENT, "roadmap bound to another device");
+  QueryDesc q;
+  to_desc(q, env, start, goal, perception_bound);
+  std::vector<int32_t> pbuf((size_t)std::max(path_capacity, 1));
+  mpap_result r{};
+  s = search_batch_device(rm, 1, &q, lambda, pbuf.data(), std::max(path_capacity, 1), &r, waves, waves_capacity,
+                          MPAP_MEM_HOST, static_cast<cudaStream_t>(cuda_stream));
+  if (s != MPAP_OK) return s;
+  *result = r;
+  if (r.status == MPAP_OK) {
+    if (r.path_len > path_capacity) {
+      result->status = MPAP_ERR_BUFFER_TOO_SMALL;
+      return set_error(MPAP_ERR_BUFFER_TOO_SMALL, "path_capacity too small");
+    }
+    std::memcpy(path, pbuf.data(), sizeof(int32_t) * r.path_len);
+    return MPAP_OK;
+  }
+  if (r.status == MPAP_ERR_BUFFER_TOO_SMALL) return set_error(MPAP_ERR_BUFFER_TOO_SMALL, "path_capacity too small");
+  if (r.status == MPAP_ERR_NO_FEASIBLE_PLAN) return set_error(MPAP_ERR_NO_FEASIBLE_PLAN, "no feasible plan");
+  if (r.status == MPAP_ERR_NO_GOAL_NODE) return set_error(MPAP_ERR_NO_GOAL_NODE, "no node in the goal region");
+  return set_error((mpap_status)r.status, "search failed");
+}
+
+mpap_status mpap_search_batch(const mpap_roadmap* rm, int32_t n_queries, const int32_t* envs, const int32_t* starts,
+                              const mpap_goal* goals, const double* perception_bounds, double lambda, int32_t* paths,
+                              int32_t path_capacity, mpap_result* results, int32_t mem, void* cuda_stream) {
+  if (!rm || n_queries < 0 || (n_queries > 0 && (!envs || !starts || !goals || !perception_bounds || !paths ||
+                                                  !results)) || path_capacity < 1)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "NULL argument or path_capacity < 1");
+  if (mem != MPAP_MEM_HOST && mem != MPAP_MEM_DEVICE) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad mem space");
+  if (!(lambda > 0.0) || lambda > 1.0) return set_error(MPAP_ERR_INVALID_ARGUMENT, "lambda must be in (0, 1]");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != rm->device) return set_error(MPAP_ERR_INVALID_ARGUMENT, "roadmap bound to another device");
+  std::vector<QueryDesc> qs(n_queries);
+  for (int k = 0; k < n_queries; ++k) {
+    mpap_status s = check_query(rm, envs[k], starts[k], &goals[k], perception_bounds[k]);
+    if (s != MPAP_OK) return s;
+    to_desc(qs[k], envs[k], starts[k], &goals[k], perception_bounds[k]);
+  }
+  return search_batch_device(rm, n_queries, qs.data(), lambda, paths, path_capacity, results, nullptr, 0, mem,
+                             static_cast<cudaStream_t>(cuda_stream));
+}
+
+}  // extern "C"

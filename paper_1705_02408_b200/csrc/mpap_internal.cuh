@@ -1,0 +1,85 @@
+// paper_1705_02408_b200/csrc/mpap_internal.cuh -- internal declarations of
+// libmpap.so (CUDA side only; the CPU oracle in oracle/ shares nothing with
+// this file).  Public ABI: include/mpap.h.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "mpap.h"
+
+namespace mpap {
+
+constexpr int kMlpSize = 122;
+
+// Kernel-parameter copy of mpap_params plus derived constants; passed by value
+// (lives in the constant bank, so every lane reads it as a broadcast).
+struct DevParams {
+  int pos_dim, dynamics, has_heading, heuristic;
+  int stride;  // doubles per sample row
+  int hoff;    // offset of (cos yaw, sin yaw) in a row
+  double ws_lo[3], ws_hi[3];
+  double control_weight, nominal_speed, dt, collision_dt, n_f, fov_cos_half, max_range;
+  double mlp_gain, v_ref, w_ref;
+  double r;
+  double mlp[kMlpSize];
+};
+
+// One roadmap edge: 16 bytes, read with one LDG.128 by the search
+// (SURVEY.md §8(a) a4).  x = dst | coll << 31, y = w (f32 bits), z = s, w = c.
+struct __align__(16) EdgeRec {
+  uint32_t dst_coll;
+  float w, s, c;
+};
+
+// Output of the neighbour kernel: one r-disc entry before collision/heuristic.
+struct __align__(16) NearRec {
+  int32_t v;
+  float w;      // (float)Cost(u,v)
+  double tau;   // edge duration (kinematic: length/speed; DI: tau*)
+};
+
+}  // namespace mpap
+
+struct mpap_roadmap {
+  int device = 0;
+  int B = 0;
+  mpap::DevParams prm{};
+  std::vector<int32_t> n;          // nodes per env
+  std::vector<int64_t> node_base;  // first global row of each env (B+1)
+  std::vector<int64_t> edge_base;  // first global edge of each env (B+1)
+  std::vector<int32_t> n_obst, n_feat;
+  std::vector<int64_t> nnz_free;   // collision-free edges per env
+  int32_t n_max = 0, o_max = 0, f_max = 0;
+  double* d_samples = nullptr;     // [sum n][stride]
+  double* d_obst = nullptr;        // [sum O][2d]
+  double* d_feat = nullptr;        // [sum F][d]
+  int32_t* d_obst_base = nullptr;  // [B+1]
+  int32_t* d_feat_base = nullptr;  // [B+1]
+  int64_t* d_node_base = nullptr;  // [B+1]
+  int64_t* d_row_ptr = nullptr;    // [sum n + 1] global edge offsets
+  mpap::EdgeRec* d_edges = nullptr;
+  int64_t nnz_total = 0;
+};
+
+namespace mpap {
+// launch bookkeeping shared by the translation units (host side)
+void note_launch(int k = 1);
+mpap_status set_error(mpap_status s, const std::string& msg);
+mpap_status cuda_error(cudaError_t e, const char* what);
+
+// roadmap build (build_kernels.cu)
+mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st);
+
+// search (search_kernels.cu)
+struct QueryDesc {
+  int32_t env, start;
+  double beta;
+  double goal_lo[3], goal_hi[3];
+};
+mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryDesc* h_queries,
+                                double lambda, int32_t* paths, int32_t path_cap, mpap_result* results,
+                                mpap_wave* h_waves, int32_t waves_cap, int32_t mem, cudaStream_t st);
+}  // namespace mpap

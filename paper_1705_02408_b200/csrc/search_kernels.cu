@@ -1,0 +1,758 @@
+// paper_1705_02408_b200/csrc/search_kernels.cu -- Alg. 3 Explore on sm_100a.
+//
+// The group-marching multiobjective search of PAPER.md P:237-265 (text
+// P:227-235), one persistent CTA per query at a time (queries are pulled from
+// an atomic work counter, so a batch of independent queries load-balances
+// across the 148 SMs).  Per wave (one non-empty group G_i):
+//
+//   expand   warp per plan p of G_i; the head's CSR row is streamed 32 edges
+//            at a time with one 16-byte load per lane (A3.6-A3.8):
+//              cost' = p.cost + w,  h' = max(c, p.h + s)       (PH; R10)
+//            cutoff h' <= beta (A3.9); a candidate already dominated by the
+//            node's current non-dominated staircase is dropped on the spot
+//            (it cannot survive RemoveDominated); survivors are
+//            appended with warp-aggregated atomics (ballot + popc).
+//   group    per-destination counts -> block scan -> scatter, so each touched
+//            node's candidates are contiguous.
+//   merge    warp per touched node: RemoveDominated (A3.15) as a set
+//            operation -- old staircase entries dominated by a candidate die
+//            (open ones are removed from P_open), candidates dominated by
+//            another candidate are dropped, survivors get label ids (warp-
+//            aggregated) and enter the staircase and the pending open list.
+//   advance  G_i is retired (A3.16), i <- i+1 (A3.17), and the pending list
+//            is partitioned into G_{i+1} = {cost <= (i+1) lambda r_n} (A3.18)
+//            with ballot compaction; empty groups are skipped exactly (R24).
+// The loop stops when G holds a goal plan (A3.5) or nothing is open; the
+// result is the minimum (cost, h, node sequence) plan over the goal nodes'
+// staircases (A3.20-A3.21; R16).  Every per-wave decision depends only on
+// sets, never on thread order (R14), so plans are bit-identical to the oracle.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "mpap_internal.cuh"
+
+namespace mpap {
+
+#define FULLM 0xffffffffu
+constexpr int kST = 512;              // threads per search CTA
+constexpr int kSW = kST / 32;         // warps per search CTA
+enum : uint8_t { L_OPEN = 0, L_CLOSED = 1, L_DEAD = 2 };
+enum { OVF_LABELS = 1, OVF_CAND = 2, OVF_STAIR = 4 };
+constexpr int kRetryBase = 100;       // result.status = kRetryBase + OVF_* mask
+
+struct SlotCaps {
+  int n;     // nodes per slot (max over envs)
+  int K;     // staircase slots per node
+  int L;     // label pool capacity
+  int C;     // candidates per wave
+};
+
+struct SearchArgs {
+  // roadmap
+  const double* samples;
+  const int64_t* node_base;
+  const int32_t* n_env;
+  const int64_t* row_ptr;
+  const EdgeRec* edges;
+  int stride, pos_dim;
+  double T;           // lambda * r_n (f64)
+  // queries
+  const QueryDesc* queries;
+  const int32_t* qidx;   // query index list (retries run a subset)
+  int nq;
+  int* work;
+  // slots
+  SlotCaps caps;
+  int4* labels;
+  uint8_t* lstate;
+  float2* stair_ch;
+  int32_t* stair_id;
+  int32_t* stair_n;
+  int32_t* cand_cnt;
+  int32_t* cand_off;
+  int4* cand;
+  int4* cand_sorted;
+  int32_t* touched;
+  int32_t* G;
+  int32_t* pend;
+  int32_t* pend2;
+  int32_t* stamp;
+  uint8_t* goal;
+  // outputs
+  int32_t* paths;
+  int path_cap;
+  mpap_result* results;
+  mpap_wave* waves;
+  int waves_cap;
+};
+
+struct Ctl {
+  int q, gsize, psize, nsize, ncand, ntouched, nlabels, goal_in_g, overflow, any_goal;
+  long long i, minb;
+  unsigned long long relax, bpass, tcount, ssum, inserted, killed;
+  unsigned long long relax_total, inserted_total;
+  int waves;
+  unsigned long long best_key;
+  int nties;
+  int ties[32];
+};
+
+__device__ __forceinline__ unsigned lane_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ long long bucket_of(float cost, double T) {
+  const double c = (double)cost;
+  long long b = (long long)ceil(c / T);
+  if (b < 0) b = 0;
+  while (b > 0 && c <= (double)(b - 1) * T) --b;
+  while (c > (double)b * T) ++b;
+  return b;
+}
+
+// Block-wide exclusive scan of cand_cnt over the touched list -> cand_off.
+__device__ void scan_touched(int nt, const int32_t* touched, const int32_t* cnt, int32_t* off, int* s_wsum) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int chunk = (nt + kST - 1) / kST;
+  const int lo = t * chunk, hi = min(nt, lo + chunk);
+  int s = 0;
+  for (int k = lo; k < hi; ++k) s += cnt[touched[k]];
+  int x = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULLM, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int y = (lane < kSW) ? s_wsum[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int z = __shfl_up_sync(FULLM, y, o);
+      if (lane >= o) y += z;
+    }
+    if (lane < kSW) s_wsum[lane] = y;
+  }
+  __syncthreads();
+  int excl = x - s + (w > 0 ? s_wsum[w - 1] : 0);
+  for (int k = lo; k < hi; ++k) {
+    const int xk = touched[k];
+    off[xk] = excl;
+    excl += cnt[xk];
+  }
+}
+
+// Partition src -> (G if cost <= inext*T else dst).  Tracks the goal flag of
+// G and the minimum bucket of dst.  Dead labels are dropped (lazy deletion).
+__device__ void partition(const SearchArgs& A, Ctl& S, const int32_t* src, int nsrc, int32_t* G, int32_t* dst,
+                          long long inext, const int4* labels, const uint8_t* lstate, const uint8_t* goal) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lane_lt();
+  const double thr = (double)inext * A.T;
+  long long myminb = LLONG_MAX;
+  bool mygoal = false;
+  for (int k0 = (threadIdx.x >> 5) * 32; k0 < nsrc; k0 += kST) {
+    const int k = k0 + lane;
+    bool toG = false, toD = false;
+    int id = -1;
+    if (k < nsrc) {
+      id = src[k];
+      if (lstate[id] == L_OPEN) {
+        const int4 lb = labels[id];
+        const float cost = __int_as_float(lb.z);
+        if ((double)cost <= thr) {
+          toG = true;
+          if (goal[lb.x]) mygoal = true;
+        } else {
+          toD = true;
+          myminb = min(myminb, bucket_of(cost, A.T));
+        }
+      }
+    }
+    const unsigned mg = __ballot_sync(FULLM, toG);
+    const unsigned md = __ballot_sync(FULLM, toD);
+    int bg = 0, bd = 0;
+    if (lane == 0) {
+      if (mg) bg = atomicAdd(&S.gsize, __popc(mg));
+      if (md) bd = atomicAdd(&S.nsize, __popc(md));
+    }
+    bg = __shfl_sync(FULLM, bg, 0);
+    bd = __shfl_sync(FULLM, bd, 0);
+    if (toG) G[bg + __popc(mg & lt)] = id;
+    if (toD) dst[bd + __popc(md & lt)] = id;
+  }
+  if (mygoal) S.goal_in_g = 1;
+  if (myminb != LLONG_MAX) atomicMin(&S.minb, myminb);
+}
+
+template <bool TRACE>
+__device__ void run_query(const SearchArgs& A, Ctl& S, int* s_wsum, int slot, int qpos) {
+  const int q = A.qidx[qpos];
+  const QueryDesc Q = A.queries[q];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = lane_lt();
+  const SlotCaps C = A.caps;
+  const int env = Q.env;
+  const int n = A.n_env[env];
+  const int64_t nbase = A.node_base[env];
+  const int64_t* rp = A.row_ptr + nbase;
+  // slot views
+  int4* labels = A.labels + (size_t)slot * C.L;
+  uint8_t* lstate = A.lstate + (size_t)slot * C.L;
+  float2* sch = A.stair_ch + (size_t)slot * C.n * C.K;
+  int32_t* sid = A.stair_id + (size_t)slot * C.n * C.K;
+  int32_t* sn = A.stair_n + (size_t)slot * C.n;
+  int32_t* ccnt = A.cand_cnt + (size_t)slot * C.n;
+  int32_t* coff = A.cand_off + (size_t)slot * C.n;
+  int4* cand = A.cand + (size_t)slot * C.C;
+  int4* cs = A.cand_sorted + (size_t)slot * C.C;
+  int32_t* touched = A.touched + (size_t)slot * C.n;
+  int32_t* G = A.G + (size_t)slot * C.L;
+  int32_t* pend = A.pend + (size_t)slot * C.L;
+  int32_t* pend2 = A.pend2 + (size_t)slot * C.L;
+  int32_t* stamp = A.stamp + (size_t)slot * C.n;
+  uint8_t* goal = A.goal + (size_t)slot * C.n;
+  const double beta = Q.beta;
+  const int d = A.pos_dim;
+
+  // ---- a5: init (A3.1-A3.4) ----
+  if (tid == 0) {
+    S.gsize = 1; S.psize = 0; S.nsize = 0; S.ncand = 0; S.ntouched = 0; S.nlabels = 1;
+    S.goal_in_g = 0; S.overflow = 0; S.any_goal = 0; S.i = 0; S.minb = LLONG_MAX;
+    S.relax_total = 0; S.inserted_total = 0; S.waves = 0;
+  }
+  __syncthreads();
+  bool mygoal = false;
+  for (int x = tid; x < n; x += kST) {
+    sn[x] = 0;
+    ccnt[x] = 0;
+    if (TRACE) stamp[x] = -1;
+    const double* p = A.samples + (nbase + x) * A.stride;
+    bool in = true;
+    for (int k = 0; k < d; ++k)
+      if (p[k] < Q.goal_lo[k] || p[k] > Q.goal_hi[k]) in = false;
+    goal[x] = in ? 1 : 0;
+    mygoal |= in;
+  }
+  if (__any_sync(FULLM, mygoal) && lane == 0) S.any_goal = 1;
+  __syncthreads();
+  if (tid == 0) {
+    labels[0] = make_int4(Q.start, -1, __float_as_int(0.0f), __float_as_int(0.0f));
+    lstate[0] = L_OPEN;
+    sch[(size_t)Q.start * C.K] = make_float2(0.0f, 0.0f);
+    sid[(size_t)Q.start * C.K] = 0;
+    sn[Q.start] = 1;
+    G[0] = 0;
+    S.goal_in_g = goal[Q.start];
+  }
+  __syncthreads();
+  mpap_result* R = A.results + q;
+  if (!S.any_goal) {
+    if (tid == 0) {
+      mpap_result r{};
+      r.status = MPAP_ERR_NO_GOAL_NODE;
+      *R = r;
+    }
+    return;
+  }
+
+  // ---- wave loop (A3.5-A3.19) ----
+  int wave = 0;
+  while (true) {
+    if (S.goal_in_g || S.gsize == 0) break;     // A3.5 (G = {} <=> P_open = {} here)
+    const int gsize = S.gsize;
+    const long long i_cur = S.i;
+    if (tid == 0) {
+      S.relax = 0; S.bpass = 0; S.tcount = 0; S.ssum = 0; S.inserted = 0; S.killed = 0;
+      S.ncand = 0; S.ntouched = 0;
+    }
+    __syncthreads();
+    // ---- a7 expand (A3.6-A3.11) ----
+    {
+      unsigned long long my_relax = 0, my_bpass = 0, my_t = 0, my_ss = 0;
+      for (int k = warp; k < gsize; k += kSW) {
+        const int p = G[k];
+        const int4 lb = labels[p];
+        const int u = lb.x;
+        const float pc = __int_as_float(lb.z), ph = __int_as_float(lb.w);
+        const int64_t e0 = rp[u], e1 = rp[u + 1];
+        for (int64_t eb = e0; eb < e1; eb += 32) {
+          const int64_t e = eb + lane;
+          bool fr = false, emit = false;
+          int x = 0;
+          float qc = 0.f, qh = 0.f;
+          if (e < e1) {
+            const uint4 raw = __ldg(reinterpret_cast<const uint4*>(A.edges) + e);
+            fr = (raw.x >> 31) == 0u;
+            if (fr) {
+              x = (int)(raw.x & 0x7fffffffu);
+              qc = pc + __uint_as_float(raw.y);
+              const float t = ph + __uint_as_float(raw.z);
+              const float cc = __uint_as_float(raw.w);
+              qh = (t > cc) ? t : cc;
+              if ((double)qh <= beta) {
+                ++my_bpass;
+                const int m = sn[x];
+                if (TRACE) {
+                  if (atomicExch(&stamp[x], wave) != wave) { ++my_t; my_ss += (unsigned long long)m; }
+                }
+                bool dom = false;
+                const float2* st = sch + (size_t)x * C.K;
+                for (int j = 0; j < m; ++j) {
+                  const float2 b = st[j];
+                  if (b.x < qc && b.y <= qh) { dom = true; break; }
+                }
+                emit = !dom;
+              }
+            }
+          }
+          my_relax += __popc(__ballot_sync(FULLM, fr)) * (lane == 0 ? 1u : 0u);
+          const unsigned em = __ballot_sync(FULLM, emit);
+          if (em) {
+            int base = 0;
+            if (lane == 0) base = atomicAdd(&S.ncand, __popc(em));
+            base = __shfl_sync(FULLM, base, 0);
+            if (emit) {
+              const int idx = base + __popc(em & lt);
+              if (idx < C.C) {
+                cand[idx] = make_int4(x, __float_as_int(qc), __float_as_int(qh), p);
+                if (atomicAdd(&ccnt[x], 1) == 0) touched[atomicAdd(&S.ntouched, 1)] = x;
+              } else {
+                atomicOr(&S.overflow, OVF_CAND);
+              }
+            }
+          }
+        }
+      }
+      if (my_relax) atomicAdd(&S.relax, my_relax);
+      if (my_bpass) atomicAdd(&S.bpass, my_bpass);
+      if (TRACE) {
+        if (my_t) atomicAdd(&S.tcount, my_t);
+        if (my_ss) atomicAdd(&S.ssum, my_ss);
+      }
+    }
+    __syncthreads();
+    if (S.overflow) break;
+    const int nt = S.ntouched;
+    const int ncand = S.ncand;
+    // ---- group candidates by destination ----
+    scan_touched(nt, touched, ccnt, coff, s_wsum);
+    __syncthreads();
+    for (int k = tid; k < ncand; k += kST) {
+      const int4 cq = cand[k];
+      const int pos = atomicAdd(&coff[cq.x], 1);
+      cs[pos] = cq;
+    }
+    __syncthreads();
+    // ---- a8 RemoveDominated + insert (A3.10-A3.15) ----
+    {
+      unsigned long long my_ins = 0, my_kill = 0;
+      for (int t = warp; t < nt; t += kSW) {
+        const int x = touched[t];
+        const int kc = ccnt[x];
+        const int beg = coff[x] - kc;
+        const int m = sn[x];
+        float2* st = sch + (size_t)x * C.K;
+        int32_t* si = sid + (size_t)x * C.K;
+        int newm = 0;
+        // old staircase entries: killed if a candidate dominates them
+        for (int j0 = 0; j0 < m; j0 += 32) {
+          const int j = j0 + lane;
+          bool alive = false;
+          float2 o = make_float2(0.f, 0.f);
+          int oid = -1;
+          if (j < m) {
+            o = st[j];
+            oid = si[j];
+            alive = true;
+            for (int r2 = 0; r2 < kc; ++r2) {
+              const int4 cr = cs[beg + r2];
+              if (__int_as_float(cr.y) < o.x && __int_as_float(cr.z) <= o.y) { alive = false; break; }
+            }
+            if (!alive && lstate[oid] == L_OPEN) {
+              lstate[oid] = L_DEAD;
+              ++my_kill;
+            }
+          }
+          const unsigned am = __ballot_sync(FULLM, alive);
+          __syncwarp();
+          if (alive) {
+            const int pos = newm + __popc(am & lt);
+            st[pos] = o;
+            si[pos] = oid;
+          }
+          newm += __popc(am);
+          __syncwarp();
+        }
+        // candidates: survive unless another candidate dominates them
+        for (int q0 = 0; q0 < kc; q0 += 32) {
+          const int qq = q0 + lane;
+          bool surv = false;
+          int4 cq = make_int4(0, 0, 0, 0);
+          if (qq < kc) {
+            cq = cs[beg + qq];
+            surv = true;
+            const float qc = __int_as_float(cq.y), qh = __int_as_float(cq.z);
+            for (int r2 = 0; r2 < kc; ++r2) {
+              const int4 cr = cs[beg + r2];
+              if (__int_as_float(cr.y) < qc && __int_as_float(cr.z) <= qh) { surv = false; break; }
+            }
+          }
+          const unsigned sm = __ballot_sync(FULLM, surv);
+          if (sm) {
+            int lbase = 0, pbase = 0;
+            if (lane == 0) {
+              lbase = atomicAdd(&S.nlabels, __popc(sm));
+              pbase = atomicAdd(&S.psize, __popc(sm));
+            }
+            lbase = __shfl_sync(FULLM, lbase, 0);
+            pbase = __shfl_sync(FULLM, pbase, 0);
+            if (lbase + __popc(sm) > C.L) {
+              if (lane == 0) atomicOr(&S.overflow, OVF_LABELS);
+            } else if (surv) {
+              const int rk = __popc(sm & lt);
+              const int id = lbase + rk;
+              labels[id] = make_int4(x, cq.w, cq.y, cq.z);
+              lstate[id] = L_OPEN;
+              pend[pbase + rk] = id;
+              const int pos = newm + rk;
+              if (pos < C.K) {
+                st[pos] = make_float2(__int_as_float(cq.y), __int_as_float(cq.z));
+                si[pos] = id;
+              }
+            }
+            newm += __popc(sm);
+            if (lane == 0) my_ins += __popc(sm);
+          }
+        }
+        if (lane == 0) {
+          if (newm > C.K) atomicOr(&S.overflow, OVF_STAIR);
+          sn[x] = min(newm, C.K);
+        }
+      }
+      if (my_kill) atomicAdd(&S.killed, my_kill);
+      if (my_ins) atomicAdd(&S.inserted, my_ins);
+    }
+    __syncthreads();
+    if (S.overflow) break;
+    // reset per-node candidate counters of touched nodes
+    for (int t = tid; t < nt; t += kST) ccnt[touched[t]] = 0;
+    // ---- a9 retire G_i (A3.16), i <- i+1 (A3.17) ----
+    for (int k = tid; k < gsize; k += kST) {
+      const int p = G[k];
+      if (lstate[p] == L_OPEN) lstate[p] = L_CLOSED;
+    }
+    if (tid == 0) {
+      if (TRACE && wave < A.waves_cap) {
+        mpap_wave wv;
+        wv.i = i_cur; wv.group = gsize; wv.relax = (long long)S.relax; wv.beta_pass = (long long)S.bpass;
+        wv.inserted = (long long)S.inserted; wv.killed = (long long)S.killed; wv.touched = (long long)S.tcount;
+        wv.stair_sum = (long long)S.ssum;
+        A.waves[(size_t)q * A.waves_cap + wave] = wv;
+      }
+      S.relax_total += S.relax;
+      S.inserted_total += S.inserted;
+      S.waves = wave + 1;
+      S.gsize = 0; S.nsize = 0; S.goal_in_g = 0; S.minb = LLONG_MAX;
+    }
+    __syncthreads();
+    // ---- a6 G_{i+1} (A3.18), with the exact empty-group skip (R24) ----
+    const int np = S.psize;
+    long long inext = i_cur + 1;
+    partition(A, S, pend, np, G, pend2, inext, labels, lstate, goal);
+    __syncthreads();
+    if (S.gsize == 0 && S.nsize > 0) {
+      inext = S.minb;
+      const int n2 = S.nsize;
+      __syncthreads();
+      if (tid == 0) { S.nsize = 0; S.minb = LLONG_MAX; }
+      __syncthreads();
+      partition(A, S, pend2, n2, G, pend, inext, labels, lstate, goal);
+      __syncthreads();
+      if (tid == 0) { S.psize = S.nsize; S.i = inext; }
+    } else {
+      // swap pending lists
+      if (tid == 0) { S.psize = S.nsize; S.i = inext; }
+      int32_t* tmp = pend; pend = pend2; pend2 = tmp;
+    }
+    __syncthreads();
+    ++wave;
+  }
+
+  // ---- a10 goal extraction (A3.20-A3.21) ----
+  if (S.overflow) {
+    if (tid == 0) {
+      mpap_result r{};
+      r.status = kRetryBase + S.overflow;
+      *R = r;
+    }
+    return;
+  }
+  if (!S.goal_in_g) {   // P_open emptied: no feasible plan
+    if (tid == 0) {
+      mpap_result r{};
+      r.status = MPAP_ERR_NO_FEASIBLE_PLAN;
+      r.waves = S.waves;
+      r.relaxations = (int64_t)S.relax_total;
+      r.labels_inserted = (int64_t)S.inserted_total;
+      *R = r;
+    }
+    return;
+  }
+  if (tid == 0) { S.best_key = ~0ull; S.nties = 0; }
+  __syncthreads();
+  for (int x = tid; x < n; x += kST) {
+    if (!goal[x]) continue;
+    const int m = sn[x];
+    for (int j = 0; j < m; ++j) {
+      const float2 ch = sch[(size_t)x * C.K + j];
+      const unsigned long long key = ((unsigned long long)__float_as_uint(ch.x) << 32) | __float_as_uint(ch.y);
+      atomicMin(&S.best_key, key);
+    }
+  }
+  __syncthreads();
+  for (int x = tid; x < n; x += kST) {
+    if (!goal[x]) continue;
+    const int m = sn[x];
+    for (int j = 0; j < m; ++j) {
+      const float2 ch = sch[(size_t)x * C.K + j];
+      const unsigned long long key = ((unsigned long long)__float_as_uint(ch.x) << 32) | __float_as_uint(ch.y);
+      if (key == S.best_key) {
+        const int slot_t = atomicAdd(&S.nties, 1);
+        if (slot_t < 32) S.ties[slot_t] = sid[(size_t)x * C.K + j];
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // lexicographic tie-break on node sequences (R16); chains reversed into
+    // the (now unused) G / pend2 arrays
+    int best = S.ties[0];
+    const int nties = min(S.nties, 32);
+    for (int k = 1; k < nties; ++k) {
+      const int cand_id = S.ties[k];
+      int la = 0, lb = 0;
+      for (int x = cand_id; x >= 0; x = labels[x].y) G[la++] = labels[x].x;
+      for (int x = best; x >= 0; x = labels[x].y) pend2[lb++] = labels[x].x;
+      bool less = false, decided = false;
+      for (int s = 0; s < min(la, lb); ++s) {
+        const int a = G[la - 1 - s], b = pend2[lb - 1 - s];
+        if (a != b) { less = a < b; decided = true; break; }
+      }
+      if (!decided) less = la < lb;
+      if (less) best = cand_id;
+    }
+    int len = 0;
+    float hp = 0.0f;
+    for (int x = best; x >= 0; x = labels[x].y) {
+      ++len;
+      const float hx = __int_as_float(labels[x].w);
+      if (hx > hp) hp = hx;
+    }
+    mpap_result r{};
+    r.waves = S.waves;
+    r.relaxations = (int64_t)S.relax_total;
+    r.labels_inserted = (int64_t)S.inserted_total;
+    r.cost = __int_as_float(labels[best].z);
+    r.h = __int_as_float(labels[best].w);
+    r.h_peak = hp;
+    r.path_len = len;
+    if (len <= A.path_cap) {
+      int32_t* out = A.paths + (size_t)q * A.path_cap;
+      int k = len - 1;
+      for (int x = best; x >= 0; x = labels[x].y) out[k--] = labels[x].x;
+      r.status = MPAP_OK;
+    } else {
+      r.status = MPAP_ERR_BUFFER_TOO_SMALL;
+    }
+    *R = r;
+  }
+}
+
+template <bool TRACE>
+__global__ void __launch_bounds__(kST) k_search(SearchArgs A) {
+  __shared__ Ctl S;
+  __shared__ int s_wsum[32];
+  while (true) {
+    if (threadIdx.x == 0) S.q = atomicAdd(A.work, 1);
+    __syncthreads();
+    const int qpos = S.q;
+    __syncthreads();
+    if (qpos >= A.nq) break;
+    run_query<TRACE>(A, S, s_wsum, blockIdx.x, qpos);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host driver
+// ---------------------------------------------------------------------------
+#define CKS(x)                                         \
+  do {                                                 \
+    cudaError_t _e = (x);                              \
+    if (_e != cudaSuccess) return cuda_error(_e, #x);  \
+  } while (0)
+
+namespace {
+// Carves the per-launch slot arena: every array holds nslots consecutive
+// per-slot views (slot s at element offset s * cap), each array 256-B aligned.
+// With base == nullptr it only returns the byte count.
+size_t carve(SearchArgs* A, const SlotCaps& c, int nslots, char* base) {
+  size_t off = 0;
+  auto take = [&](size_t per_slot) -> void* {
+    void* r = base ? base + off : nullptr;
+    off += ((per_slot * (size_t)nslots) + 255) & ~size_t(255);
+    return r;
+  };
+  void* p;
+  p = take(sizeof(int4) * (size_t)c.L);                 if (A) A->labels = (int4*)p;
+  p = take((size_t)c.L);                                if (A) A->lstate = (uint8_t*)p;
+  p = take(sizeof(float2) * (size_t)c.n * c.K);         if (A) A->stair_ch = (float2*)p;
+  p = take(sizeof(int32_t) * (size_t)c.n * c.K);        if (A) A->stair_id = (int32_t*)p;
+  p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->stair_n = (int32_t*)p;
+  p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->cand_cnt = (int32_t*)p;
+  p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->cand_off = (int32_t*)p;
+  p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->touched = (int32_t*)p;
+  p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->stamp = (int32_t*)p;
+  p = take((size_t)c.n);                                if (A) A->goal = (uint8_t*)p;
+  p = take(sizeof(int4) * (size_t)c.C);                 if (A) A->cand = (int4*)p;
+  p = take(sizeof(int4) * (size_t)c.C);                 if (A) A->cand_sorted = (int4*)p;
+  p = take(sizeof(int32_t) * (size_t)c.L);              if (A) A->G = (int32_t*)p;
+  p = take(sizeof(int32_t) * (size_t)c.L);              if (A) A->pend = (int32_t*)p;
+  p = take(sizeof(int32_t) * (size_t)c.L);              if (A) A->pend2 = (int32_t*)p;
+  return off;
+}
+}  // namespace
+
+mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryDesc* h_queries, double lambda,
+                                int32_t* paths, int32_t path_cap, mpap_result* results, mpap_wave* h_waves,
+                                int32_t waves_cap, int32_t mem, cudaStream_t st) {
+  if (nq <= 0) return MPAP_OK;
+  int dev = 0, nsm = 0;
+  CKS(cudaGetDevice(&dev));
+  CKS(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const bool trace = (h_waves != nullptr && waves_cap > 0);
+  int occ = 1;
+  if (trace) CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_search<true>, kST, 0));
+  else CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_search<false>, kST, 0));
+  occ = std::max(occ, 1);
+  SlotCaps caps;
+  caps.n = rm->n_max;
+  caps.K = 64;
+  caps.L = std::max(1 << 17, 64 * rm->n_max);
+  caps.C = caps.L;
+
+  // device copies of the queries and outputs
+  QueryDesc* d_q = nullptr;
+  int32_t* d_qidx = nullptr;
+  int* d_work = nullptr;
+  mpap_result* d_res = nullptr;
+  int32_t* d_paths = nullptr;
+  mpap_wave* d_waves = nullptr;
+  CKS(cudaMallocAsync(&d_q, sizeof(QueryDesc) * nq, st));
+  CKS(cudaMemcpyAsync(d_q, h_queries, sizeof(QueryDesc) * nq, cudaMemcpyHostToDevice, st));
+  CKS(cudaMallocAsync(&d_qidx, sizeof(int32_t) * nq, st));
+  CKS(cudaMallocAsync(&d_work, sizeof(int), st));
+  if (mem == MPAP_MEM_DEVICE) {
+    d_res = results;
+    d_paths = paths;
+  } else {
+    CKS(cudaMallocAsync(&d_res, sizeof(mpap_result) * nq, st));
+    CKS(cudaMallocAsync(&d_paths, sizeof(int32_t) * (size_t)nq * std::max(path_cap, 1), st));
+  }
+  if (trace) CKS(cudaMallocAsync(&d_waves, sizeof(mpap_wave) * (size_t)nq * waves_cap, st));
+
+  std::vector<int32_t> todo(nq);
+  for (int k = 0; k < nq; ++k) todo[k] = k;
+  std::vector<int32_t> retries(nq, 0);
+  std::vector<mpap_result> hres(nq);
+  mpap_status status = MPAP_OK;
+  for (int round = 0; round < 12 && !todo.empty(); ++round) {
+    const int nrun = (int)todo.size();
+    const int nslots = std::min(nrun, nsm * occ);
+    const size_t sb = carve(nullptr, caps, nslots, nullptr);
+    void* base = nullptr;
+    if (cudaMallocAsync(&base, sb, st) != cudaSuccess) {
+      cudaGetLastError();
+      status = set_error(MPAP_ERR_OUT_OF_MEMORY, "search slot allocation failed");
+      break;
+    }
+    SearchArgs A{};
+    A.samples = rm->d_samples;
+    A.node_base = rm->d_node_base;
+    A.n_env = nullptr;
+    A.row_ptr = rm->d_row_ptr;
+    A.edges = rm->d_edges;
+    A.stride = rm->prm.stride;
+    A.pos_dim = rm->prm.pos_dim;
+    A.T = lambda * rm->prm.r;
+    A.queries = d_q;
+    A.qidx = d_qidx;
+    A.nq = nrun;
+    A.work = d_work;
+    A.caps = caps;
+    carve(&A, caps, nslots, static_cast<char*>(base));
+    A.paths = d_paths;
+    A.path_cap = path_cap;
+    A.results = d_res;
+    A.waves = d_waves;
+    A.waves_cap = trace ? waves_cap : 0;
+    // n_env lives with the roadmap's node bases: n_env[b] = node_base[b+1]-node_base[b]
+    int32_t* d_nenv = nullptr;
+    CKS(cudaMallocAsync(&d_nenv, sizeof(int32_t) * rm->B, st));
+    CKS(cudaMemcpyAsync(d_nenv, rm->n.data(), sizeof(int32_t) * rm->B, cudaMemcpyHostToDevice, st));
+    A.n_env = d_nenv;
+    CKS(cudaMemcpyAsync(d_qidx, todo.data(), sizeof(int32_t) * nrun, cudaMemcpyHostToDevice, st));
+    CKS(cudaMemsetAsync(d_work, 0, sizeof(int), st));
+    if (trace) k_search<true><<<nslots, kST, 0, st>>>(A);
+    else k_search<false><<<nslots, kST, 0, st>>>(A);
+    note_launch();
+    CKS(cudaGetLastError());
+    CKS(cudaFreeAsync(base, st));
+    CKS(cudaFreeAsync(d_nenv, st));
+    CKS(cudaMemcpyAsync(hres.data(), d_res, sizeof(mpap_result) * nq, cudaMemcpyDeviceToHost, st));
+    CKS(cudaStreamSynchronize(st));
+    std::vector<int32_t> again;
+    int mask = 0;
+    for (int k : todo) {
+      if (hres[k].status >= kRetryBase) {
+        again.push_back(k);
+        mask |= hres[k].status - kRetryBase;
+        retries[k]++;
+      }
+    }
+    if (mask & OVF_STAIR) caps.K *= 2;
+    if (mask & OVF_LABELS) caps.L *= 2;
+    if (mask & OVF_CAND) caps.C *= 2;
+    todo.swap(again);
+  }
+  if (status == MPAP_OK && !todo.empty()) status = set_error(MPAP_ERR_OUT_OF_MEMORY, "search capacity regrow limit");
+  // write retry counts into the results
+  for (int k = 0; k < nq; ++k) hres[k].retries = retries[k];
+  if (mem == MPAP_MEM_DEVICE) {
+    CKS(cudaMemcpyAsync(d_res, hres.data(), sizeof(mpap_result) * nq, cudaMemcpyHostToDevice, st));
+  } else {
+    std::memcpy(results, hres.data(), sizeof(mpap_result) * nq);
+    CKS(cudaMemcpyAsync(paths, d_paths, sizeof(int32_t) * (size_t)nq * path_cap, cudaMemcpyDeviceToHost, st));
+  }
+  if (trace)
+    CKS(cudaMemcpyAsync(h_waves, d_waves, sizeof(mpap_wave) * (size_t)nq * waves_cap, cudaMemcpyDeviceToHost, st));
+  CKS(cudaStreamSynchronize(st));
+  CKS(cudaFreeAsync(d_q, st));
+  CKS(cudaFreeAsync(d_qidx, st));
+  CKS(cudaFreeAsync(d_work, st));
+  if (mem != MPAP_MEM_DEVICE) {
+    CKS(cudaFreeAsync(d_res, st));
+    CKS(cudaFreeAsync(d_paths, st));
+  }
+  if (d_waves) CKS(cudaFreeAsync(d_waves, st));
+  if (mem == MPAP_MEM_DEVICE) CKS(cudaStreamSynchronize(st));
+  return status;
+}
+
+}  // namespace mpap

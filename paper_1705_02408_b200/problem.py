@@ -1,0 +1,67 @@
+"""Marshalling helpers: synth.Problem objects -> the C ABI calls.
+
+Argument packing only (no arithmetic of the method); used by tests, smoke()
+and bench.py.
+"""
+from __future__ import annotations
+
+from typing import Any, Dict, List, Sequence
+
+import numpy as np
+
+from . import (MPAP_MEM_DEVICE, Roadmap, mpap_build_roadmap, mpap_build_roadmap_batch, mpap_search,
+               mpap_search_batch, params_from_problem)
+
+
+def build_problem(prob, stream=None) -> Roadmap:
+    prm, keep = params_from_problem(prob)
+    obst = prob.obstacles if prob.obstacles.size else None
+    feat = prob.features if prob.features.size else None
+    rm = mpap_build_roadmap(prob.samples, obst if obst is not None else np.zeros((0, 2 * prob.pos_dim)),
+                            feat if feat is not None else np.zeros((0, prob.pos_dim)), prob.r, prm, stream=stream)
+    del keep
+    return rm
+
+
+def search_problem(rm: Roadmap, prob, beta: float, env: int = 0, lam=None, trace_waves: int = 0,
+                   path_capacity: int = 65536, stream=None) -> Dict[str, Any]:
+    return mpap_search(rm, env, prob.start, prob.goal_lo, prob.goal_hi, beta, prob.lam if lam is None else lam,
+                       path_capacity=path_capacity, trace_waves=trace_waves, stream=stream)
+
+
+class Batch:
+    """Concatenated host arrays of a list of problems sharing params and r."""
+
+    def __init__(self, probs: Sequence[Any]):
+        p0 = probs[0]
+        self.probs = list(probs)
+        self.stride = p0.stride
+        self.n = np.array([p.n for p in probs], np.int32)
+        self.n_obst = np.array([p.obstacles.shape[0] for p in probs], np.int32)
+        self.n_feat = np.array([p.features.shape[0] for p in probs], np.int32)
+        self.samples = np.ascontiguousarray(np.concatenate([p.samples for p in probs]), np.float64)
+        self.obstacles = np.ascontiguousarray(np.concatenate([p.obstacles.reshape(-1) for p in probs]), np.float64)
+        self.features = np.ascontiguousarray(np.concatenate([p.features.reshape(-1) for p in probs]), np.float64)
+        self.prm, self._keep = params_from_problem(p0)
+        self.r = p0.r
+        self.lam = p0.lam
+        self.starts = np.array([p.start for p in probs], np.int32)
+        self.goals_lo = [p.goal_lo for p in probs]
+        self.goals_hi = [p.goal_hi for p in probs]
+
+    @property
+    def h2d_bytes(self) -> int:
+        return int(self.samples.nbytes + self.obstacles.nbytes + self.features.nbytes)
+
+    def build(self, samples=None, obstacles=None, features=None, stream=None) -> Roadmap:
+        """Host arrays by default; pass CUDA tensors for device-resident inputs."""
+        return mpap_build_roadmap_batch(self.samples if samples is None else samples, self.n, self.stride,
+                                        self.obstacles if obstacles is None else obstacles, self.n_obst,
+                                        self.features if features is None else features, self.n_feat, self.r,
+                                        self.prm, stream=stream)
+
+    def search(self, rm: Roadmap, betas: Sequence[float], path_capacity: int = 1024, paths=None, results=None,
+               stream=None):
+        envs = np.arange(len(self.probs), dtype=np.int32)
+        return mpap_search_batch(rm, envs, self.starts, self.goals_lo, self.goals_hi, betas, self.lam,
+                                 path_capacity, paths=paths, results=results, stream=stream)

@@ -1,0 +1,76 @@
+"""Writes tests/golden/*.json: oracle results at BASELINE.json's full sizes.
+
+Calls only oracle/ (and the synth/ input generators); nothing here touches
+the CUDA path.  The GPU parity tests compare libmpap.so against these stored
+oracle outputs, because the full-size oracle build takes minutes of CPU.
+
+    python tests/golden/make_golden.py [c3] [c5] [c4]
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+from synth import load_config, make_problem  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def f32hex(x) -> str:
+    return np.float32(x).tobytes().hex()
+
+
+def run_one(prob, betas, procs):
+    t = time.time()
+    rm = oracle.build_roadmap_parallel(prob, procs)
+    tb = time.time() - t
+    free = rm["coll"] == 0
+    out = {"name": prob.name, "n": int(prob.n), "nnz": int(len(rm["dst"])), "nnz_free": int(free.sum()),
+           "w_sum": float(rm["w"].astype(np.float64).sum()), "s_sum": float(rm["s"][free].astype(np.float64).sum()),
+           "c_sum": float(rm["c"][free].astype(np.float64).sum()), "oracle_build_s": tb, "searches": []}
+    for beta in betas:
+        t = time.time()
+        r = oracle.search(rm, prob, beta)
+        out["searches"].append({
+            "beta": beta if np.isfinite(beta) else "inf", "status": r["status"], "path": r["path"].tolist(),
+            "cost": f32hex(r["cost"]), "h": f32hex(r["h"]), "h_peak": f32hex(r["h_peak"]), "waves": r["waves"],
+            "relaxations": r["relaxations"], "labels_inserted": r["labels_inserted"],
+            "wave_counters": r["wave_counters"].tolist(), "oracle_search_s": time.time() - t,
+        })
+        print(prob.name, beta, r["status_str"], r["cost"], r["h"], r["waves"], r["relaxations"], flush=True)
+    return out
+
+
+def main(argv):
+    procs = os.cpu_count() or 1
+    which = argv or ["c3", "c5"]
+    if "c3" in which:
+        cfg = load_config("c3")
+        prob = make_problem(cfg)
+        res = run_one(prob, [float(b) if b != "inf" else float("inf") for b in cfg["golden_betas"]], procs)
+        json.dump(res, open(os.path.join(HERE, "c3_full.json"), "w"), indent=1)
+    if "c5" in which:
+        cfg = load_config("c5")
+        envs = []
+        for k in range(cfg["golden_envs"]):
+            prob = make_problem(cfg, env_index=k)
+            envs.append(run_one(prob, [float(b) if b != "inf" else float("inf") for b in cfg["golden_betas"]],
+                                procs))
+        json.dump({"envs": envs}, open(os.path.join(HERE, "c5_full.json"), "w"), indent=1)
+    if "c4" in which:
+        cfg = load_config("c4")
+        prob = make_problem(cfg)
+        res = run_one(prob, [float(b) if b != "inf" else float("inf") for b in cfg["golden_betas"]], procs)
+        json.dump(res, open(os.path.join(HERE, "c4_full.json"), "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
