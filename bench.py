@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""bench.py -- MPAP hot path on B200: batched roadmap build + search.
+
+Metric (BASELINE.json): "edges relaxed/sec and queries/sec at 1/2/4/8 B200;
+HBM roofline fraction".  Workload: C5 (BASELINE.json configs[4]), the 6D
+double-integrator quadrotor named by north_star, weak-scaled: each rank
+processes its own shard of `queries_per_gpu` independent environment+query
+units (env seeds 1000 + rank*Q + k), so 8 GPUs x 64 = C5's 512 queries.
+
+One step = one pass of the whole hot path over
+the rank's batch: mpap_build_roadmap_batch (neighbours, collision, heuristic,
+CSR) + mpap_search_batch (Alg. 3 for every query) + the NCCL all-gather of the
+fixed-size result records (N > 1; the only collective, never inside the wave
+loop).  `value` = queries of all ranks / max-over-ranks device time, inputs
+resident in HBM; `e2e` = the same through the C ABI with pinned HOST buffers
+(H2D of the inputs and D2H of the results inside the timed region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mpap|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0
+# FP64 issue peak for a non-FMA DADD/DMUL stream: 148 SMs x 64 FP64 lanes x clock
+# (B200: FP64 = half the FP32 lane count; DESIGN.md §7 derivation).
+SMS = 148
+FP64_LANES_PER_SM = 64
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mpap", choices=["mpap", "reference"])
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--queries-per-gpu", type=int, default=0)
+    ap.add_argument("--beta", type=float, default=float("nan"))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-procs", type=int, default=0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if parts[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if sm:
+            out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                   "samples": len(sm)}
+        return out
+
+
+def load_peaks():
+    try:
+        pk = json.load(open(PEAKS_PATH))
+        return pk, "measured"
+    except Exception:
+        return {"hbm_gbs": FALLBACK_HBM_GBS, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+def make_shard(cfg, rank: int, Q: int):
+    from synth import make_problem
+    return [make_problem(cfg, env_index=rank * Q + k) for k in range(Q)]
+
+
+def cpu_baseline(cfg, beta: float, procs: int):
+    """The oracle as it stands on one environment+query of the workload:
+    build rows spread over `procs` processes (each the sequential oracle),
+    search single-threaded."""
+    import oracle
+    from synth import make_problem
+    oracle.build()
+    prob = make_problem(cfg, env_index=0)
+    t0 = time.perf_counter()
+    rm = oracle.build_roadmap_parallel(prob, procs)
+    t1 = time.perf_counter()
+    res = oracle.search(rm, prob, beta)
+    t2 = time.perf_counter()
+    return {"value": 1.0 / (t2 - t0), "unit": "queries/s", "cores": procs, "kind": "oracle",
+            "sample": f"1 {cfg['name']} environment+query (env 0, n={prob.n}): oracle build {t1 - t0:.2f} s "
+                      f"over {procs} processes + oracle search {t2 - t1:.3f} s (1 thread), beta={beta}",
+            "edges_relaxed_per_s": res["relaxations"] / (t2 - t0),
+            "search_only_edges_relaxed_per_s": res["relaxations"] / max(t2 - t1, 1e-9)}
+
+
+def run_reference(args, cfg, beta):
+    """--impl reference: the oracle (CPU) timed as the reference arm."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    procs = args.cpu_procs or os.cpu_count() or 1
+    import oracle
+    from synth import make_problem
+    oracle.build()
+    prob = make_problem(cfg, env_index=0)
+    times = []
+    relax = 0
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        rm = oracle.build_roadmap_parallel(prob, procs)
+        res = oracle.search(rm, prob, beta)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+            relax += res["relaxations"]
+    tot = sum(times)
+    value = args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
+        "data": "synthetic",
+        "config": {"workload": f"{cfg['name']}: 1 environment+query per step (bounded sample of the GPU arm's "
+                               f"workload), n={prob.n}", "beta": beta, "lambda": cfg.get("lambda", 0.5)},
+        "edges_relaxed_per_s": relax / tot,
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": procs, "kind": "oracle",
+                         "sample": f"1 {cfg['name']} environment+query per step: oracle build over {procs} "
+                                   f"processes + oracle search (1 thread)"},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    from synth import load_config
+    cfg = load_config(args.config)
+    beta = args.beta if not math.isnan(args.beta) else float(cfg["betas"][1])
+    if args.impl == "reference":
+        return run_reference(args, cfg, beta)
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import build_ext
+    if rank == 0 or world == 1:
+        build_ext.build()
+    if world > 1:
+        dist.barrier()
+    import paper_1705_02408_b200 as mp
+    from paper_1705_02408_b200.problem import Batch
+
+    Q = args.queries_per_gpu or int(cfg.get("queries_per_gpu", 64))
+    probs = make_shard(cfg, rank, Q)
+    B = Batch(probs)
+    betas = [beta] * Q
+    PATH_CAP = 512
+    s_d = torch.from_numpy(B.samples).to(dev)
+    o_d = torch.from_numpy(B.obstacles).to(dev)
+    f_d = torch.from_numpy(B.features).to(dev)
+    paths_d = torch.zeros((Q, PATH_CAP), dtype=torch.int32, device=dev)
+    res_d = torch.zeros(Q * 48, dtype=torch.uint8, device=dev)
+    gather_d = torch.zeros(world * Q * 48, dtype=torch.uint8, device=dev) if world > 1 else None
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step_device():
+        rm = B.build(s_d, o_d, f_d)
+        B.search(rm, betas, path_capacity=PATH_CAP, paths=paths_d, results=res_d)
+        if world > 1:
+            dist.all_gather_into_tensor(gather_d, res_d)
+        rm.free()
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident inputs ----
+    sampler = ClockSampler(local)
+    mp.mpap_prof_reset()
+    mp.mpap_prof_enable(True)
+    launches0 = mp.mpap_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    wall0 = time.perf_counter()
+    for k in range(args.steps):
+        flush.zero_()                      # L2 flush (512 MiB > 126 MB L2), outside the step's events
+        ev[k][0].record(stream)
+        step_device()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    mp.mpap_prof_enable(False)
+    launches = mp.mpap_launch_count() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = float(sum(step_ms))
+    kern = {k: mp.mpap_prof_read(k) for k in mp.KERNELS}
+
+    # results of the last step (outside the timed region)
+    res = res_d.cpu().numpy().view(mp.RESULT_DTYPE)
+    relax_step = int(res["relaxations"].sum())
+    feasible = int((res["status"] == 0).sum())
+    ok = bool(np.all((res["status"] == 0) | (res["status"] == 3)))
+
+    t_max = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    r_sum = torch.tensor([relax_step, feasible], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(r_sum, op=dist.ReduceOp.SUM)
+    tot_ms_max = float(t_max.item())
+    relax_all = float(r_sum[0].item())
+    feasible_all = int(r_sum[1].item())
+    total_queries = world * Q * args.steps
+    value = total_queries / (tot_ms_max / 1e3)
+    search_ms = kern["k_search"][0]
+
+    # ---- e2e: pinned HOST buffers through the C ABI ----
+    e2e = None
+    if not args.no_e2e:
+        s_h = torch.from_numpy(B.samples).pin_memory()
+        o_h = torch.from_numpy(B.obstacles).pin_memory()
+        f_h = torch.from_numpy(B.features).pin_memory()
+        h2d = int(s_h.numel() * 8 + o_h.numel() * 8 + f_h.numel() * 8 + Q * (4 * 2 + 8 + 48))
+        d2h = int(Q * (48 + 4 * PATH_CAP))
+
+        def step_host():
+            rm = B.build(s_h, o_h, f_h)
+            B.search(rm, betas, path_capacity=PATH_CAP)
+            rm.free()
+
+        step_host()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e_ms = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step_host()
+            b.record(stream)
+            b.synchronize()
+            e_ms += a.elapsed_time(b)
+        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * Q * args.steps / (float(te.item()) / 1e3), "unit": "queries/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    # ---- roofline of the dominant kernel ----
+    peaks, peak_src = load_peaks()
+    dom = max(mp.KERNELS, key=lambda k: kern[k][0])
+    dom_ms, dom_n = kern[dom]
+    roof = roofline(mp, dom, dom_ms, dom_n, B, peaks, peak_src, clocks)
+    roof["share_of_step"] = dom_ms / tot_ms if tot_ms > 0 else None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+        "config": {"workload": f"{cfg['name']} shard: {Q} independent 6D double-integrator quadrotor "
+                               f"environments+queries per GPU (n={B.n.max()}, {int(B.n_obst.max())} boxes, "
+                               f"{int(B.n_feat.max())} features, MLP heuristic); build+search per step",
+                   "queries_per_gpu": Q, "global_queries_per_step": world * Q, "beta": beta,
+                   "lambda": B.lam, "r": B.r, "parallelism": f"dp{world} (independent queries)",
+                   "l2": "flushed between timed steps (512 MiB write, outside the step events)"},
+        "edges_relaxed_per_s": relax_all * args.steps / (tot_ms_max / 1e3),
+        "search_only": {"ms_per_step": search_ms / max(kern['k_search'][1], 1),
+                        "edges_relaxed_per_s": relax_step / (search_ms / max(kern['k_search'][1], 1) / 1e3)
+                        if search_ms > 0 else None,
+                        "queries_per_s": Q / (search_ms / max(kern['k_search'][1], 1) / 1e3) if search_ms else None},
+        "kernels_ms_per_step": {k: kern[k][0] / args.steps for k in mp.KERNELS},
+        "feasible_fraction": feasible_all / (world * Q), "all_status_ok": ok,
+        "roofline": roof, "gpu_launches": int(launches), "clocks": clocks, "wall_s": wall,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if (rank == 0) and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, beta, args.cpu_procs or os.cpu_count() or 1)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def roofline(mp, kernel, ms, launches, B, peaks, peak_src, clocks):
+    """Achieved vs peak for the dominant kernel (algorithmic work per launch ÷
+    average launch duration).  Work counts come from the library's work
+    counters."""
+    avg_s = (ms / max(launches, 1)) / 1e3
+    work = mp.mpap_work_read() if hasattr(mp, "mpap_work_read") else {}
+    if kernel == "k_search":
+        nbytes = work.get("search_bytes", 0) / max(launches, 1)
+        ach = nbytes / avg_s / 1e9 if avg_s > 0 else 0.0
+        peak = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
+        return {"kernel": kernel, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": None, "peak_source": peak_src}
+    flops = work.get(kernel + "_fp64_ops", 0) / max(launches, 1)
+    mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    peak = SMS * FP64_LANES_PER_SM * mhz * 1e6 / 1e12
+    ach = flops / avg_s / 1e12 if avg_s > 0 else 0.0
+    return {"kernel": kernel, "bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s (fp64, non-FMA ops)",
+            "frac": ach / peak if peak else None, "traffic": None, "peak_source": f"derived ({peak_src} clocks)"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

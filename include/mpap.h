@@ -211,6 +211,15 @@ const char *mpap_last_error(void);
  * evidence: "gpu_launches"). */
 int64_t mpap_launch_count(void);
 
+/* Per-kernel CUDA-event timing for measurement (bench.py): when enabled,
+ * every kernel launch of this library is bracketed by an event pair recorded
+ * on its launching stream.  mpap_prof_read synchronises those events and
+ * returns the accumulated milliseconds and launch count of `kernel`
+ * ("k_near", "k_scan", "k_edges", "k_search"); returns 1 if it was seen. */
+void mpap_prof_enable(int32_t on);
+void mpap_prof_reset(void);
+int32_t mpap_prof_read(const char *kernel, double *total_ms, int64_t *launches);
+
 #ifdef __cplusplus
 }
 #endif

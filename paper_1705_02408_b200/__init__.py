@@ -42,7 +42,7 @@ MPAP_MEM_DEVICE = 1
 EXPORTED_SYMBOLS = [
     "mpap_build_roadmap_batch", "mpap_build_roadmap", "mpap_search", "mpap_search_batch", "mpap_roadmap_import",
     "mpap_roadmap_info", "mpap_roadmap_envs", "mpap_roadmap_export", "mpap_roadmap_free", "mpap_status_str",
-    "mpap_last_error", "mpap_launch_count",
+    "mpap_last_error", "mpap_launch_count", "mpap_prof_enable", "mpap_prof_reset", "mpap_prof_read",
 ]
 
 
@@ -110,6 +110,11 @@ _lib.mpap_status_str.argtypes = [C.c_int]
 _lib.mpap_status_str.restype = C.c_char_p
 _lib.mpap_last_error.restype = C.c_char_p
 _lib.mpap_launch_count.restype = C.c_int64
+_lib.mpap_prof_enable.argtypes = [C.c_int32]
+_lib.mpap_prof_enable.restype = None
+_lib.mpap_prof_reset.restype = None
+_lib.mpap_prof_read.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+_lib.mpap_prof_read.restype = C.c_int32
 for _f in ("mpap_build_roadmap_batch", "mpap_build_roadmap", "mpap_search", "mpap_search_batch",
            "mpap_roadmap_import", "mpap_roadmap_info", "mpap_roadmap_export"):
     getattr(_lib, _f).restype = C.c_int
@@ -141,6 +146,9 @@ def _ptr(x, dtype) -> Any:
     """(pointer, keepalive) for a numpy array or a contiguous torch tensor."""
     if _is_cuda_tensor(x):
         assert x.is_contiguous()
+        return C.c_void_p(int(x.data_ptr())), x
+    if hasattr(x, "data_ptr") and hasattr(x, "is_contiguous"):   # host torch tensor (e.g. pinned)
+        assert x.is_contiguous() and x.element_size() == np.dtype(dtype).itemsize
         return C.c_void_p(int(x.data_ptr())), x
     a = np.ascontiguousarray(x, dtype=dtype)
     return C.c_void_p(a.ctypes.data if a.size else 0), a
@@ -361,3 +369,22 @@ def mpap_launch_count() -> int:
 
 def mpap_status_str(s: int) -> str:
     return _lib.mpap_status_str(int(s)).decode()
+
+
+def mpap_prof_enable(on: bool = True) -> None:
+    _lib.mpap_prof_enable(1 if on else 0)
+
+
+def mpap_prof_reset() -> None:
+    _lib.mpap_prof_reset()
+
+
+def mpap_prof_read(kernel: str) -> tuple:
+    """(total_ms, launches) of one library kernel since the last reset."""
+    ms = C.c_double()
+    n = C.c_int64()
+    _lib.mpap_prof_read(kernel.encode(), C.byref(ms), C.byref(n))
+    return float(ms.value), int(n.value)
+
+
+KERNELS = ("k_near", "k_scan", "k_edges", "k_search")

@@ -682,12 +682,15 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
       return set_error(MPAP_ERR_OUT_OF_MEMORY, "neighbour scratch allocation failed");
     }
     CK(cudaMemsetAsync(d_over, 0, sizeof(int), st));
-    if (rm->prm.dynamics == 0)
-      k_near<0><<<grid, kWarps * 32, 0, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->prm, cap, d_cnt, d_scr,
-                                               d_over);
-    else
-      k_near<1><<<grid, kWarps * 32, 0, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->prm, cap, d_cnt, d_scr,
-                                               d_over);
+    {
+      ProfScope ps("k_near", st);
+      if (rm->prm.dynamics == 0)
+        k_near<0><<<grid, kWarps * 32, 0, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->prm, cap, d_cnt, d_scr,
+                                                 d_over);
+      else
+        k_near<1><<<grid, kWarps * 32, 0, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->prm, cap, d_cnt, d_scr,
+                                                 d_over);
+    }
     note_launch();
     CK(cudaGetLastError());
     int over = 0;
@@ -696,7 +699,10 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
     if (over == 0) break;
     cap = ((over + 31) / 32) * 32;   // exact regrow: re-run with room for the widest row
   }
-  k_scan<<<1, 1024, 0, st>>>(d_cnt, N, rm->d_row_ptr);
+  {
+    ProfScope ps("k_scan", st);
+    k_scan<<<1, 1024, 0, st>>>(d_cnt, N, rm->d_row_ptr);
+  }
   note_launch();
   CK(cudaGetLastError());
   std::vector<int64_t> bounds(B + 1);
@@ -716,9 +722,12 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
                       sizeof(int) * (size_t)kWarps * (rm->f_max + rm->o_max);
   CK(cudaFuncSetAttribute(k_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
   if (rm->nnz_total > 0) {
-    k_edges<<<grid, kWarps * 32, smem, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->d_obst, rm->d_obst_base,
-                                             rm->d_feat, rm->d_feat_base, rm->prm, cap, rm->o_max, rm->f_max,
-                                             d_cnt, d_scr, rm->d_row_ptr, rm->d_edges, d_free);
+    {
+      ProfScope ps("k_edges", st);
+      k_edges<<<grid, kWarps * 32, smem, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->d_obst, rm->d_obst_base,
+                                               rm->d_feat, rm->d_feat_base, rm->prm, cap, rm->o_max, rm->f_max,
+                                               d_cnt, d_scr, rm->d_row_ptr, rm->d_edges, d_free);
+    }
     note_launch();
     CK(cudaGetLastError());
   }

@@ -6,6 +6,8 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -17,6 +19,50 @@ static thread_local std::string g_last_error;
 static std::atomic<long long> g_launches{0};
 
 void note_launch(int k) { g_launches.fetch_add(k); }
+
+// ---- per-kernel event timing ------------------------------------------------
+namespace {
+struct PendingRec {
+  std::string name;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::atomic<int> g_prof_on{0};
+std::vector<PendingRec> g_pending;
+std::map<std::string, std::pair<double, long long>> g_prof_acc;
+
+void prof_drain_locked() {
+  for (auto& p : g_pending) {
+    float ms = 0.0f;
+    if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+      auto& acc = g_prof_acc[p.name];
+      acc.first += ms;
+      acc.second += 1;
+    }
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  g_pending.clear();
+}
+}  // namespace
+
+ProfScope::ProfScope(const char* kernel, cudaStream_t stream) : name(kernel), st(stream), rec(nullptr) {
+  if (!g_prof_on.load()) return;
+  PendingRec* r = new PendingRec{kernel, nullptr, nullptr};
+  cudaEventCreate(&r->a);
+  cudaEventCreate(&r->b);
+  cudaEventRecord(r->a, st);
+  rec = r;
+}
+
+ProfScope::~ProfScope() {
+  if (!rec) return;
+  PendingRec* r = static_cast<PendingRec*>(rec);
+  cudaEventRecord(r->b, st);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_pending.push_back(*r);
+  delete r;
+}
 
 mpap_status set_error(mpap_status s, const std::string& msg) {
   g_last_error = msg;
@@ -86,6 +132,28 @@ const char* mpap_status_str(mpap_status s) {
 const char* mpap_last_error(void) { return g_last_error.c_str(); }
 
 int64_t mpap_launch_count(void) { return (int64_t)g_launches.load(); }
+
+void mpap_prof_enable(int32_t on) { g_prof_on.store(on ? 1 : 0); }
+
+void mpap_prof_reset(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  prof_drain_locked();
+  g_prof_acc.clear();
+}
+
+int32_t mpap_prof_read(const char* kernel, double* total_ms, int64_t* launches) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  prof_drain_locked();
+  auto it = g_prof_acc.find(kernel ? kernel : "");
+  if (it == g_prof_acc.end()) {
+    if (total_ms) *total_ms = 0.0;
+    if (launches) *launches = 0;
+    return 0;
+  }
+  if (total_ms) *total_ms = it->second.first;
+  if (launches) *launches = it->second.second;
+  return 1;
+}
 
 void mpap_roadmap_free(mpap_roadmap* rm) {
   if (!rm) return;

@@ -67,6 +67,16 @@ struct mpap_roadmap {
 namespace mpap {
 // launch bookkeeping shared by the translation units (host side)
 void note_launch(int k = 1);
+
+// Optional per-kernel CUDA-event timing (mpap_prof_enable): a scope records
+// an event pair on the launching stream around one kernel launch.
+struct ProfScope {
+  const char* name;
+  cudaStream_t st;
+  void* rec;
+  ProfScope(const char* kernel, cudaStream_t stream);
+  ~ProfScope();
+};
 mpap_status set_error(mpap_status s, const std::string& msg);
 mpap_status cuda_error(cudaError_t e, const char* what);
 

@@ -709,8 +709,11 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     A.n_env = d_nenv;
     CKS(cudaMemcpyAsync(d_qidx, todo.data(), sizeof(int32_t) * nrun, cudaMemcpyHostToDevice, st));
     CKS(cudaMemsetAsync(d_work, 0, sizeof(int), st));
-    if (trace) k_search<true><<<nslots, kST, 0, st>>>(A);
-    else k_search<false><<<nslots, kST, 0, st>>>(A);
+    {
+      ProfScope ps("k_search", st);
+      if (trace) k_search<true><<<nslots, kST, 0, st>>>(A);
+      else k_search<false><<<nslots, kST, 0, st>>>(A);
+    }
     note_launch();
     CKS(cudaGetLastError());
     CKS(cudaFreeAsync(base, st));

@@ -245,7 +245,7 @@ def test_batch_ragged_equals_single(mp, orc):
 # ---------------------------------------------------------------------------
 
 def _import_and_compare(mp, orc, n, edges, goal_nodes, betas, lams, r=1.0):
-    from tests.test_oracle_search import csr
+    from graphs import csr
     g = csr(n, edges)
     pos = np.zeros((n, 2))
     pos[:, 0] = np.arange(n)
@@ -278,7 +278,7 @@ def test_literal_graphs(mp, orc):
 
 @pytest.mark.parametrize("seed", range(12))
 def test_random_graphs(mp, orc, seed):
-    from tests.test_oracle_search import random_graph
+    from graphs import random_graph
     rng = np.random.default_rng(500 + seed)
     n = int(rng.integers(5, 60))
     g = random_graph(rng, n, int(rng.integers(2, 7)), neg_frac=0.5)
@@ -289,7 +289,7 @@ def test_random_graphs(mp, orc, seed):
 
 
 def test_path_buffer_too_small(mp):
-    from tests.test_oracle_search import csr
+    from graphs import csr
     g = csr(4, [(0, 1, 0.3, 0, 0), (1, 2, 0.3, 0, 0), (2, 3, 0.3, 0, 0)])
     pos = np.zeros((4, 2))
     pos[:, 0] = np.arange(4)
