@@ -196,12 +196,23 @@ mpap_status mpap_roadmap_info(const mpap_roadmap *rm, int32_t env, int32_t *n, i
                               int64_t *nnz_free);
 int32_t mpap_roadmap_envs(const mpap_roadmap *rm);
 
+/* Work counters of the build that produced `rm` (summed over its envs),
+ * counted by the kernels themselves; bench.py turns them into algorithmic
+ * FP64 operation counts.  Index: 0 pairs scanned, 1 pairs
+ * passing the double-integrator prefilter, 2 bisection iterations, 3 r-disc
+ * edges, 4 collision segments, 5 collision slab tests, 6 heuristic steps,
+ * 7 feature range tests, 8 FOV tests, 9 occlusion segments, 10 occlusion slab
+ * tests, 11 MLP evaluations, 12 collision-free edges, 13 culling tests.
+ * Writes min(n, 16) counters, zero-fills the rest. */
+mpap_status mpap_roadmap_work(const mpap_roadmap *rm, uint64_t *counters, int32_t n);
+
 /* Copy env's CSR to host buffers (parity/debug): row_ptr[n+1] (local edge
  * offsets), dst_coll[nnz] = dst | coll << 31, w, s, c [nnz] (f32). */
 mpap_status mpap_roadmap_export(const mpap_roadmap *rm, int32_t env, int32_t *row_ptr,
                                 uint32_t *dst_coll, float *w, float *s, float *c);
 
-/* Releases the roadmap's device memory (NULL is a no-op). */
+/* Releases the roadmap's device memory (NULL is a no-op).  Waits for the
+ * device to be idle first (searches of this roadmap may be in flight). */
 void mpap_roadmap_free(mpap_roadmap *rm);
 
 const char *mpap_status_str(mpap_status s);

@@ -43,6 +43,7 @@ EXPORTED_SYMBOLS = [
     "mpap_build_roadmap_batch", "mpap_build_roadmap", "mpap_search", "mpap_search_batch", "mpap_roadmap_import",
     "mpap_roadmap_info", "mpap_roadmap_envs", "mpap_roadmap_export", "mpap_roadmap_free", "mpap_status_str",
     "mpap_last_error", "mpap_launch_count", "mpap_prof_enable", "mpap_prof_reset", "mpap_prof_read",
+    "mpap_roadmap_work",
 ]
 
 
@@ -101,6 +102,8 @@ _lib.mpap_search_batch.argtypes = [_vp, C.c_int32, _i32p, _i32p, C.POINTER(mpap_
 _lib.mpap_roadmap_import.argtypes = [C.c_int32, C.c_int32, _vp, _i32p, _vp, _vp, _vp, _vp, C.c_double, _vp,
                                      C.POINTER(_vp)]
 _lib.mpap_roadmap_info.argtypes = [_vp, C.c_int32, _i32p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+_lib.mpap_roadmap_work.argtypes = [_vp, C.POINTER(C.c_uint64), C.c_int32]
+_lib.mpap_roadmap_work.restype = C.c_int
 _lib.mpap_roadmap_envs.argtypes = [_vp]
 _lib.mpap_roadmap_envs.restype = C.c_int32
 _lib.mpap_roadmap_export.argtypes = [_vp, C.c_int32, _i32p, _vp, _vp, _vp, _vp]
@@ -388,3 +391,16 @@ def mpap_prof_read(kernel: str) -> tuple:
 
 
 KERNELS = ("k_near", "k_scan", "k_edges", "k_search")
+
+
+WORK_FIELDS = ["pairs", "prefilter_pass", "bisect_iters", "edges", "coll_segs", "coll_box_tests", "steps",
+               "range_tests", "fov_tests", "occl_segs", "occl_box_tests", "mlp", "free_edges", "cull_tests"]
+
+
+def mpap_roadmap_work(rm: Roadmap) -> dict:
+    """Build work counters of a roadmap (counted by the kernels)."""
+    a = (C.c_uint64 * 16)()
+    s = _lib.mpap_roadmap_work(rm.handle, a, 16)
+    if s != MPAP_OK:
+        raise MpapError(s, "mpap_roadmap_work")
+    return {k: int(a[i]) for i, k in enumerate(WORK_FIELDS)}

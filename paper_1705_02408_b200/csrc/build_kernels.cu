@@ -14,14 +14,16 @@
 //   k_edges  one warp per row, one edge at a time: Collision(u,v) (P:190,
 //            A2.5 P:215; reading R8) with lanes over polyline segments, then
 //            the heuristic summary (R9, R10, R12) with lanes over timesteps;
-//            per edge the warp culls features/boxes against the bounding box
-//            of its sample points (exact: a culled item provably fails its
+//            per 32-step chunk the warp culls features/boxes against the
+//            chunk's bounding box (exact: a culled item provably fails its
 //            test), and folds the per-step increments in time
 //            order with shuffles.  Writes the 16-byte EdgeRec.
 //
-// Every floating-point expression follows DESIGN.md §3 ("Numeric contract")
-// operation by operation and is compiled with --fmad=false (no contraction),
-// so results are bit-identical to the CPU oracle without sharing its code.
+// The position dimension D (2 or 3) and the dynamics are template parameters
+// so every per-axis array lives in registers.  Every floating-point
+// expression follows DESIGN.md §3 ("Numeric contract") operation by operation
+// and is compiled with --fmad=false (no contraction), so results are
+// bit-identical to the CPU oracle without sharing its code.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -45,12 +47,12 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // ---------------------------------------------------------------------------
 // geometry (DESIGN.md §3 "slab")
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ bool seg_box(const double* A, const double* B, const double* box, int d) {
+template <int D>
+__device__ __forceinline__ bool seg_box(const double* A, const double* B, const double* box) {
   double t0 = 0.0, t1 = 1.0;
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    if (k >= d) break;
-    const double lo = box[k], hi = box[d + k];
+  for (int k = 0; k < D; ++k) {
+    const double lo = box[k], hi = box[D + k];
     const double dk = B[k] - A[k];
     if (dk == 0.0) {
       if (A[k] < lo || A[k] > hi) return false;
@@ -67,10 +69,13 @@ __device__ __forceinline__ bool seg_box(const double* A, const double* B, const 
   return true;
 }
 
+template <int D>
 __device__ __forceinline__ bool outside_ws(const double* p, const DevParams& P) {
-  for (int k = 0; k < P.pos_dim; ++k)
-    if (p[k] < P.ws_lo[k] || p[k] > P.ws_hi[k]) return true;
-  return false;
+  bool out = false;
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+    if (p[k] < P.ws_lo[k] || p[k] > P.ws_hi[k]) out = true;
+  return out;
 }
 
 // ---------------------------------------------------------------------------
@@ -78,10 +83,12 @@ __device__ __forceinline__ bool outside_ws(const double* p, const DevParams& P) 
 // ---------------------------------------------------------------------------
 struct DiCoef { double vv, av, aa, B, C, D, ru; };
 
-__device__ __forceinline__ void di_coefs(const double* su, const double* sv, int d, double ru, DiCoef& k) {
+template <int D>
+__device__ __forceinline__ void di_coefs(const double* su, const double* sv, double ru, DiCoef& k) {
   double vv = 0.0, av = 0.0, aa = 0.0;
-  for (int j = 0; j < d; ++j) {
-    const double p0 = su[j], v0 = su[d + j], p1 = sv[j], v1 = sv[d + j];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const double p0 = su[j], v0 = su[D + j], p1 = sv[j], v1 = sv[D + j];
     const double a = p1 - p0;
     vv = vv + ((v0 * v0 + v0 * v1) + v1 * v1);
     av = av + a * (v0 + v1);
@@ -107,21 +114,23 @@ template <int WHICH>
 __device__ __forceinline__ double di_f(const DiCoef& k, double t) { return WHICH == 0 ? di_q(k, t) : di_qp(k, t); }
 
 template <int WHICH>
-__device__ double di_bisect(const DiCoef& k, double lo, double hi) {
+__device__ double di_bisect(const DiCoef& k, double lo, double hi, unsigned& iters) {
   const bool hi_pos = di_f<WHICH>(k, hi) > 0.0;
   for (int it = 0; it < 100; ++it) {
     const double mid = lo + 0.5 * (hi - lo);
     if (!(mid > lo && mid < hi)) break;
+    ++iters;
     if ((di_f<WHICH>(k, mid) > 0.0) == hi_pos) hi = mid; else lo = mid;
   }
   return hi;
 }
 
 // Returns true and (c*, tau*) when c has a local minimiser on (0, r].
-__device__ bool cost_di(const double* su, const double* sv, int d, double ru, double r, double& c_out,
-                        double& tau_out) {
+template <int D>
+__device__ bool cost_di(const double* su, const double* sv, double ru, double r, double& c_out, double& tau_out,
+                        unsigned& iters) {
   DiCoef k;
-  di_coefs(su, sv, d, ru, k);
+  di_coefs<D>(su, sv, ru, k);
   if (k.D == 0.0) return false;
   double bp[4];
   int nb = 0;
@@ -135,7 +144,7 @@ __device__ bool cost_di(const double* su, const double* sv, int d, double ru, do
   for (int s = 0; s + 1 < np; ++s) {
     const double a = pieces[s], b = pieces[s + 1];
     const double fa = di_qp(k, a), fb = di_qp(k, b);
-    if ((fa > 0.0 && fb < 0.0) || (fa < 0.0 && fb > 0.0)) bp[nb++] = di_bisect<1>(k, a, b);
+    if ((fa > 0.0 && fb < 0.0) || (fa < 0.0 && fb > 0.0)) bp[nb++] = di_bisect<1>(k, a, b, iters);
   }
   bp[nb++] = r;
   for (int i = 1; i < nb; ++i) {  // ascending already; kept for the contract
@@ -150,7 +159,7 @@ __device__ bool cost_di(const double* su, const double* sv, int d, double ru, do
     const double a = bp[s], b = bp[s + 1];
     if (!(b > a)) continue;
     if (di_q(k, a) <= 0.0 && di_q(k, b) > 0.0) {
-      const double t = di_bisect<0>(k, a, b);
+      const double t = di_bisect<0>(k, a, b, iters);
       const double c = di_c(k, t);
       if (!found || c < best_c || (c == best_c && t < best_t)) { found = true; best_c = c; best_t = t; }
     }
@@ -161,37 +170,48 @@ __device__ bool cost_di(const double* su, const double* sv, int d, double ru, do
   return true;
 }
 
-__device__ __forceinline__ void di_traj(const double* su, const double* sv, int d, double tau, double* c2,
-                                        double* c3) {
+template <int D>
+__device__ __forceinline__ void di_traj(const double* su, const double* sv, double tau, double* c2, double* c3) {
   const double tau2 = tau * tau;
   const double tau3 = tau2 * tau;
-  for (int j = 0; j < d; ++j) {
-    const double dp = (sv[j] - su[j]) - su[d + j] * tau;
-    const double dl = sv[d + j] - su[d + j];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const double dp = (sv[j] - su[j]) - su[D + j] * tau;
+    const double dl = sv[D + j] - su[D + j];
     c2[j] = (3.0 * dp - dl * tau) / tau2;
     c3[j] = (dl * tau - 2.0 * dp) / tau3;
   }
 }
 
-__device__ __forceinline__ void di_pos(const double* su, const double* c2, const double* c3, int d, double t,
-                                       double* x) {
-  for (int j = 0; j < d; ++j) x[j] = su[j] + t * (su[d + j] + t * (c2[j] + t * c3[j]));
+template <int D>
+__device__ __forceinline__ void di_pos(const double* su, const double* c2, const double* c3, double t, double* x) {
+#pragma unroll
+  for (int j = 0; j < D; ++j) x[j] = su[j] + t * (su[D + j] + t * (c2[j] + t * c3[j]));
 }
 
-__device__ __forceinline__ void di_vel(const double* su, const double* c2, const double* c3, int d, double t,
-                                       double* v) {
-  for (int j = 0; j < d; ++j) v[j] = su[d + j] + t * (2.0 * c2[j] + t * (3.0 * c3[j]));
+template <int D>
+__device__ __forceinline__ void di_vel(const double* su, const double* c2, const double* c3, double t, double* v) {
+#pragma unroll
+  for (int j = 0; j < D; ++j) v[j] = su[D + j] + t * (2.0 * c2[j] + t * (3.0 * c3[j]));
 }
+
+// Work counters (always on; one atomicAdd per row per counter).
+enum {
+  W_PAIRS = 0, W_PREFILTER_PASS, W_BISECT_ITERS, W_EDGES, W_COLL_SEGS, W_COLL_BOX_TESTS, W_STEPS, W_RANGE_TESTS,
+  W_FOV_TESTS, W_OCCL_SEGS, W_OCCL_BOX_TESTS, W_MLP, W_FREE_EDGES, W_CULL_TESTS, W_NUM
+};
 
 // ---------------------------------------------------------------------------
 // k_near
 // ---------------------------------------------------------------------------
-template <int DYN>
+template <int D, int DYN>
 __global__ void __launch_bounds__(kWarps * 32) k_near(const double* __restrict__ samples,
                                                       const int64_t* __restrict__ node_base,
                                                       const int32_t* __restrict__ n_env, DevParams P, int cap,
                                                       int32_t* __restrict__ cnt, NearRec* __restrict__ scratch,
-                                                      int* __restrict__ overflow) {
+                                                      int* __restrict__ overflow,
+                                                      unsigned long long* __restrict__ work) {
+  constexpr int NS = DYN ? 2 * D : D;   // state doubles used by the cost
   __shared__ int queue[kWarps][64];
   const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -199,15 +219,16 @@ __global__ void __launch_bounds__(kWarps * 32) k_near(const double* __restrict__
   const int u = blockIdx.x * kWarps + warp;
   if (u >= nb) return;  // warp-uniform
   const int64_t row = node_base[b] + u;
-  const int d = P.pos_dim;
   const int stride = P.stride;
   const double* envs = samples + node_base[b] * stride;
-  double su[6];
-  for (int j = 0; j < 2 * d && j < 6; ++j) su[j] = (j < d || DYN == 1) ? envs[(int64_t)u * stride + j] : 0.0;
+  double su[NS];
+#pragma unroll
+  for (int j = 0; j < NS; ++j) su[j] = envs[(int64_t)u * stride + j];
   NearRec* out = scratch + row * (int64_t)cap;
   const double r = P.r;
   const unsigned lt = lanemask_lt();
   int count = 0;
+  unsigned n_pass = 0, n_iter = 0;
   if (DYN == 0) {
     for (int v0 = 0; v0 < nb; v0 += 32) {
       const int v = v0 + lane;
@@ -216,7 +237,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_near(const double* __restrict__
       if (v < nb && v != u) {
         const double* sv = envs + (int64_t)v * stride;
         double acc = 0.0;
-        for (int k = 0; k < d; ++k) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
           const double dk = sv[k] - su[k];
           acc = acc + dk * dk;
         }
@@ -233,7 +255,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_near(const double* __restrict__
   } else {
     const double ru = P.control_weight;
     double v02 = 0.0;
-    for (int j = 0; j < d; ++j) v02 += su[d + j] * su[d + j];
+#pragma unroll
+    for (int j = 0; j < D; ++j) v02 += su[D + j] * su[D + j];
     const double bp = (sqrt(v02) * r + r * r / sqrt(3.0 * ru)) * (1.0 + 1e-9);
     const double bv = (r / sqrt(ru)) * (1.0 + 1e-9);
     const double bp2 = bp * bp, bv2 = bv * bv;
@@ -244,10 +267,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_near(const double* __restrict__
       int v = -1;
       if (lane < k) {
         v = queue[warp][lane];
-        double sv[6];
+        double sv[NS];
         const double* svp = envs + (int64_t)v * stride;
-        for (int j = 0; j < 2 * d; ++j) sv[j] = svp[j];
-        ok = cost_di(su, sv, d, ru, r, c, tau) && (c < r);
+#pragma unroll
+        for (int j = 0; j < NS; ++j) sv[j] = svp[j];
+        ++n_pass;
+        ok = cost_di<D>(su, sv, ru, r, c, tau, n_iter) && (c < r);
       }
       const unsigned m = __ballot_sync(FULL, ok);
       if (ok) {
@@ -262,8 +287,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_near(const double* __restrict__
       if (v < nb && v != u) {
         const double* sv = envs + (int64_t)v * stride;
         double dp2 = 0.0, dv2 = 0.0;
-        for (int j = 0; j < d; ++j) {
-          const double a = sv[j] - su[j], e = sv[d + j] - su[d + j];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const double a = sv[j] - su[j], e = sv[D + j] - su[D + j];
           dp2 += a * a;
           dv2 += e * e;
         }
@@ -290,6 +316,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_near(const double* __restrict__
     cnt[row] = count;
     if (count > cap) atomicMax(overflow, count);
   }
+  for (int o = 16; o > 0; o >>= 1) {
+    n_pass += __shfl_xor_sync(FULL, n_pass, o);
+    n_iter += __shfl_xor_sync(FULL, n_iter, o);
+  }
+  if (lane == 0) {
+    atomicAdd(&work[W_PAIRS], (unsigned long long)(nb - 1));
+    if (n_pass) atomicAdd(&work[W_PREFILTER_PASS], (unsigned long long)n_pass);
+    if (n_iter) atomicAdd(&work[W_BISECT_ITERS], (unsigned long long)n_iter);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -303,7 +338,6 @@ __global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ cnt, 
   const int64_t lo = t * chunk, hi = min(N, lo + chunk);
   int64_t s = 0;
   for (int64_t i = lo; i < hi; ++i) s += cnt[i];
-  // block exclusive scan of s
   const int lane = t & 31, w = t >> 5;
   int64_t x = s;
   for (int o = 1; o < 32; o <<= 1) {
@@ -333,10 +367,14 @@ __global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ cnt, 
 // k_edges: collision + heuristic summary per edge
 // ---------------------------------------------------------------------------
 struct EdgeSmem {
-  double* box;   // [O][2d]
-  double* feat;  // [F][d]
-  int* flist;    // [kWarps][F]
-  int* blist;    // [kWarps][O]
+  double* box;   // [O][2D]
+  double* feat;  // [F][D]
+  int* flist;    // per warp [F]
+  int* blist;    // per warp [O]
+};
+
+struct Work {
+  unsigned v[W_NUM];
 };
 
 __device__ __forceinline__ double warp_min(double x) {
@@ -349,7 +387,10 @@ __device__ __forceinline__ double warp_max(double x) {
 }
 
 // Boxes overlapping [lo - m, hi + m] -> per-warp list; returns the count.
-__device__ int cull_boxes(const double* box, int O, int d, const double* lo, const double* hi, double m, int* list,
+// A box outside that region cannot be hit by any segment inside [lo, hi]
+// (its slab interval is empty by a margin far above rounding).
+template <int D>
+__device__ int cull_boxes(const double* box, int O, const double* lo, const double* hi, double m, int* list,
                           int lane) {
   int nc = 0;
   const unsigned lt = lanemask_lt();
@@ -359,9 +400,10 @@ __device__ int cull_boxes(const double* box, int O, int d, const double* lo, con
     bool keep = false;
     if (o < O) {
       keep = true;
-      const double* bx = box + (size_t)o * 2 * d;
-      for (int k = 0; k < d; ++k)
-        if (bx[k] > hi[k] + m || bx[d + k] < lo[k] - m) keep = false;
+      const double* bx = box + (size_t)o * 2 * D;
+#pragma unroll
+      for (int k = 0; k < D; ++k)
+        if (bx[k] > hi[k] + m || bx[D + k] < lo[k] - m) keep = false;
     }
     const unsigned msk = __ballot_sync(FULL, keep);
     if (keep) list[nc + __popc(msk & lt)] = o;
@@ -371,44 +413,90 @@ __device__ int cull_boxes(const double* box, int O, int d, const double* lo, con
   return nc;
 }
 
-__device__ __forceinline__ bool seg_hits_list(const double* A, const double* B, const double* box, const int* list,
-                                              int nl, int d) {
-  for (int i = 0; i < nl; ++i)
-    if (seg_box(A, B, box + (size_t)list[i] * 2 * d, d)) return true;
+// Does the closed segment [A, B] (Dv = B - A) hit one of the listed boxes?
+// The slab test of DESIGN.md §3 with the per-axis reciprocal 1/Dv_k computed
+// once per segment (the value the per-box formula computes); a box separated
+// from the segment's bounding box by more than kCullMargin is skipped (its
+// slab test is provably false).  `tests` counts the slab tests executed.
+template <int D>
+__device__ __forceinline__ bool seg_hits_boxes(const double* A, const double* B, const double* Dv,
+                                               const double* box, const int* list, int nl, unsigned& tests) {
+  double inv[D], slo[D], shi[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    inv[k] = (Dv[k] != 0.0) ? 1.0 / Dv[k] : 0.0;
+    slo[k] = fmin(A[k], B[k]) - kCullMargin;
+    shi[k] = fmax(A[k], B[k]) + kCullMargin;
+  }
+  for (int i = 0; i < nl; ++i) {
+    const double* bx = box + (size_t)list[i] * 2 * D;
+    bool sep = false;
+#pragma unroll
+    for (int k = 0; k < D; ++k)
+      if (bx[k] > shi[k] || bx[D + k] < slo[k]) sep = true;
+    if (sep) continue;
+    ++tests;
+    double t0 = 0.0, t1 = 1.0;
+    bool hit = true;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const double lo = bx[k], hi = bx[D + k];
+      if (Dv[k] == 0.0) {
+        if (A[k] < lo || A[k] > hi) hit = false;
+      } else {
+        double ta = (lo - A[k]) * inv[k];
+        double tb = (hi - A[k]) * inv[k];
+        if (ta > tb) { const double tmp = ta; ta = tb; tb = tmp; }
+        if (ta > t0) t0 = ta;
+        if (tb < t1) t1 = tb;
+        if (t0 > t1) hit = false;
+      }
+    }
+    if (hit) return true;
+  }
   return false;
 }
 
 // Collision(u,v) of reading R8, warp-cooperative; every lane returns the result.
+template <int D, int DYN>
 __device__ bool edge_collision(const DevParams& P, const double* su, const double* sv, double tau,
-                               const EdgeSmem& S, int O, int lane) {
-  const int d = P.pos_dim;
-  if (P.dynamics == 0) {
+                               const EdgeSmem& S, int O, int lane, Work& W) {
+  if (DYN == 0) {
     bool hit = false;
     for (int o0 = 0; o0 < O; o0 += 32) {
       const int o = o0 + lane;
-      if (o < O && seg_box(su, sv, S.box + (size_t)o * 2 * d, d)) hit = true;
+      if (o < O) {
+        ++W.v[W_COLL_BOX_TESTS];
+        if (seg_box<D>(su, sv, S.box + (size_t)o * 2 * D)) hit = true;
+      }
       if (__any_sync(FULL, hit)) return true;
     }
+    if (lane == 0) ++W.v[W_COLL_SEGS];
     return false;
   }
-  double c2[3], c3[3];
-  di_traj(su, sv, d, tau, c2, c3);
+  double c2[D], c3[D];
+  di_traj<D>(su, sv, tau, c2, c3);
   const double kc = ceil(tau / P.collision_dt);
   const int Kc = (kc < 1.0) ? 1 : (int)kc;
   // bounding box of the polyline vertices P_0..P_Kc
-  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  double lo[D], hi[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) { lo[j] = 1e300; hi[j] = -1e300; }
   bool out = false;
   for (int k = lane; k <= Kc; k += 32) {
     const double t = (k == 0) ? 0.0 : ((double)k * tau) / (double)Kc;
-    double x[3];
-    di_pos(su, c2, c3, d, t, x);
-    if (outside_ws(x, P)) out = true;
-    for (int j = 0; j < d; ++j) { lo[j] = fmin(lo[j], x[j]); hi[j] = fmax(hi[j], x[j]); }
+    double x[D];
+    di_pos<D>(su, c2, c3, t, x);
+    if (outside_ws<D>(x, P)) out = true;
+#pragma unroll
+    for (int j = 0; j < D; ++j) { lo[j] = fmin(lo[j], x[j]); hi[j] = fmax(hi[j], x[j]); }
   }
   if (__any_sync(FULL, out)) return true;
-  for (int j = 0; j < d; ++j) { lo[j] = warp_min(lo[j]); hi[j] = warp_max(hi[j]); }
+#pragma unroll
+  for (int j = 0; j < D; ++j) { lo[j] = warp_min(lo[j]); hi[j] = warp_max(hi[j]); }
   int* list = S.blist;
-  const int nl = cull_boxes(S.box, O, d, lo, hi, kCullMargin, list, lane);
+  const int nl = cull_boxes<D>(S.box, O, lo, hi, kCullMargin, list, lane);
+  if (lane == 0) W.v[W_CULL_TESTS] += O;
   if (nl == 0) return false;
   for (int k0 = 1; k0 <= Kc; k0 += 32) {
     const int k = k0 + lane;
@@ -416,10 +504,15 @@ __device__ bool edge_collision(const DevParams& P, const double* su, const doubl
     if (k <= Kc) {
       const double ta = (k - 1 == 0) ? 0.0 : ((double)(k - 1) * tau) / (double)Kc;
       const double tb = ((double)k * tau) / (double)Kc;
-      double A[3], B[3];
-      di_pos(su, c2, c3, d, ta, A);
-      di_pos(su, c2, c3, d, tb, B);
-      hit = seg_hits_list(A, B, S.box, list, nl, d);
+      double A[D], B[D], Dv[D];
+      di_pos<D>(su, c2, c3, ta, A);
+      di_pos<D>(su, c2, c3, tb, B);
+#pragma unroll
+      for (int j = 0; j < D; ++j) Dv[j] = B[j] - A[j];
+      ++W.v[W_COLL_SEGS];
+      unsigned t = 0;
+      hit = seg_hits_boxes<D>(A, B, Dv, S.box, list, nl, t);
+      W.v[W_COLL_BOX_TESTS] += t;
     }
     if (__any_sync(FULL, hit)) return true;
   }
@@ -455,108 +548,126 @@ __device__ __forceinline__ double mlp_out0(const DevParams& P, double z0, double
   return o;
 }
 
-// Heuristic summary (s, c) of reading R10 for a collision-free edge.
+// Heuristic summary (s, c) of reading R10 for a collision-free edge.  Steps
+// are processed 32 at a time (one per lane); per chunk the warp culls the
+// features within range of the chunk's bounding box and the boxes that can
+// occlude a sight line from it, then every lane counts its visible features
+// and the increments are folded in time order with shuffles.
+template <int D, int DYN>
 __device__ void edge_heuristic(const DevParams& P, const double* su, const double* sv, double T, const EdgeSmem& S,
-                               int O, int F, int lane, double& s_out, double& c_out) {
-  const int d = P.pos_dim;
+                               int O, int F, int lane, double& s_out, double& c_out, Work& W) {
   const double kk = ceil(T / P.dt);
   const int K = (kk < 1.0) ? 1 : (int)kk;
   const double Dl = T / (double)K;
-  double c2[3] = {0, 0, 0}, c3[3] = {0, 0, 0};
-  if (P.dynamics == 1) di_traj(su, sv, d, T, c2, c3);
+  double c2[D], c3[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) { c2[j] = 0.0; c3[j] = 0.0; }
+  if (DYN == 1) di_traj<D>(su, sv, T, c2, c3);
   const int hoff = P.hoff;
   double omega = 0.0;
+  double hu0 = 0.0, hu1 = 0.0, hv0 = 0.0, hv1 = 0.0;
   if (P.has_heading) {
-    const double ex = sv[hoff] - su[hoff], ey = sv[hoff + 1] - su[hoff + 1];
+    hu0 = su[hoff]; hu1 = su[hoff + 1]; hv0 = sv[hoff]; hv1 = sv[hoff + 1];
+    const double ex = hv0 - hu0, ey = hv1 - hu1;
     omega = sqrt(ex * ex + ey * ey) / T;
   }
-  // bounding box of the step positions
-  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-  for (int k = lane; k < K; k += 32) {
-    const double t = (double)k * Dl;
-    double x[3];
-    if (P.dynamics == 0) {
-      const double s = t / T;
-      for (int j = 0; j < d; ++j) x[j] = su[j] + s * (sv[j] - su[j]);
-    } else {
-      di_pos(su, c2, c3, d, t, x);
-    }
-    for (int j = 0; j < d; ++j) { lo[j] = fmin(lo[j], x[j]); hi[j] = fmax(hi[j], x[j]); }
-  }
-  for (int j = 0; j < d; ++j) { lo[j] = warp_min(lo[j]); hi[j] = warp_max(hi[j]); }
   const double R = P.max_range;
   const double m = R + kCullMargin;
-  // features within R (+margin) of the box, per axis
-  int nf = 0;
-  {
-    const unsigned lt = lanemask_lt();
+  const double R2 = R * R;
+  const double cos2 = P.fov_cos_half * P.fov_cos_half;
+  const int heur = P.heuristic;
+  const unsigned lt = lanemask_lt();
+  double s = 0.0, c = 0.0;
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    const int k = k0 + lane;
+    const bool act = k < K;
+    double x[D], hv[D], vel[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) { x[j] = 0.0; hv[j] = 0.0; vel[j] = 0.0; }
+    const double t = (double)k * Dl;
+    if (act) {
+      if (DYN == 0) {
+        const double sp = t / T;
+#pragma unroll
+        for (int j = 0; j < D; ++j) x[j] = su[j] + sp * (sv[j] - su[j]);
+      } else {
+        di_pos<D>(su, c2, c3, t, x);
+        di_vel<D>(su, c2, c3, t, vel);
+      }
+      if (heur == 1) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) hv[j] = (DYN == 1) ? vel[j] : sv[j] - su[j];
+      } else if (heur >= 2) {
+        const double sp = t / T;
+        hv[0] = (1.0 - sp) * hu0 + sp * hv0;
+        hv[1] = (1.0 - sp) * hu1 + sp * hv1;
+      }
+    }
+    // chunk bounding box -> culled features and occluders
+    double lo[D], hi[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      lo[j] = warp_min(act ? x[j] : 1e300);
+      hi[j] = warp_max(act ? x[j] : -1e300);
+    }
+    int nf = 0;
     __syncwarp();
     for (int f0 = 0; f0 < F; f0 += 32) {
       const int f = f0 + lane;
       bool keep = false;
       if (f < F) {
         keep = true;
-        const double* fp = S.feat + (size_t)f * d;
-        for (int k = 0; k < d; ++k)
-          if (fp[k] > hi[k] + m || fp[k] < lo[k] - m) keep = false;
+        const double* fp = S.feat + (size_t)f * D;
+#pragma unroll
+        for (int q = 0; q < D; ++q)
+          if (fp[q] > hi[q] + m || fp[q] < lo[q] - m) keep = false;
       }
       const unsigned msk = __ballot_sync(FULL, keep);
       if (keep) S.flist[nf + __popc(msk & lt)] = f;
       nf += __popc(msk);
     }
     __syncwarp();
-  }
-  const int nb = (nf > 0) ? cull_boxes(S.box, O, d, lo, hi, m, S.blist, lane) : 0;
-  const double R2 = R * R;
-  const double cos2 = P.fov_cos_half * P.fov_cos_half;
-  double s = 0.0, c = 0.0;
-  for (int k0 = 0; k0 < K; k0 += 32) {
-    const int k = k0 + lane;
+    const int nb = (nf > 0) ? cull_boxes<D>(S.box, O, lo, hi, m, S.blist, lane) : 0;
+    if (lane == 0) W.v[W_CULL_TESTS] += F + (nf > 0 ? O : 0);
     double inc = 0.0;
-    if (k < K) {
-      const double t = (double)k * Dl;
-      double x[3] = {0, 0, 0}, hv[3] = {0, 0, 0}, vel[3] = {0, 0, 0};
-      if (P.dynamics == 0) {
-        const double sp = t / T;
-        for (int j = 0; j < d; ++j) x[j] = su[j] + sp * (sv[j] - su[j]);
-      } else {
-        di_pos(su, c2, c3, d, t, x);
-        di_vel(su, c2, c3, d, t, vel);
-      }
-      if (P.heuristic == 1) {
-        if (P.dynamics == 1) { for (int j = 0; j < d; ++j) hv[j] = vel[j]; }
-        else { for (int j = 0; j < d; ++j) hv[j] = sv[j] - su[j]; }
-      } else if (P.heuristic >= 2) {
-        const double sp = t / T;
-        hv[0] = (1.0 - sp) * su[hoff] + sp * sv[hoff];
-        hv[1] = (1.0 - sp) * su[hoff + 1] + sp * sv[hoff + 1];
-        hv[2] = 0.0;
-      }
+    if (act) {
+      ++W.v[W_STEPS];
       double hh = 0.0;
-      for (int j = 0; j < d; ++j) hh = hh + hv[j] * hv[j];
+#pragma unroll
+      for (int j = 0; j < D; ++j) hh = hh + hv[j] * hv[j];
       int kv = 0;
       for (int i = 0; i < nf; ++i) {
-        const double* fp = S.feat + (size_t)S.flist[i] * d;
-        double dl[3];
+        const double* fp = S.feat + (size_t)S.flist[i] * D;
+        double dl[D];
         double dd = 0.0;
-        for (int j = 0; j < d; ++j) { dl[j] = fp[j] - x[j]; dd = dd + dl[j] * dl[j]; }
+#pragma unroll
+        for (int j = 0; j < D; ++j) { dl[j] = fp[j] - x[j]; dd = dd + dl[j] * dl[j]; }
+        ++W.v[W_RANGE_TESTS];
         if (dd > R2) continue;
-        if (P.heuristic != 0) {
+        if (heur != 0) {
+          ++W.v[W_FOV_TESTS];
           double dot = 0.0;
-          for (int j = 0; j < d; ++j) dot = dot + hv[j] * dl[j];
+#pragma unroll
+          for (int j = 0; j < D; ++j) dot = dot + hv[j] * dl[j];
           if (!(hh > 0.0)) continue;
           if (dot < 0.0) continue;
           if (dot * dot < cos2 * (hh * dd)) continue;
         }
-        if (seg_hits_list(x, fp, S.box, S.blist, nb, d)) continue;
+        ++W.v[W_OCCL_SEGS];
+        unsigned tests = 0;
+        const bool occ = seg_hits_boxes<D>(x, fp, dl, S.box, S.blist, nb, tests);
+        W.v[W_OCCL_BOX_TESTS] += tests;
+        if (occ) continue;
         ++kv;
       }
       inc = Dl - (double)kv * (Dl / P.n_f);
-      if (P.heuristic == 3) {
+      if (heur == 3) {
+        ++W.v[W_MLP];
         double speed;
-        if (P.dynamics == 1) {
+        if (DYN == 1) {
           double ss = 0.0;
-          for (int j = 0; j < d; ++j) ss = ss + vel[j] * vel[j];
+#pragma unroll
+          for (int j = 0; j < D; ++j) ss = ss + vel[j] * vel[j];
           speed = sqrt(ss);
         } else {
           speed = P.nominal_speed;
@@ -571,8 +682,8 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
     const int nk = min(32, K - k0);
     for (int j = 0; j < nk; ++j) {   // fold in time order (every lane, same values)
       const double ij = __shfl_sync(FULL, inc, j);
-      const double t = c + ij;
-      c = (t > 0.0) ? t : 0.0;
+      const double tt = c + ij;
+      c = (tt > 0.0) ? tt : 0.0;
       s = s + ij;
     }
   }
@@ -580,6 +691,7 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
   c_out = c;
 }
 
+template <int D, int DYN>
 __global__ void __launch_bounds__(kWarps * 32) k_edges(const double* __restrict__ samples,
                                                        const int64_t* __restrict__ node_base,
                                                        const int32_t* __restrict__ n_env,
@@ -592,17 +704,18 @@ __global__ void __launch_bounds__(kWarps * 32) k_edges(const double* __restrict_
                                                        const NearRec* __restrict__ scratch,
                                                        const int64_t* __restrict__ row_ptr,
                                                        EdgeRec* __restrict__ edges,
-                                                       unsigned long long* __restrict__ nnz_free) {
+                                                       unsigned long long* __restrict__ nnz_free,
+                                                       unsigned long long* __restrict__ work) {
+  constexpr int NS = 2 * D + 2;   // p, v (double integrator), heading
   extern __shared__ double smem[];
   const int b = blockIdx.y;
-  const int d = P.pos_dim;
   const int O = obst_base[b + 1] - obst_base[b];
   const int F = feat_base[b + 1] - feat_base[b];
   double* sbox = smem;
-  double* sfeat = smem + (size_t)o_max * 2 * d;
-  int* lists = reinterpret_cast<int*>(sfeat + (size_t)f_max * d);
-  for (int i = threadIdx.x; i < O * 2 * d; i += blockDim.x) sbox[i] = obst[(size_t)obst_base[b] * 2 * d + i];
-  for (int i = threadIdx.x; i < F * d; i += blockDim.x) sfeat[i] = feat[(size_t)feat_base[b] * d + i];
+  double* sfeat = smem + (size_t)o_max * 2 * D;
+  int* lists = reinterpret_cast<int*>(sfeat + (size_t)f_max * D);
+  for (int i = threadIdx.x; i < O * 2 * D; i += blockDim.x) sbox[i] = obst[(size_t)obst_base[b] * 2 * D + i];
+  for (int i = threadIdx.x; i < F * D; i += blockDim.x) sfeat[i] = feat[(size_t)feat_base[b] * D + i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = n_env[b];
@@ -616,19 +729,24 @@ __global__ void __launch_bounds__(kWarps * 32) k_edges(const double* __restrict_
   const int stride = P.stride;
   const int64_t row = node_base[b] + u;
   const double* envs = samples + node_base[b] * stride;
-  double su[8], sv[8];
-  for (int j = 0; j < stride && j < 8; ++j) su[j] = envs[(int64_t)u * stride + j];
+  double su[NS], sv[NS];
+#pragma unroll
+  for (int j = 0; j < NS; ++j) su[j] = (j < stride) ? envs[(int64_t)u * stride + j] : 0.0;
   const int deg = min(cnt[row], cap);
   const int64_t e0 = row_ptr[row];
   int nfree = 0;
+  Work W;
+#pragma unroll
+  for (int i = 0; i < W_NUM; ++i) W.v[i] = 0;
   for (int j = 0; j < deg; ++j) {
     const NearRec rec = scratch[row * (int64_t)cap + j];
-    for (int q = 0; q < stride && q < 8; ++q) sv[q] = envs[(int64_t)rec.v * stride + q];
-    const bool coll = edge_collision(P, su, sv, rec.tau, S, O, lane);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) sv[q] = (q < stride) ? envs[(int64_t)rec.v * stride + q] : 0.0;
+    const bool coll = edge_collision<D, DYN>(P, su, sv, rec.tau, S, O, lane, W);
     float s32 = 0.0f, c32 = 0.0f;
     if (!coll) {
       double s64, c64;
-      edge_heuristic(P, su, sv, rec.tau, S, O, F, lane, s64, c64);
+      edge_heuristic<D, DYN>(P, su, sv, rec.tau, S, O, F, lane, s64, c64, W);
       s32 = (float)s64;
       c32 = (float)c64;
       ++nfree;
@@ -643,7 +761,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_edges(const double* __restrict_
     }
     __syncwarp();
   }
+  if (lane == 0) {
+    W.v[W_EDGES] = deg;
+    W.v[W_FREE_EDGES] = nfree;
+  }
   if (lane == 0 && nfree) atomicAdd(&nnz_free[b], (unsigned long long)nfree);
+#pragma unroll
+  for (int i = W_EDGES; i < W_NUM; ++i) {
+    unsigned x = W.v[i];
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+    if (lane == 0 && x) atomicAdd(&work[i], (unsigned long long)x);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -655,15 +783,42 @@ __global__ void __launch_bounds__(kWarps * 32) k_edges(const double* __restrict_
     if (_e != cudaSuccess) return cuda_error(_e, #x);  \
   } while (0)
 
+namespace {
+template <int D, int DYN>
+cudaError_t launch_near(dim3 grid, cudaStream_t st, const mpap_roadmap* rm, const int32_t* d_n, int cap,
+                        int32_t* d_cnt, NearRec* d_scr, int* d_over, unsigned long long* d_work) {
+  k_near<D, DYN><<<grid, kWarps * 32, 0, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->prm, cap, d_cnt, d_scr,
+                                               d_over, d_work);
+  return cudaGetLastError();
+}
+
+template <int D, int DYN>
+cudaError_t launch_edges(dim3 grid, size_t smem, cudaStream_t st, const mpap_roadmap* rm, const int32_t* d_n,
+                         int cap, const int32_t* d_cnt, const NearRec* d_scr, unsigned long long* d_free,
+                         unsigned long long* d_work) {
+  cudaError_t e = cudaFuncSetAttribute(k_edges<D, DYN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)std::max<size_t>(smem, 1));
+  if (e != cudaSuccess) return e;
+  k_edges<D, DYN><<<grid, kWarps * 32, smem, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->d_obst,
+                                                   rm->d_obst_base, rm->d_feat, rm->d_feat_base, rm->prm, cap,
+                                                   rm->o_max, rm->f_max, d_cnt, d_scr, rm->d_row_ptr, rm->d_edges,
+                                                   d_free, d_work);
+  return cudaGetLastError();
+}
+}  // namespace
+
 mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
   const int B = rm->B;
   const int64_t N = rm->node_base[B];
+  const int d = rm->prm.pos_dim;
+  const int dyn = rm->prm.dynamics;
   int32_t* d_n = nullptr;
   int32_t* d_cnt = nullptr;
   int* d_over = nullptr;
   NearRec* d_scr = nullptr;
   unsigned long long* d_free = nullptr;
-  mpap_status status = MPAP_OK;
+  unsigned long long* d_work = nullptr;
+  static_assert(W_NUM <= kWorkCounters, "work counter array too small");
   int cap = 128;
   CK(cudaMallocAsync(&d_n, sizeof(int32_t) * B, st));
   CK(cudaMemcpyAsync(d_n, rm->n.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice, st));
@@ -671,6 +826,8 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
   CK(cudaMallocAsync(&d_over, sizeof(int), st));
   CK(cudaMallocAsync(&d_free, sizeof(unsigned long long) * B, st));
   CK(cudaMemsetAsync(d_free, 0, sizeof(unsigned long long) * B, st));
+  CK(cudaMallocAsync(&d_work, sizeof(unsigned long long) * W_NUM, st));
+  CK(cudaMemsetAsync(d_work, 0, sizeof(unsigned long long) * W_NUM, st));
   CK(cudaMallocAsync(&rm->d_row_ptr, sizeof(int64_t) * (N + 1), st));
   const dim3 grid((rm->n_max + kWarps - 1) / kWarps, B);
   for (int attempt = 0; attempt < 8; ++attempt) {
@@ -682,17 +839,17 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
       return set_error(MPAP_ERR_OUT_OF_MEMORY, "neighbour scratch allocation failed");
     }
     CK(cudaMemsetAsync(d_over, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(d_work, 0, sizeof(unsigned long long) * 3, st));
     {
       ProfScope ps("k_near", st);
-      if (rm->prm.dynamics == 0)
-        k_near<0><<<grid, kWarps * 32, 0, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->prm, cap, d_cnt, d_scr,
-                                                 d_over);
-      else
-        k_near<1><<<grid, kWarps * 32, 0, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->prm, cap, d_cnt, d_scr,
-                                                 d_over);
+      cudaError_t e;
+      if (d == 2) e = dyn ? launch_near<2, 1>(grid, st, rm, d_n, cap, d_cnt, d_scr, d_over, d_work)
+                          : launch_near<2, 0>(grid, st, rm, d_n, cap, d_cnt, d_scr, d_over, d_work);
+      else e = dyn ? launch_near<3, 1>(grid, st, rm, d_n, cap, d_cnt, d_scr, d_over, d_work)
+                   : launch_near<3, 0>(grid, st, rm, d_n, cap, d_cnt, d_scr, d_over, d_work);
+      CK(e);
     }
     note_launch();
-    CK(cudaGetLastError());
     int over = 0;
     CK(cudaMemcpyAsync(&over, d_over, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -717,30 +874,32 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
     cudaGetLastError();
     return set_error(MPAP_ERR_OUT_OF_MEMORY, "edge array allocation failed");
   }
-  const int d = rm->prm.pos_dim;
   const size_t smem = sizeof(double) * ((size_t)rm->o_max * 2 * d + (size_t)rm->f_max * d) +
                       sizeof(int) * (size_t)kWarps * (rm->f_max + rm->o_max);
-  CK(cudaFuncSetAttribute(k_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
   if (rm->nnz_total > 0) {
     {
       ProfScope ps("k_edges", st);
-      k_edges<<<grid, kWarps * 32, smem, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->d_obst, rm->d_obst_base,
-                                               rm->d_feat, rm->d_feat_base, rm->prm, cap, rm->o_max, rm->f_max,
-                                               d_cnt, d_scr, rm->d_row_ptr, rm->d_edges, d_free);
+      cudaError_t e;
+      if (d == 2) e = dyn ? launch_edges<2, 1>(grid, smem, st, rm, d_n, cap, d_cnt, d_scr, d_free, d_work)
+                          : launch_edges<2, 0>(grid, smem, st, rm, d_n, cap, d_cnt, d_scr, d_free, d_work);
+      else e = dyn ? launch_edges<3, 1>(grid, smem, st, rm, d_n, cap, d_cnt, d_scr, d_free, d_work)
+                   : launch_edges<3, 0>(grid, smem, st, rm, d_n, cap, d_cnt, d_scr, d_free, d_work);
+      CK(e);
     }
     note_launch();
-    CK(cudaGetLastError());
   }
   std::vector<unsigned long long> fr(B);
   CK(cudaMemcpyAsync(fr.data(), d_free, sizeof(unsigned long long) * B, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(rm->work, d_work, sizeof(unsigned long long) * W_NUM, cudaMemcpyDeviceToHost, st));
   CK(cudaFreeAsync(d_scr, st));
   CK(cudaFreeAsync(d_cnt, st));
   CK(cudaFreeAsync(d_over, st));
   CK(cudaFreeAsync(d_free, st));
+  CK(cudaFreeAsync(d_work, st));
   CK(cudaFreeAsync(d_n, st));
   CK(cudaStreamSynchronize(st));
   rm->nnz_free.assign(fr.begin(), fr.end());
-  return status;
+  return MPAP_OK;
 }
 
 }  // namespace mpap

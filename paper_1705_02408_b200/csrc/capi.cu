@@ -20,6 +20,20 @@ static std::atomic<long long> g_launches{0};
 
 void note_launch(int k) { g_launches.fetch_add(k); }
 
+void retain_pool_memory(int device) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  for (int d : done)
+    if (d == device) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.push_back(device);
+}
+
 // ---- per-kernel event timing ------------------------------------------------
 namespace {
 struct PendingRec {
@@ -160,14 +174,13 @@ void mpap_roadmap_free(mpap_roadmap* rm) {
   int cur = 0;
   cudaGetDevice(&cur);
   cudaSetDevice(rm->device);
-  cudaFree(rm->d_samples);
-  cudaFree(rm->d_obst);
-  cudaFree(rm->d_feat);
-  cudaFree(rm->d_obst_base);
-  cudaFree(rm->d_feat_base);
-  cudaFree(rm->d_node_base);
-  cudaFree(rm->d_row_ptr);
-  cudaFree(rm->d_edges);
+  // every search of this roadmap may still be in flight on some stream:
+  // wait for the device, then hand the memory back to the stream-ordered pool
+  cudaDeviceSynchronize();
+  void* ptrs[] = {rm->d_samples, rm->d_obst, rm->d_feat, rm->d_obst_base, rm->d_feat_base, rm->d_node_base,
+                  rm->d_row_ptr, rm->d_edges};
+  for (void* p : ptrs)
+    if (p) cudaFreeAsync(p, 0);
   cudaSetDevice(cur);
   delete rm;
 }
@@ -212,6 +225,7 @@ mpap_status mpap_build_roadmap_batch(int32_t n_envs, const double* samples, cons
   mpap_roadmap* rm = new (std::nothrow) mpap_roadmap();
   if (!rm) return set_error(MPAP_ERR_OUT_OF_MEMORY, "host allocation failed");
   CKC(cudaGetDevice(&rm->device));
+  retain_pool_memory(rm->device);
   rm->B = n_envs;
   DevParams& P = rm->prm;
   std::memset(&P, 0, sizeof(P));
@@ -251,17 +265,17 @@ mpap_status mpap_build_roadmap_batch(int32_t n_envs, const double* samples, cons
     rm->f_max = std::max(rm->f_max, n_features[b]);
   }
   const cudaMemcpyKind kind = (mem == MPAP_MEM_HOST) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-  CKC(cudaMalloc(&rm->d_samples, sizeof(double) * N * row_stride));
+  CKC(cudaMallocAsync(&rm->d_samples, sizeof(double) * N * row_stride, st));
   CKC(cudaMemcpyAsync(rm->d_samples, samples, sizeof(double) * N * row_stride, kind, st));
-  CKC(cudaMalloc(&rm->d_obst, sizeof(double) * std::max<int64_t>(O * 2 * d, 1)));
+  CKC(cudaMallocAsync(&rm->d_obst, sizeof(double) * std::max<int64_t>(O * 2 * d, 1), st));
   if (O) CKC(cudaMemcpyAsync(rm->d_obst, obstacles, sizeof(double) * O * 2 * d, kind, st));
-  CKC(cudaMalloc(&rm->d_feat, sizeof(double) * std::max<int64_t>(F * d, 1)));
+  CKC(cudaMallocAsync(&rm->d_feat, sizeof(double) * std::max<int64_t>(F * d, 1), st));
   if (F) CKC(cudaMemcpyAsync(rm->d_feat, features, sizeof(double) * F * d, kind, st));
-  CKC(cudaMalloc(&rm->d_obst_base, sizeof(int32_t) * (n_envs + 1)));
+  CKC(cudaMallocAsync(&rm->d_obst_base, sizeof(int32_t) * (n_envs + 1), st));
   CKC(cudaMemcpyAsync(rm->d_obst_base, ob.data(), sizeof(int32_t) * (n_envs + 1), cudaMemcpyHostToDevice, st));
-  CKC(cudaMalloc(&rm->d_feat_base, sizeof(int32_t) * (n_envs + 1)));
+  CKC(cudaMallocAsync(&rm->d_feat_base, sizeof(int32_t) * (n_envs + 1), st));
   CKC(cudaMemcpyAsync(rm->d_feat_base, fb.data(), sizeof(int32_t) * (n_envs + 1), cudaMemcpyHostToDevice, st));
-  CKC(cudaMalloc(&rm->d_node_base, sizeof(int64_t) * (n_envs + 1)));
+  CKC(cudaMallocAsync(&rm->d_node_base, sizeof(int64_t) * (n_envs + 1), st));
   CKC(cudaMemcpyAsync(rm->d_node_base, rm->node_base.data(), sizeof(int64_t) * (n_envs + 1),
                       cudaMemcpyHostToDevice, st));
   s = build_roadmap_device(rm, st);
@@ -312,6 +326,7 @@ mpap_status mpap_roadmap_import(int32_t n, int32_t pos_dim, const double* positi
   if (!rm) return set_error(MPAP_ERR_OUT_OF_MEMORY, "host allocation failed");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   CKC(cudaGetDevice(&rm->device));
+  retain_pool_memory(rm->device);
   rm->B = 1;
   std::memset(&rm->prm, 0, sizeof(rm->prm));
   rm->prm.pos_dim = pos_dim;
@@ -329,13 +344,13 @@ mpap_status mpap_roadmap_import(int32_t n, int32_t pos_dim, const double* positi
   rm->nnz_total = nnz;
   std::vector<int64_t> rp64(n + 1);
   for (int32_t u = 0; u <= n; ++u) rp64[u] = row_ptr[u];
-  CKC(cudaMalloc(&rm->d_samples, sizeof(double) * n * pos_dim));
+  CKC(cudaMallocAsync(&rm->d_samples, sizeof(double) * n * pos_dim, st));
   CKC(cudaMemcpyAsync(rm->d_samples, positions, sizeof(double) * n * pos_dim, cudaMemcpyHostToDevice, st));
-  CKC(cudaMalloc(&rm->d_node_base, sizeof(int64_t) * 2));
+  CKC(cudaMallocAsync(&rm->d_node_base, sizeof(int64_t) * 2, st));
   CKC(cudaMemcpyAsync(rm->d_node_base, rm->node_base.data(), sizeof(int64_t) * 2, cudaMemcpyHostToDevice, st));
-  CKC(cudaMalloc(&rm->d_row_ptr, sizeof(int64_t) * (n + 1)));
+  CKC(cudaMallocAsync(&rm->d_row_ptr, sizeof(int64_t) * (n + 1), st));
   CKC(cudaMemcpyAsync(rm->d_row_ptr, rp64.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
-  CKC(cudaMalloc(&rm->d_edges, sizeof(EdgeRec) * er.size()));
+  CKC(cudaMallocAsync(&rm->d_edges, sizeof(EdgeRec) * er.size(), st));
   CKC(cudaMemcpyAsync(rm->d_edges, er.data(), sizeof(EdgeRec) * er.size(), cudaMemcpyHostToDevice, st));
   CKC(cudaStreamSynchronize(st));
   *out = rm;
@@ -343,6 +358,12 @@ mpap_status mpap_roadmap_import(int32_t n, int32_t pos_dim, const double* positi
 }
 
 int32_t mpap_roadmap_envs(const mpap_roadmap* rm) { return rm ? rm->B : 0; }
+
+mpap_status mpap_roadmap_work(const mpap_roadmap* rm, uint64_t* counters, int32_t n) {
+  if (!rm || !counters || n < 0) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad roadmap/counters");
+  for (int32_t i = 0; i < n; ++i) counters[i] = (i < kWorkCounters) ? (uint64_t)rm->work[i] : 0;
+  return MPAP_OK;
+}
 
 mpap_status mpap_roadmap_info(const mpap_roadmap* rm, int32_t env, int32_t* n, int64_t* nnz, int64_t* nnz_free) {
   if (!rm || env < 0 || env >= rm->B) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad roadmap/env");

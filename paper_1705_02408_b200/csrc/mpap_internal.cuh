@@ -13,6 +13,7 @@
 namespace mpap {
 
 constexpr int kMlpSize = 122;
+constexpr int kWorkCounters = 16;
 
 // Kernel-parameter copy of mpap_params plus derived constants; passed by value
 // (lives in the constant bank, so every lane reads it as a broadcast).
@@ -62,6 +63,8 @@ struct mpap_roadmap {
   int64_t* d_row_ptr = nullptr;    // [sum n + 1] global edge offsets
   mpap::EdgeRec* d_edges = nullptr;
   int64_t nnz_total = 0;
+  unsigned long long work[mpap::kWorkCounters] = {};  // build work counters (mpap_roadmap_work)
+  cudaStream_t alloc_stream = nullptr;                 // stream the device arrays were allocated on
 };
 
 namespace mpap {
@@ -78,6 +81,8 @@ struct ProfScope {
   ~ProfScope();
 };
 mpap_status set_error(mpap_status s, const std::string& msg);
+// keeps freed stream-ordered memory in the device pool (no OS round trip per call)
+void retain_pool_memory(int device);
 mpap_status cuda_error(cudaError_t e, const char* what);
 
 // roadmap build (build_kernels.cu)
