@@ -21,6 +21,7 @@ SOURCES = ["capi.cu", "build_kernels.cu", "search_kernels.cu"]
 HEADERS = [os.path.join(CSRC, "mpap_internal.cuh"), os.path.join(INCLUDE, "mpap.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+EXTRA = os.environ.get("MPAP_NVCC_EXTRA", "").split()   # tuning experiments only
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
            "-I", INCLUDE, "-I", CSRC]
@@ -34,8 +35,9 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = None) -> str:
+    lib = out or LIB
+    if not force and out is None and not _stale():
         return LIB
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
@@ -43,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for s in SOURCES:
         src = os.path.join(CSRC, s)
         obj = os.path.join(objdir, s.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *NVFLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *NVFLAGS, *EXTRA, "-c", src, "-o", obj]
         out = subprocess.run(cmd, capture_output=True, text=True)
         if out.returncode != 0:
             raise RuntimeError(f"nvcc failed for {s}:\n{out.stderr}")
@@ -52,15 +54,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         with open(os.path.join(objdir, s + ".ptxas.txt"), "w") as f:
             f.write(out.stderr)
         objs.append(obj)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs]
     out = subprocess.run(cmd, capture_output=True, text=True)
     if out.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{out.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    outp = None
+    if "--out" in sys.argv:
+        outp = sys.argv[sys.argv.index("--out") + 1]
+    print(build(force="--force" in sys.argv or outp is not None, verbose=True, out=outp))

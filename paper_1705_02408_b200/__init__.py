@@ -19,7 +19,7 @@ from typing import Any, Dict, Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmpap.so")
+LIB_PATH = os.environ.get("MPAP_LIB") or os.path.join(_PKG, "libmpap.so")   # MPAP_LIB: tuning variants
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libmpap.so not found at {LIB_PATH}: build it with "

@@ -35,8 +35,12 @@
 namespace mpap {
 
 #define FULL 0xffffffffu
+#ifndef MPAP_EDGES_MIN_BLOCKS
+#define MPAP_EDGES_MIN_BLOCKS 1
+#endif
 constexpr int kWarps = 8;                 // warps per block in the build kernels
 constexpr double kCullMargin = 1e-6;      // absolute; >> rounding of O(100) coordinates
+constexpr int kNearIntervals = 16;        // level-2 neighbour filter resolution
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -257,8 +261,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_near(const double* __restrict__
     double v02 = 0.0;
 #pragma unroll
     for (int j = 0; j < D; ++j) v02 += su[D + j] * su[D + j];
+    // level 1 (necessary conditions of c* < r): min energy to
+    // move by Dp with free end velocity is 3|Dp|^2/tau^3, and by AM-GM
+    // tau + r_u |dv|^2 / tau >= 2 sqrt(r_u) |dv|; 1e-9 relative slack
     const double bp = (sqrt(v02) * r + r * r / sqrt(3.0 * ru)) * (1.0 + 1e-9);
-    const double bv = (r / sqrt(ru)) * (1.0 + 1e-9);
+    const double bv = (r / (2.0 * sqrt(ru))) * (1.0 + 1e-9);
     const double bp2 = bp * bp, bv2 = bv * bv;
     int qn = 0;
     auto process = [&](int k) {
@@ -294,6 +301,28 @@ __global__ void __launch_bounds__(kWarps * 32) k_near(const double* __restrict__
           dv2 += e * e;
         }
         pf = !(dp2 > bp2 || dv2 > bv2);
+        if (pf) {
+          // level 2: c(tau) = tau + r_u (12 |a - s tau/2|^2 / tau^3 + |dv|^2 / tau)
+          // (a = p1 - p0, s = v0 + v1) is bounded below on [ta, tb] by
+          // ta + r_u (12 max(0, |a| - |s| tb/2)^2 / tb^3 + |dv|^2 / tb);
+          // a pair whose bound reaches r on every interval has no edge.
+          double ss = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            const double e = sv[D + j] + su[D + j];
+            ss += e * e;
+          }
+          const double na = sqrt(dp2), ns = sqrt(ss);
+          bool possible = false;
+          for (int jj = 0; jj < kNearIntervals && !possible; ++jj) {
+            const double ta = r * (double)jj / (double)kNearIntervals;
+            const double tb = r * (double)(jj + 1) / (double)kNearIntervals;
+            const double g = fmax(na - ns * tb * 0.5, 0.0);
+            const double L = ta + ru * (12.0 * g * g / (tb * tb * tb) + dv2 / tb);
+            possible = L * (1.0 - 1e-9) < r;
+          }
+          pf = possible;
+        }
       }
       const unsigned m = __ballot_sync(FULL, pf);
       if (pf) queue[warp][qn + __popc(m & lt)] = v;
@@ -366,15 +395,35 @@ __global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ cnt, 
 // ---------------------------------------------------------------------------
 // k_edges: collision + heuristic summary per edge
 // ---------------------------------------------------------------------------
-struct EdgeSmem {
-  double* box;   // [O][2D]
-  double* feat;  // [F][D]
-  int* flist;    // per warp [F]
-  int* blist;    // per warp [O]
+// Per-warp shared scratch: culled feature coordinates (SoA) and culled boxes.
+template <int D>
+struct WarpLists {
+  double* f[D];                 // [F_max] each
+  double* box;                  // [O_max][2D]
+  unsigned long long* fmask;    // [F_max] per-feature box masks
+  const double* mlp;            // [122] block-shared MLP weights
 };
 
+// Work counters: warp-uniform counts go to the warp's shared-memory slots
+// (written by lane 0 only); per-lane counts live in four registers and are
+// folded into the slots once per edge.
 struct Work {
-  unsigned v[W_NUM];
+  unsigned* sm;   // [W_NUM] per warp
+  unsigned occl_segs, occl_tests, coll_segs, coll_tests;
+  __device__ __forceinline__ void add(int lane, int i, unsigned x) {
+    if (lane == 0) sm[i] += x;
+  }
+  __device__ __forceinline__ void flush(int lane) {
+    const unsigned a = __reduce_add_sync(FULL, occl_segs), b = __reduce_add_sync(FULL, occl_tests);
+    const unsigned c = __reduce_add_sync(FULL, coll_segs), e = __reduce_add_sync(FULL, coll_tests);
+    if (lane == 0) {
+      sm[W_OCCL_SEGS] += a;
+      sm[W_OCCL_BOX_TESTS] += b;
+      sm[W_COLL_SEGS] += c;
+      sm[W_COLL_BOX_TESTS] += e;
+    }
+    occl_segs = occl_tests = coll_segs = coll_tests = 0;
+  }
 };
 
 __device__ __forceinline__ double warp_min(double x) {
@@ -386,27 +435,33 @@ __device__ __forceinline__ double warp_max(double x) {
   return x;
 }
 
-// Boxes overlapping [lo - m, hi + m] -> per-warp list; returns the count.
-// A box outside that region cannot be hit by any segment inside [lo, hi]
-// (its slab interval is empty by a margin far above rounding).
+// Boxes overlapping [lo - m, hi + m] -> coordinates in the warp's list.  A box
+// outside that region cannot be hit by any segment inside [lo, hi] (its slab
+// interval is empty by a margin far above rounding).
 template <int D>
-__device__ int cull_boxes(const double* box, int O, const double* lo, const double* hi, double m, int* list,
-                          int lane) {
+__device__ int cull_boxes(const double* __restrict__ box, int O, const double* lo, const double* hi, double m,
+                          double* out, int lane) {
   int nc = 0;
   const unsigned lt = lanemask_lt();
   __syncwarp();
   for (int o0 = 0; o0 < O; o0 += 32) {
     const int o = o0 + lane;
     bool keep = false;
+    double bl[2 * D];
     if (o < O) {
       keep = true;
-      const double* bx = box + (size_t)o * 2 * D;
+#pragma unroll
+      for (int k = 0; k < 2 * D; ++k) bl[k] = __ldg(box + (size_t)o * 2 * D + k);
 #pragma unroll
       for (int k = 0; k < D; ++k)
-        if (bx[k] > hi[k] + m || bx[D + k] < lo[k] - m) keep = false;
+        if (bl[k] > hi[k] + m || bl[D + k] < lo[k] - m) keep = false;
     }
     const unsigned msk = __ballot_sync(FULL, keep);
-    if (keep) list[nc + __popc(msk & lt)] = o;
+    if (keep) {
+      double* dst = out + (size_t)(nc + __popc(msk & lt)) * 2 * D;
+#pragma unroll
+      for (int k = 0; k < 2 * D; ++k) dst[k] = bl[k];
+    }
     nc += __popc(msk);
   }
   __syncwarp();
@@ -417,10 +472,12 @@ __device__ int cull_boxes(const double* box, int O, const double* lo, const doub
 // The slab test of DESIGN.md §3 with the per-axis reciprocal 1/Dv_k computed
 // once per segment (the value the per-box formula computes); a box separated
 // from the segment's bounding box by more than kCullMargin is skipped (its
-// slab test is provably false).  `tests` counts the slab tests executed.
-template <int D>
-__device__ __forceinline__ bool seg_hits_boxes(const double* A, const double* B, const double* Dv,
-                                               const double* box, const int* list, int nl, unsigned& tests) {
+// slab test is provably false).  With USE_MASK only the boxes whose bit is
+// set in `mask` are visited (a superset of the boxes that can be hit).
+// Returns hit | (slab tests executed << 1).
+template <int D, bool USE_MASK>
+__device__ __forceinline__ unsigned seg_hits_boxes(const double* A, const double* B, const double* Dv,
+                                                   const double* bl, int nl, unsigned long long mask) {
   double inv[D], slo[D], shi[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
@@ -428,8 +485,17 @@ __device__ __forceinline__ bool seg_hits_boxes(const double* A, const double* B,
     slo[k] = fmin(A[k], B[k]) - kCullMargin;
     shi[k] = fmax(A[k], B[k]) + kCullMargin;
   }
-  for (int i = 0; i < nl; ++i) {
-    const double* bx = box + (size_t)list[i] * 2 * D;
+  unsigned tests = 0;
+  int i = -1;
+  for (;;) {
+    if (USE_MASK) {
+      if (!mask) break;
+      i = __ffsll((long long)mask) - 1;
+      mask &= mask - 1;
+    } else {
+      if (++i >= nl) break;
+    }
+    const double* bx = bl + (size_t)i * 2 * D;
     bool sep = false;
 #pragma unroll
     for (int k = 0; k < D; ++k)
@@ -452,26 +518,29 @@ __device__ __forceinline__ bool seg_hits_boxes(const double* A, const double* B,
         if (t0 > t1) hit = false;
       }
     }
-    if (hit) return true;
+    if (hit) return 1u | (tests << 1);
   }
-  return false;
+  return tests << 1;
 }
 
 // Collision(u,v) of reading R8, warp-cooperative; every lane returns the result.
 template <int D, int DYN>
-__device__ bool edge_collision(const DevParams& P, const double* su, const double* sv, double tau,
-                               const EdgeSmem& S, int O, int lane, Work& W) {
+__device__ __forceinline__ bool edge_collision(const DevParams& P, const double* su, const double* sv, double tau,
+                               const double* __restrict__ box, int O, WarpLists<D>& L, int lane, Work& W) {
   if (DYN == 0) {
     bool hit = false;
     for (int o0 = 0; o0 < O; o0 += 32) {
       const int o = o0 + lane;
       if (o < O) {
-        ++W.v[W_COLL_BOX_TESTS];
-        if (seg_box<D>(su, sv, S.box + (size_t)o * 2 * D)) hit = true;
+        ++W.coll_tests;
+        double bl[2 * D];
+#pragma unroll
+        for (int k = 0; k < 2 * D; ++k) bl[k] = __ldg(box + (size_t)o * 2 * D + k);
+        if (seg_box<D>(su, sv, bl)) hit = true;
       }
       if (__any_sync(FULL, hit)) return true;
     }
-    if (lane == 0) ++W.v[W_COLL_SEGS];
+    W.add(lane, W_COLL_SEGS, 1);
     return false;
   }
   double c2[D], c3[D];
@@ -494,9 +563,8 @@ __device__ bool edge_collision(const DevParams& P, const double* su, const doubl
   if (__any_sync(FULL, out)) return true;
 #pragma unroll
   for (int j = 0; j < D; ++j) { lo[j] = warp_min(lo[j]); hi[j] = warp_max(hi[j]); }
-  int* list = S.blist;
-  const int nl = cull_boxes<D>(S.box, O, lo, hi, kCullMargin, list, lane);
-  if (lane == 0) W.v[W_CULL_TESTS] += O;
+  const int nl = cull_boxes<D>(box, O, lo, hi, kCullMargin, L.box, lane);
+  W.add(lane, W_CULL_TESTS, O);
   if (nl == 0) return false;
   for (int k0 = 1; k0 <= Kc; k0 += 32) {
     const int k = k0 + lane;
@@ -509,24 +577,26 @@ __device__ bool edge_collision(const DevParams& P, const double* su, const doubl
       di_pos<D>(su, c2, c3, tb, B);
 #pragma unroll
       for (int j = 0; j < D; ++j) Dv[j] = B[j] - A[j];
-      ++W.v[W_COLL_SEGS];
-      unsigned t = 0;
-      hit = seg_hits_boxes<D>(A, B, Dv, S.box, list, nl, t);
-      W.v[W_COLL_BOX_TESTS] += t;
+      ++W.coll_segs;
+      const unsigned rr = seg_hits_boxes<D, false>(A, B, Dv, L.box, nl, 0ull);
+      hit = rr & 1u;
+      W.coll_tests += rr >> 1;
     }
     if (__any_sync(FULL, hit)) return true;
   }
   return false;
 }
 
-__device__ __forceinline__ double mlp_out0(const DevParams& P, double z0, double z1, double z2) {
-  const double* W1 = P.mlp;
-  const double* b1 = P.mlp + 24;
-  const double* W2 = P.mlp + 32;
-  const double* b2 = P.mlp + 96;
-  const double* W3 = P.mlp + 104;
-  const double* b3 = P.mlp + 120;
-  double h1[8], h2[8];
+// The weights are read from shared memory on every call (staged once per
+// block) so the compiler cannot hoist all 122 of them into registers.
+__device__ __noinline__ double mlp_out0(const double* w, double z0, double z1, double z2) {
+  const double* W1 = w;
+  const double* b1 = w + 24;
+  const double* W2 = w + 32;
+  const double* b2 = w + 96;
+  const double* W3 = w + 104;
+  const double* b3 = w + 120;
+  double h1[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     double a = b1[i];
@@ -535,27 +605,87 @@ __device__ __forceinline__ double mlp_out0(const DevParams& P, double z0, double
     a = a + W1[i * 3 + 2] * z2;
     h1[i] = (a > 0.0) ? a : 0.0;
   }
-#pragma unroll
+  // output sum o = b3[0] + sum_i W3[i] h2[i] accumulated in index order as
+  // each hidden-2 unit is produced (same operation sequence as the contract)
+  double o = b3[0];
+#pragma unroll 1
   for (int i = 0; i < 8; ++i) {
     double a = b2[i];
 #pragma unroll
     for (int j = 0; j < 8; ++j) a = a + W2[i * 8 + j] * h1[j];
-    h2[i] = (a > 0.0) ? a : 0.0;
+    const double h2 = (a > 0.0) ? a : 0.0;
+    o = o + W3[i] * h2;
   }
-  double o = b3[0];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) o = o + W3[j] * h2[j];
   return o;
 }
 
-// Heuristic summary (s, c) of reading R10 for a collision-free edge.  Steps
-// are processed 32 at a time (one per lane); per chunk the warp culls the
-// features within range of the chunk's bounding box and the boxes that can
-// occlude a sight line from it, then every lane counts its visible features
-// and the increments are folded in time order with shuffles.
+#ifndef MPAP_FEAT_UNROLL
+#define MPAP_FEAT_UNROLL 1
+#endif
+constexpr int kFeatUnroll = MPAP_FEAT_UNROLL;   // features tested per inner iteration (ILP)
+
+// Bounding box of the positions of steps t in [ta, tb] along the edge, computed
+// analytically by every lane (no shuffles): endpoints plus, for the cubic, the
+// interior stationary points.  It contains the contract's step positions up to
+// rounding (~1e-15 relative), far inside the culling margins.
 template <int D, int DYN>
-__device__ void edge_heuristic(const DevParams& P, const double* su, const double* sv, double T, const EdgeSmem& S,
-                               int O, int F, int lane, double& s_out, double& c_out, Work& W) {
+__device__ __forceinline__ void chunk_bbox(const double* su, const double* sv, const double* c2, const double* c3,
+                                           double T, double ta, double tb, double* lo, double* hi) {
+  double xa[D], xb[D];
+  if (DYN == 0) {
+    const double sa = ta / T, sb = tb / T;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      xa[j] = su[j] + sa * (sv[j] - su[j]);
+      xb[j] = su[j] + sb * (sv[j] - su[j]);
+    }
+  } else {
+    di_pos<D>(su, c2, c3, ta, xa);
+    di_pos<D>(su, c2, c3, tb, xb);
+  }
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    lo[j] = fmin(xa[j], xb[j]);
+    hi[j] = fmax(xa[j], xb[j]);
+    if (DYN == 1) {
+      // p'(t) = v0 + 2 c2 t + 3 c3 t^2 = 0
+      const double A = 3.0 * c3[j], Bq = 2.0 * c2[j], Cq = su[D + j];
+      double r0 = -1.0, r1 = -1.0;
+      if (A != 0.0) {
+        const double disc = Bq * Bq - 4.0 * A * Cq;
+        if (disc >= 0.0) {
+          const double sq = sqrt(disc);
+          r0 = (-Bq - sq) / (2.0 * A);
+          r1 = (-Bq + sq) / (2.0 * A);
+        }
+      } else if (Bq != 0.0) {
+        r0 = -Cq / Bq;
+      }
+      if (r0 > ta && r0 < tb) {
+        const double x = su[j] + r0 * (su[D + j] + r0 * (c2[j] + r0 * c3[j]));
+        lo[j] = fmin(lo[j], x);
+        hi[j] = fmax(hi[j], x);
+      }
+      if (r1 > ta && r1 < tb) {
+        const double x = su[j] + r1 * (su[D + j] + r1 * (c2[j] + r1 * c3[j]));
+        lo[j] = fmin(lo[j], x);
+        hi[j] = fmax(hi[j], x);
+      }
+    }
+  }
+}
+
+// Heuristic summary (s, c) of reading R10 for a collision-free edge.  Steps
+// are processed 32 at a time (one per lane).  Per chunk every lane computes
+// the chunk's bounding box and heading arc analytically; the warp culls the
+// features that can be visible from the chunk and the boxes that can occlude
+// a sight line into shared memory (ballot compaction); each lane then counts
+// the visible features of its step, and the per-step increments are folded in
+// time order from shared memory (every lane folds the same sequence).
+template <int D, int DYN>
+__device__ void edge_heuristic(const DevParams& P, const double* su, const double* sv, double T,
+                               const double* __restrict__ feat, int F, const double* __restrict__ box, int O,
+                               WarpLists<D>& L, double* fold, int lane, double& s_out, double& c_out, Work& W) {
   const double kk = ceil(T / P.dt);
   const int K = (kk < 1.0) ? 1 : (int)kk;
   const double Dl = T / (double)K;
@@ -576,76 +706,178 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
   const double R2 = R * R;
   const double cos2 = P.fov_cos_half * P.fov_cos_half;
   const int heur = P.heuristic;
+  const float half_fov = acosf((float)P.fov_cos_half);
   const unsigned lt = lanemask_lt();
   double s = 0.0, c = 0.0;
   for (int k0 = 0; k0 < K; k0 += 32) {
-    const int k = k0 + lane;
-    const bool act = k < K;
-    double x[D], hv[D], vel[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) { x[j] = 0.0; hv[j] = 0.0; vel[j] = 0.0; }
-    const double t = (double)k * Dl;
-    if (act) {
-      if (DYN == 0) {
-        const double sp = t / T;
-#pragma unroll
-        for (int j = 0; j < D; ++j) x[j] = su[j] + sp * (sv[j] - su[j]);
-      } else {
-        di_pos<D>(su, c2, c3, t, x);
-        di_vel<D>(su, c2, c3, t, vel);
-      }
-      if (heur == 1) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) hv[j] = (DYN == 1) ? vel[j] : sv[j] - su[j];
-      } else if (heur >= 2) {
-        const double sp = t / T;
-        hv[0] = (1.0 - sp) * hu0 + sp * hv0;
-        hv[1] = (1.0 - sp) * hu1 + sp * hv1;
-      }
-    }
-    // chunk bounding box -> culled features and occluders
+    const int nk = min(32, K - k0);
+    const double ta = (double)k0 * Dl, tb = (double)(k0 + nk - 1) * Dl;
     double lo[D], hi[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      lo[j] = warp_min(act ? x[j] : 1e300);
-      hi[j] = warp_max(act ? x[j] : -1e300);
+    chunk_bbox<D, DYN>(su, sv, c2, c3, T, ta, tb, lo, hi);
+    // Conservative single-precision culls (only discard features whose exact
+    // test provably fails; margins >> float rounding):
+    //  * range: distance(feature, chunk box) > R + 1e-3;
+    //  * angle (heading heuristics): the FOV test needs the horizontal angle
+    //    between heading and sight line <= the half angle (the 3D angle is
+    //    never smaller for a horizontal heading).  Headings (1-s) hu + s hv on
+    //    [s0, s1] rotate monotonically between their end directions (a chord);
+    //    sight lines from the chunk's xy-rectangle (circumradius rho inflated
+    //    by 1e-4 m) lie within asin(rho / dc) of the centre direction.
+    bool ang = false;
+    float ux = 0.0f, uy = 0.0f, c1 = 0.0f, s1 = 0.0f, smax = -1.0f;
+    if (heur >= 2) {
+      const float sa = (float)(ta / T), sb = (float)(tb / T);
+      const float ax = (1.0f - sa) * (float)hu0 + sa * (float)hv0, ay = (1.0f - sa) * (float)hu1 + sa * (float)hv1;
+      const float bx = (1.0f - sb) * (float)hu0 + sb * (float)hv0, by = (1.0f - sb) * (float)hu1 + sb * (float)hv1;
+      // distance of the chord [a, b] from the origin (headings must stay away from 0)
+      const float ex = bx - ax, ey = by - ay;
+      const float ee = ex * ex + ey * ey;
+      float tq = (ee > 0.0f) ? -(ax * ex + ay * ey) / ee : 0.0f;
+      tq = fminf(fmaxf(tq, 0.0f), 1.0f);
+      const float qx = ax + tq * ex, qy = ay + tq * ey;
+      if (qx * qx + qy * qy > 1e-4f) {
+        const float na = rsqrtf(ax * ax + ay * ay), nb = rsqrtf(bx * bx + by * by);
+        const float dax = ax * na, day = ay * na, dbx = bx * nb, dby = by * nb;
+        const float mx = dax + dbx, my = day + dby;
+        const float mn = sqrtf(mx * mx + my * my);
+        if (mn > 1e-2f) {
+          ux = mx / mn;
+          uy = my / mn;
+          const float dev = 0.5f * atan2f(fabsf(dax * dby - day * dbx), dax * dbx + day * dby);
+          const float beta0 = half_fov + dev + 2e-3f;   // half angle + arc + margin
+          const float wmax = 3.1315927f - beta0;        // keep the total below pi - 0.01
+          if (wmax > 0.0f) {
+            ang = true;
+            c1 = cosf(beta0);
+            s1 = sinf(beta0);
+            smax = (wmax >= 1.5707963f) ? 2.0f : sinf(wmax);
+          }
+        }
+      }
     }
+    const float flx = (float)lo[0], fhx = (float)hi[0], fly = (float)lo[1], fhy = (float)hi[1];
+    const float flz = (D == 3) ? (float)lo[D - 1] : 0.0f, fhz = (D == 3) ? (float)hi[D - 1] : 0.0f;
+    const float ccx = 0.5f * (flx + fhx), ccy = 0.5f * (fly + fhy);
+    const float rho = 0.5f * sqrtf((fhx - flx) * (fhx - flx) + (fhy - fly) * (fhy - fly)) + 1e-4f;
+    const float rho2 = rho * rho;
+    const float mf = (float)R + 1e-3f;
+    const float mf2 = mf * mf;
     int nf = 0;
     __syncwarp();
     for (int f0 = 0; f0 < F; f0 += 32) {
       const int f = f0 + lane;
       bool keep = false;
+      double fc[D];
       if (f < F) {
-        keep = true;
-        const double* fp = S.feat + (size_t)f * D;
 #pragma unroll
-        for (int q = 0; q < D; ++q)
-          if (fp[q] > hi[q] + m || fp[q] < lo[q] - m) keep = false;
+        for (int q = 0; q < D; ++q) fc[q] = __ldg(feat + (size_t)f * D + q);
+        const float fx = (float)fc[0], fy = (float)fc[1], fz = (D == 3) ? (float)fc[D - 1] : 0.0f;
+        const float ex = fmaxf(fmaxf(flx - fx, fx - fhx), 0.0f);
+        const float ey = fmaxf(fmaxf(fly - fy, fy - fhy), 0.0f);
+        const float ez = (D == 3) ? fmaxf(fmaxf(flz - fz, fz - fhz), 0.0f) : 0.0f;
+        keep = ex * ex + ey * ey + ez * ez <= mf2;
+        if (keep && ang) {
+          const float dx = fx - ccx, dy = fy - ccy;
+          const float dc2 = dx * dx + dy * dy;
+          if (dc2 > rho2) {
+            const float inv = rsqrtf(dc2);
+            const float sw = rho * inv;
+            if (sw < smax) {
+              const float cw = sqrtf(fmaxf(1.0f - sw * sw, 0.0f));
+              const float cosb = c1 * cw - s1 * sw;            // cos(beta0 + omega)
+              const float dotv = (ux * dx + uy * dy) * inv;      // cos(angle to the centre direction)
+              if (dotv < cosb - 2e-4f) keep = false;
+            }
+          }
+        }
       }
       const unsigned msk = __ballot_sync(FULL, keep);
-      if (keep) S.flist[nf + __popc(msk & lt)] = f;
+      if (keep) {
+        const int pos = nf + __popc(msk & lt);
+#pragma unroll
+        for (int q = 0; q < D; ++q) L.f[q][pos] = fc[q];
+      }
       nf += __popc(msk);
     }
-    __syncwarp();
-    const int nb = (nf > 0) ? cull_boxes<D>(S.box, O, lo, hi, m, S.blist, lane) : 0;
-    if (lane == 0) W.v[W_CULL_TESTS] += F + (nf > 0 ? O : 0);
+    const int nb = (nf > 0) ? cull_boxes<D>(box, O, lo, hi, m, L.box, lane) : 0;
+    W.add(lane, W_CULL_TESTS, F + (nf > 0 ? O : 0));
+    // per kept feature: which of the chunk's boxes meet the box spanned by the
+    // chunk and the feature (every sight line to it lies inside that box)
+    const bool use_mask = nb > 0 && nb <= 64;
+    if (use_mask) {
+      for (int i = lane; i < nf; i += 32) {
+        double fl[D], fh[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+          const double fq = L.f[q][i];
+          fl[q] = fmin(lo[q], fq) - kCullMargin;
+          fh[q] = fmax(hi[q], fq) + kCullMargin;
+        }
+        unsigned long long msk = 0ull;
+        for (int bb = 0; bb < nb; ++bb) {
+          const double* bx = L.box + (size_t)bb * 2 * D;
+          bool sep = false;
+#pragma unroll
+          for (int q = 0; q < D; ++q)
+            if (bx[q] > fh[q] || bx[D + q] < fl[q]) sep = true;
+          if (!sep) msk |= 1ull << bb;
+        }
+        L.fmask[i] = msk;
+      }
+      W.add(lane, W_CULL_TESTS, nf * nb);
+      __syncwarp();
+    }
+    W.add(lane, W_STEPS, nk);
+    W.add(lane, W_RANGE_TESTS, nk * nf);
+    if (heur != 0) W.add(lane, W_FOV_TESTS, nk * nf);
+    if (heur == 3) W.add(lane, W_MLP, nk);
+    const int k = k0 + lane;
     double inc = 0.0;
-    if (act) {
-      ++W.v[W_STEPS];
+    if (k < K) {
+      const double t = (double)k * Dl;
+      double x[D], hv[D];
+      double speed = P.nominal_speed;   // |v(t)| for the MLP (kinematic: nominal)
+#pragma unroll
+      for (int j = 0; j < D; ++j) hv[j] = 0.0;
+      if (DYN == 0) {
+        const double sp = t / T;
+#pragma unroll
+        for (int j = 0; j < D; ++j) x[j] = su[j] + sp * (sv[j] - su[j]);
+        if (heur == 1) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) hv[j] = sv[j] - su[j];
+        }
+      } else {
+        double vel[D];
+        di_pos<D>(su, c2, c3, t, x);
+        di_vel<D>(su, c2, c3, t, vel);
+        if (heur == 3) {
+          double ss = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) ss = ss + vel[j] * vel[j];
+          speed = sqrt(ss);
+        }
+        if (heur == 1) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) hv[j] = vel[j];
+        }
+      }
+      if (heur >= 2) {
+        const double sp = t / T;
+        hv[0] = (1.0 - sp) * hu0 + sp * hv0;
+        hv[1] = (1.0 - sp) * hu1 + sp * hv1;
+      }
       double hh = 0.0;
 #pragma unroll
       for (int j = 0; j < D; ++j) hh = hh + hv[j] * hv[j];
       int kv = 0;
       for (int i = 0; i < nf; ++i) {
-        const double* fp = S.feat + (size_t)S.flist[i] * D;
         double dl[D];
         double dd = 0.0;
 #pragma unroll
-        for (int j = 0; j < D; ++j) { dl[j] = fp[j] - x[j]; dd = dd + dl[j] * dl[j]; }
-        ++W.v[W_RANGE_TESTS];
+        for (int j = 0; j < D; ++j) { dl[j] = L.f[j][i] - x[j]; dd = dd + dl[j] * dl[j]; }
         if (dd > R2) continue;
         if (heur != 0) {
-          ++W.v[W_FOV_TESTS];
           double dot = 0.0;
 #pragma unroll
           for (int j = 0; j < D; ++j) dot = dot + hv[j] * dl[j];
@@ -653,125 +885,134 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
           if (dot < 0.0) continue;
           if (dot * dot < cos2 * (hh * dd)) continue;
         }
-        ++W.v[W_OCCL_SEGS];
-        unsigned tests = 0;
-        const bool occ = seg_hits_boxes<D>(x, fp, dl, S.box, S.blist, nb, tests);
-        W.v[W_OCCL_BOX_TESTS] += tests;
-        if (occ) continue;
-        ++kv;
+        double fp[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) fp[j] = L.f[j][i];
+        ++W.occl_segs;
+        const unsigned rr = use_mask ? seg_hits_boxes<D, true>(x, fp, dl, L.box, nb, L.fmask[i])
+                                     : seg_hits_boxes<D, false>(x, fp, dl, L.box, nb, 0ull);
+        W.occl_tests += rr >> 1;
+        if (!(rr & 1u)) ++kv;
       }
       inc = Dl - (double)kv * (Dl / P.n_f);
       if (heur == 3) {
-        ++W.v[W_MLP];
-        double speed;
-        if (DYN == 1) {
-          double ss = 0.0;
-#pragma unroll
-          for (int j = 0; j < D; ++j) ss = ss + vel[j] * vel[j];
-          speed = sqrt(ss);
-        } else {
-          speed = P.nominal_speed;
-        }
         const double z0 = speed / P.v_ref;
         const double z1 = omega / P.w_ref;
         const double z2 = (double)kv / P.n_f;
-        const double o = mlp_out0(P, z0, z1, z2);
+        const double o = mlp_out0(L.mlp, z0, z1, z2);
         inc = inc + Dl * (P.mlp_gain * o);
       }
     }
-    const int nk = min(32, K - k0);
+    fold[lane] = inc;
+    __syncwarp();
     for (int j = 0; j < nk; ++j) {   // fold in time order (every lane, same values)
-      const double ij = __shfl_sync(FULL, inc, j);
+      const double ij = fold[j];
       const double tt = c + ij;
       c = (tt > 0.0) ? tt : 0.0;
       s = s + ij;
     }
+    __syncwarp();
   }
   s_out = s;
   c_out = c;
 }
 
+// Persistent: each warp pulls rows (over all environments of the batch) from
+// an atomic counter, so no block waits on its slowest row.
 template <int D, int DYN>
-__global__ void __launch_bounds__(kWarps * 32) k_edges(const double* __restrict__ samples,
-                                                       const int64_t* __restrict__ node_base,
-                                                       const int32_t* __restrict__ n_env,
-                                                       const double* __restrict__ obst,
-                                                       const int32_t* __restrict__ obst_base,
-                                                       const double* __restrict__ feat,
-                                                       const int32_t* __restrict__ feat_base, DevParams P,
-                                                       int cap, int o_max, int f_max,
-                                                       const int32_t* __restrict__ cnt,
-                                                       const NearRec* __restrict__ scratch,
-                                                       const int64_t* __restrict__ row_ptr,
-                                                       EdgeRec* __restrict__ edges,
-                                                       unsigned long long* __restrict__ nnz_free,
-                                                       unsigned long long* __restrict__ work) {
+__global__ void __launch_bounds__(kWarps * 32, MPAP_EDGES_MIN_BLOCKS) k_edges(const double* __restrict__ samples,
+                                                          const int64_t* __restrict__ node_base, int B,
+                                                          const double* __restrict__ obst,
+                                                          const int32_t* __restrict__ obst_base,
+                                                          const double* __restrict__ feat,
+                                                          const int32_t* __restrict__ feat_base, DevParams P,
+                                                          int cap, int o_max, int f_max,
+                                                          const int32_t* __restrict__ cnt,
+                                                          const NearRec* __restrict__ scratch,
+                                                          const int64_t* __restrict__ row_ptr,
+                                                          EdgeRec* __restrict__ edges,
+                                                          unsigned long long* __restrict__ nnz_free,
+                                                          unsigned long long* __restrict__ work,
+                                                          unsigned long long* __restrict__ next_row) {
   constexpr int NS = 2 * D + 2;   // p, v (double integrator), heading
   extern __shared__ double smem[];
-  const int b = blockIdx.y;
-  const int O = obst_base[b + 1] - obst_base[b];
-  const int F = feat_base[b + 1] - feat_base[b];
-  double* sbox = smem;
-  double* sfeat = smem + (size_t)o_max * 2 * D;
-  int* lists = reinterpret_cast<int*>(sfeat + (size_t)f_max * D);
-  for (int i = threadIdx.x; i < O * 2 * D; i += blockDim.x) sbox[i] = obst[(size_t)obst_base[b] * 2 * D + i];
-  for (int i = threadIdx.x; i < F * D; i += blockDim.x) sfeat[i] = feat[(size_t)feat_base[b] * D + i];
+  __shared__ double s_state[kWarps][2][NS];
+  __shared__ unsigned s_work[kWarps][W_NUM];
+  __shared__ double s_mlp[kMlpSize];
+  __shared__ double s_fold[kWarps][32];
+  for (int i = threadIdx.x; i < kMlpSize; i += blockDim.x) s_mlp[i] = P.mlp[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nb = n_env[b];
-  const int u = blockIdx.x * kWarps + warp;
-  if (u >= nb) return;
-  EdgeSmem S;
-  S.box = sbox;
-  S.feat = sfeat;
-  S.flist = lists + warp * (f_max + o_max);
-  S.blist = S.flist + f_max;
+  WarpLists<D> L;
+  {
+    double* base = smem + (size_t)warp * ((size_t)f_max * (D + 1) + (size_t)o_max * 2 * D);
+#pragma unroll
+    for (int q = 0; q < D; ++q) L.f[q] = base + (size_t)q * f_max;
+    L.box = base + (size_t)D * f_max;
+    L.fmask = reinterpret_cast<unsigned long long*>(L.box + (size_t)o_max * 2 * D);
+    L.mlp = s_mlp;
+  }
+  const int64_t N = node_base[B];
   const int stride = P.stride;
-  const int64_t row = node_base[b] + u;
-  const double* envs = samples + node_base[b] * stride;
-  double su[NS], sv[NS];
-#pragma unroll
-  for (int j = 0; j < NS; ++j) su[j] = (j < stride) ? envs[(int64_t)u * stride + j] : 0.0;
-  const int deg = min(cnt[row], cap);
-  const int64_t e0 = row_ptr[row];
-  int nfree = 0;
   Work W;
-#pragma unroll
-  for (int i = 0; i < W_NUM; ++i) W.v[i] = 0;
-  for (int j = 0; j < deg; ++j) {
-    const NearRec rec = scratch[row * (int64_t)cap + j];
-#pragma unroll
-    for (int q = 0; q < NS; ++q) sv[q] = (q < stride) ? envs[(int64_t)rec.v * stride + q] : 0.0;
-    const bool coll = edge_collision<D, DYN>(P, su, sv, rec.tau, S, O, lane, W);
-    float s32 = 0.0f, c32 = 0.0f;
-    if (!coll) {
-      double s64, c64;
-      edge_heuristic<D, DYN>(P, su, sv, rec.tau, S, O, F, lane, s64, c64, W);
-      s32 = (float)s64;
-      c32 = (float)c64;
-      ++nfree;
+  W.sm = s_work[warp];
+  W.occl_segs = W.occl_tests = W.coll_segs = W.coll_tests = 0;
+  if (lane < W_NUM) W.sm[lane] = 0;
+  double* su = s_state[warp][0];
+  double* sv = s_state[warp][1];
+  __syncwarp();
+  for (;;) {
+    unsigned long long rr = 0;
+    if (lane == 0) rr = atomicAdd(next_row, 1ull);
+    const int64_t row = (int64_t)__shfl_sync(FULL, rr, 0);
+    if (row >= N) break;
+    int lo_b = 0, hi_b = B;   // env = last b with node_base[b] <= row
+    while (hi_b - lo_b > 1) {
+      const int mid = (lo_b + hi_b) >> 1;
+      if (node_base[mid] <= row) lo_b = mid; else hi_b = mid;
     }
-    if (lane == 0) {
-      EdgeRec er;
-      er.dst_coll = (uint32_t)rec.v | (coll ? 0x80000000u : 0u);
-      er.w = rec.w;
-      er.s = s32;
-      er.c = c32;
-      edges[e0 + j] = er;
-    }
+    const int b = lo_b;
+    const int64_t u = row - node_base[b];
+    const int O = obst_base[b + 1] - obst_base[b];
+    const int F = feat_base[b + 1] - feat_base[b];
+    const double* ebox = obst + (size_t)obst_base[b] * 2 * D;
+    const double* efeat = feat + (size_t)feat_base[b] * D;
+    const double* envs = samples + node_base[b] * stride;
     __syncwarp();
+    if (lane < NS) su[lane] = (lane < stride) ? envs[u * stride + lane] : 0.0;
+    const int deg = min(cnt[row], cap);
+    const int64_t e0 = row_ptr[row];
+    int nfree = 0;
+    for (int j = 0; j < deg; ++j) {
+      const NearRec rec = scratch[row * (int64_t)cap + j];
+      __syncwarp();
+      if (lane < NS) sv[lane] = (lane < stride) ? envs[(int64_t)rec.v * stride + lane] : 0.0;
+      __syncwarp();
+      const bool coll = edge_collision<D, DYN>(P, su, sv, rec.tau, ebox, O, L, lane, W);
+      float s32 = 0.0f, c32 = 0.0f;
+      if (!coll) {
+        double s64, c64;
+        edge_heuristic<D, DYN>(P, su, sv, rec.tau, efeat, F, ebox, O, L, s_fold[warp], lane, s64, c64, W);
+        s32 = (float)s64;
+        c32 = (float)c64;
+        ++nfree;
+      }
+      W.flush(lane);
+      if (lane == 0) {
+        EdgeRec er;
+        er.dst_coll = (uint32_t)rec.v | (coll ? 0x80000000u : 0u);
+        er.w = rec.w;
+        er.s = s32;
+        er.c = c32;
+        edges[e0 + j] = er;
+      }
+    }
+    W.add(lane, W_EDGES, deg);
+    W.add(lane, W_FREE_EDGES, nfree);
+    if (lane == 0 && nfree) atomicAdd(&nnz_free[b], (unsigned long long)nfree);
   }
-  if (lane == 0) {
-    W.v[W_EDGES] = deg;
-    W.v[W_FREE_EDGES] = nfree;
-  }
-  if (lane == 0 && nfree) atomicAdd(&nnz_free[b], (unsigned long long)nfree);
-#pragma unroll
-  for (int i = W_EDGES; i < W_NUM; ++i) {
-    unsigned x = W.v[i];
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
-    if (lane == 0 && x) atomicAdd(&work[i], (unsigned long long)x);
-  }
+  __syncwarp();
+  if (lane >= W_EDGES && lane < W_NUM && W.sm[lane]) atomicAdd(&work[lane], (unsigned long long)W.sm[lane]);
 }
 
 // ---------------------------------------------------------------------------
@@ -793,16 +1034,24 @@ cudaError_t launch_near(dim3 grid, cudaStream_t st, const mpap_roadmap* rm, cons
 }
 
 template <int D, int DYN>
-cudaError_t launch_edges(dim3 grid, size_t smem, cudaStream_t st, const mpap_roadmap* rm, const int32_t* d_n,
-                         int cap, const int32_t* d_cnt, const NearRec* d_scr, unsigned long long* d_free,
-                         unsigned long long* d_work) {
+cudaError_t launch_edges(size_t smem, cudaStream_t st, const mpap_roadmap* rm, int cap, const int32_t* d_cnt,
+                         const NearRec* d_scr, unsigned long long* d_free, unsigned long long* d_work,
+                         unsigned long long* d_next) {
   cudaError_t e = cudaFuncSetAttribute(k_edges<D, DYN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)std::max<size_t>(smem, 1));
   if (e != cudaSuccess) return e;
-  k_edges<D, DYN><<<grid, kWarps * 32, smem, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->d_obst,
+  int dev = 0, nsm = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_edges<D, DYN>, kWarps * 32, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t N = rm->node_base[rm->B];
+  const int64_t need = (N + kWarps - 1) / kWarps;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(per_sm, 1), need));
+  k_edges<D, DYN><<<grid, kWarps * 32, smem, st>>>(rm->d_samples, rm->d_node_base, rm->B, rm->d_obst,
                                                    rm->d_obst_base, rm->d_feat, rm->d_feat_base, rm->prm, cap,
                                                    rm->o_max, rm->f_max, d_cnt, d_scr, rm->d_row_ptr, rm->d_edges,
-                                                   d_free, d_work);
+                                                   d_free, d_work, d_next);
   return cudaGetLastError();
 }
 }  // namespace
@@ -831,13 +1080,9 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
   CK(cudaMallocAsync(&rm->d_row_ptr, sizeof(int64_t) * (N + 1), st));
   const dim3 grid((rm->n_max + kWarps - 1) / kWarps, B);
   for (int attempt = 0; attempt < 8; ++attempt) {
-    if (d_scr) CK(cudaFreeAsync(d_scr, st));
     const size_t bytes = sizeof(NearRec) * (size_t)N * (size_t)cap;
-    if (cudaMallocAsync(&d_scr, bytes, st) != cudaSuccess) {
-      d_scr = nullptr;
-      cudaGetLastError();
-      return set_error(MPAP_ERR_OUT_OF_MEMORY, "neighbour scratch allocation failed");
-    }
+    d_scr = static_cast<NearRec*>(workspace(st, WS_NEAR, bytes));
+    if (!d_scr) return set_error(MPAP_ERR_OUT_OF_MEMORY, "neighbour scratch allocation failed");
     CK(cudaMemsetAsync(d_over, 0, sizeof(int), st));
     CK(cudaMemsetAsync(d_work, 0, sizeof(unsigned long long) * 3, st));
     {
@@ -874,16 +1119,18 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
     cudaGetLastError();
     return set_error(MPAP_ERR_OUT_OF_MEMORY, "edge array allocation failed");
   }
-  const size_t smem = sizeof(double) * ((size_t)rm->o_max * 2 * d + (size_t)rm->f_max * d) +
-                      sizeof(int) * (size_t)kWarps * (rm->f_max + rm->o_max);
+  const size_t smem = sizeof(double) * (size_t)kWarps * ((size_t)rm->f_max * (d + 1) + (size_t)rm->o_max * 2 * d);
+  unsigned long long* d_next = nullptr;
+  CK(cudaMallocAsync(&d_next, sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(d_next, 0, sizeof(unsigned long long), st));
   if (rm->nnz_total > 0) {
     {
       ProfScope ps("k_edges", st);
       cudaError_t e;
-      if (d == 2) e = dyn ? launch_edges<2, 1>(grid, smem, st, rm, d_n, cap, d_cnt, d_scr, d_free, d_work)
-                          : launch_edges<2, 0>(grid, smem, st, rm, d_n, cap, d_cnt, d_scr, d_free, d_work);
-      else e = dyn ? launch_edges<3, 1>(grid, smem, st, rm, d_n, cap, d_cnt, d_scr, d_free, d_work)
-                   : launch_edges<3, 0>(grid, smem, st, rm, d_n, cap, d_cnt, d_scr, d_free, d_work);
+      if (d == 2) e = dyn ? launch_edges<2, 1>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next)
+                          : launch_edges<2, 0>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next);
+      else e = dyn ? launch_edges<3, 1>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next)
+                   : launch_edges<3, 0>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next);
       CK(e);
     }
     note_launch();
@@ -891,11 +1138,11 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
   std::vector<unsigned long long> fr(B);
   CK(cudaMemcpyAsync(fr.data(), d_free, sizeof(unsigned long long) * B, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(rm->work, d_work, sizeof(unsigned long long) * W_NUM, cudaMemcpyDeviceToHost, st));
-  CK(cudaFreeAsync(d_scr, st));
   CK(cudaFreeAsync(d_cnt, st));
   CK(cudaFreeAsync(d_over, st));
   CK(cudaFreeAsync(d_free, st));
   CK(cudaFreeAsync(d_work, st));
+  CK(cudaFreeAsync(d_next, st));
   CK(cudaFreeAsync(d_n, st));
   CK(cudaStreamSynchronize(st));
   rm->nnz_free.assign(fr.begin(), fr.end());

@@ -20,6 +20,38 @@ static std::atomic<long long> g_launches{0};
 
 void note_launch(int k) { g_launches.fetch_add(k); }
 
+void* workspace(cudaStream_t st, int tag, size_t bytes) {
+  struct Key {
+    int dev;
+    cudaStream_t st;
+    int tag;
+    bool operator<(const Key& o) const {
+      if (dev != o.dev) return dev < o.dev;
+      if (st != o.st) return st < o.st;
+      return tag < o.tag;
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, std::pair<void*, size_t>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto& e = cache[Key{dev, st, tag}];
+  if (e.second >= bytes && e.first) return e.first;
+  if (e.first) cudaFreeAsync(e.first, st);
+  e.first = nullptr;
+  e.second = 0;
+  const size_t grow = bytes + bytes / 4;   // headroom against small size changes
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, grow, st) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  e.first = p;
+  e.second = grow;
+  return p;
+}
+
 void retain_pool_memory(int device) {
   static std::mutex mu;
   static std::vector<int> done;

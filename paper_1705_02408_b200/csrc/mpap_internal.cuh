@@ -83,6 +83,11 @@ struct ProfScope {
 mpap_status set_error(mpap_status s, const std::string& msg);
 // keeps freed stream-ordered memory in the device pool (no OS round trip per call)
 void retain_pool_memory(int device);
+// Per-(device, stream, tag) scratch workspace that only grows: repeated calls
+// on one stream reuse it (stream order serialises them); other streams get
+// their own.  Returns nullptr on allocation failure.
+void* workspace(cudaStream_t st, int tag, size_t bytes);
+enum { WS_NEAR = 0, WS_SEARCH = 1 };
 mpap_status cuda_error(cudaError_t e, const char* what);
 
 // roadmap build (build_kernels.cu)

@@ -29,7 +29,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -629,10 +632,29 @@ size_t carve(SearchArgs* A, const SlotCaps& c, int nslots, char* base) {
 }
 }  // namespace
 
+namespace {
+struct HostTimer {
+  const char* what;
+  std::chrono::steady_clock::time_point t0;
+  static bool on() {
+    static int v = -1;
+    if (v < 0) v = getenv("MPAP_DEBUG_TIMING") ? 1 : 0;
+    return v == 1;
+  }
+  explicit HostTimer(const char* w) : what(w), t0(std::chrono::steady_clock::now()) {}
+  ~HostTimer() {
+    if (on())
+      fprintf(stderr, "[mpap] %s %.3f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+}  // namespace
+
 mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryDesc* h_queries, double lambda,
                                 int32_t* paths, int32_t path_cap, mpap_result* results, mpap_wave* h_waves,
                                 int32_t waves_cap, int32_t mem, cudaStream_t st) {
   if (nq <= 0) return MPAP_OK;
+  HostTimer total("search_batch_device total");
   int dev = 0, nsm = 0;
   CKS(cudaGetDevice(&dev));
   CKS(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -676,9 +698,9 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     const int nrun = (int)todo.size();
     const int nslots = std::min(nrun, nsm * occ);
     const size_t sb = carve(nullptr, caps, nslots, nullptr);
-    void* base = nullptr;
-    if (cudaMallocAsync(&base, sb, st) != cudaSuccess) {
-      cudaGetLastError();
+    HostTimer ta("slot arena");
+    void* base = workspace(st, WS_SEARCH, sb);
+    if (!base) {
       status = set_error(MPAP_ERR_OUT_OF_MEMORY, "search slot allocation failed");
       break;
     }
@@ -716,10 +738,12 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     }
     note_launch();
     CKS(cudaGetLastError());
-    CKS(cudaFreeAsync(base, st));
     CKS(cudaFreeAsync(d_nenv, st));
     CKS(cudaMemcpyAsync(hres.data(), d_res, sizeof(mpap_result) * nq, cudaMemcpyDeviceToHost, st));
-    CKS(cudaStreamSynchronize(st));
+    {
+      HostTimer tsync("search sync");
+      CKS(cudaStreamSynchronize(st));
+    }
     std::vector<int32_t> again;
     int mask = 0;
     for (int k : todo) {
