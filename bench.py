@@ -123,9 +123,10 @@ def load_peaks():
 # ---------------------------------------------------------------------------
 # workload
 # ---------------------------------------------------------------------------
-def make_shard(cfg, rank: int, Q: int):
+def make_shard(cfg, rank: int, world: int, Q: int):
+    from paper_1705_02408_b200.dist import shard_envs
     from synth import make_problem
-    return [make_problem(cfg, env_index=rank * Q + k) for k in range(Q)]
+    return [make_problem(cfg, env_index=e) for e in shard_envs(rank, world, Q)]
 
 
 def cpu_baseline(cfg, beta: float, procs: int):
@@ -210,10 +211,11 @@ def main():
     if world > 1:
         dist.barrier()
     import paper_1705_02408_b200 as mp
+    from paper_1705_02408_b200.dist import gather_results
     from paper_1705_02408_b200.problem import Batch
 
     Q = args.queries_per_gpu or int(cfg.get("queries_per_gpu", 64))
-    probs = make_shard(cfg, rank, Q)
+    probs = make_shard(cfg, rank, world, Q)
     B = Batch(probs)
     betas = [beta] * Q
     PATH_CAP = 512
@@ -222,7 +224,6 @@ def main():
     f_d = torch.from_numpy(B.features).to(dev)
     paths_d = torch.zeros((Q, PATH_CAP), dtype=torch.int32, device=dev)
     res_d = torch.zeros(Q * 48, dtype=torch.uint8, device=dev)
-    gather_d = torch.zeros(world * Q * 48, dtype=torch.uint8, device=dev) if world > 1 else None
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -232,7 +233,7 @@ def main():
         rm = B.build(s_d, o_d, f_d)
         B.search(rm, betas, path_capacity=PATH_CAP, paths=paths_d, results=res_d)
         if world > 1:
-            dist.all_gather_into_tensor(gather_d, res_d)
+            gather_results(res_d, world)
         last_work.update(mp.mpap_roadmap_work(rm))
         rm.free()
 

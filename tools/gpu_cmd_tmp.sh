@@ -1,2 +1,3 @@
-for v in b1 b2; do MPAP_LIB=paper_1705_02408_b200/libmpap_$v.so timeout 300 python tools/bench_build.py 64 3 2>&1 | tail -1 | cut -c1-400; done
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -3
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench3.json 2> gpurun_out/bench3.err; echo bench=$?; cat gpurun_out/bench3.json; tail -3 gpurun_out/bench3.err
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/plain_launch.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r1b.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1; echo ncu=$?
