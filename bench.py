@@ -363,11 +363,12 @@ def main():
 def fp64_ops(kernel: str, w: dict, D: int = 3) -> float:
     if kernel == "k_near":
         return 18 * w["pairs"] + 101 * w["prefilter_pass"] + 9 * w["bisect_iters"]
-    if kernel == "k_edges":
+    if kernel == "k_collide":
+        return (12 * D + 2 * D + 4) * w["coll_segs"] + 4 * D * w["coll_box_tests"] + 27 * w["edges"]
+    if kernel == "k_heuristic":
         per_step = 1 + 12 * D + 8 + 2 * D + 6
         return (per_step * w["steps"] + 205 * w["mlp"] + 3 * D * w["range_tests"] + (2 * D + 3) * w["fov_tests"]
-                + D * w["occl_segs"] + 4 * D * w["occl_box_tests"] + (12 * D + 2 * D + 4) * w["coll_segs"]
-                + 4 * D * w["coll_box_tests"] + 2 * D * w["cull_tests"] + 40 * w["free_edges"])
+                + D * w["occl_segs"] + 4 * D * w["occl_box_tests"] + 40 * w["free_edges"])
     return 0.0
 
 

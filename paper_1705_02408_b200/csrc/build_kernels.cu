@@ -918,9 +918,15 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
 }
 
 // Persistent: each warp pulls rows (over all environments of the batch) from
-// an atomic counter, so no block waits on its slowest row.
-template <int D, int DYN>
-__global__ void __launch_bounds__(kWarps * 32, MPAP_EDGES_MIN_BLOCKS) k_edges(const double* __restrict__ samples,
+// an atomic counter, so no block waits on its slowest row.  PHASE 0 computes
+// the collision bit of every r-disc entry and writes the edge records; PHASE 1
+// fills the heuristic summary (s, c) of the collision-free ones.  Two kernels
+// keep each one's code and register footprint small.
+template <int PHASE>
+struct EdgeBounds { static constexpr int kMin = (PHASE == 0) ? 2 : MPAP_EDGES_MIN_BLOCKS; };
+
+template <int D, int DYN, int PHASE>
+__global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(const double* __restrict__ samples,
                                                           const int64_t* __restrict__ node_base, int B,
                                                           const double* __restrict__ obst,
                                                           const int32_t* __restrict__ obst_base,
@@ -984,32 +990,40 @@ __global__ void __launch_bounds__(kWarps * 32, MPAP_EDGES_MIN_BLOCKS) k_edges(co
     const int64_t e0 = row_ptr[row];
     int nfree = 0;
     for (int j = 0; j < deg; ++j) {
-      const NearRec rec = scratch[row * (int64_t)cap + j];
-      __syncwarp();
-      if (lane < NS) sv[lane] = (lane < stride) ? envs[(int64_t)rec.v * stride + lane] : 0.0;
-      __syncwarp();
-      const bool coll = edge_collision<D, DYN>(P, su, sv, rec.tau, ebox, O, L, lane, W);
-      float s32 = 0.0f, c32 = 0.0f;
-      if (!coll) {
+      if constexpr (PHASE == 0) {
+        const NearRec rec = scratch[row * (int64_t)cap + j];
+        __syncwarp();
+        if (lane < NS) sv[lane] = (lane < stride) ? envs[(int64_t)rec.v * stride + lane] : 0.0;
+        __syncwarp();
+        const bool coll = edge_collision<D, DYN>(P, su, sv, rec.tau, ebox, O, L, lane, W);
+        nfree += coll ? 0 : 1;
+        W.flush(lane);
+        if (lane == 0) {
+          EdgeRec er;
+          er.dst_coll = (uint32_t)rec.v | (coll ? 0x80000000u : 0u);
+          er.w = rec.w;
+          er.s = 0.0f;
+          er.c = 0.0f;
+          edges[e0 + j] = er;
+        }
+      } else {
+        const uint32_t dc = edges[e0 + j].dst_coll;
+        if (dc >> 31) continue;   // colliding edges keep s = c = 0 (never relaxed)
+        const NearRec rec = scratch[row * (int64_t)cap + j];
+        __syncwarp();
+        if (lane < NS) sv[lane] = (lane < stride) ? envs[(int64_t)rec.v * stride + lane] : 0.0;
+        __syncwarp();
         double s64, c64;
         edge_heuristic<D, DYN>(P, su, sv, rec.tau, efeat, F, ebox, O, L, s_fold[warp], lane, s64, c64, W);
-        s32 = (float)s64;
-        c32 = (float)c64;
-        ++nfree;
-      }
-      W.flush(lane);
-      if (lane == 0) {
-        EdgeRec er;
-        er.dst_coll = (uint32_t)rec.v | (coll ? 0x80000000u : 0u);
-        er.w = rec.w;
-        er.s = s32;
-        er.c = c32;
-        edges[e0 + j] = er;
+        W.flush(lane);
+        if (lane == 0) *reinterpret_cast<float2*>(&edges[e0 + j].s) = make_float2((float)s64, (float)c64);
       }
     }
-    W.add(lane, W_EDGES, deg);
-    W.add(lane, W_FREE_EDGES, nfree);
-    if (lane == 0 && nfree) atomicAdd(&nnz_free[b], (unsigned long long)nfree);
+    if (PHASE == 0) {
+      W.add(lane, W_EDGES, deg);
+      W.add(lane, W_FREE_EDGES, nfree);
+      if (lane == 0 && nfree) atomicAdd(&nnz_free[b], (unsigned long long)nfree);
+    }
   }
   __syncwarp();
   if (lane >= W_EDGES && lane < W_NUM && W.sm[lane]) atomicAdd(&work[lane], (unsigned long long)W.sm[lane]);
@@ -1033,30 +1047,39 @@ cudaError_t launch_near(dim3 grid, cudaStream_t st, const mpap_roadmap* rm, cons
   return cudaGetLastError();
 }
 
-template <int D, int DYN>
-cudaError_t launch_edges(size_t smem, cudaStream_t st, const mpap_roadmap* rm, int cap, const int32_t* d_cnt,
-                         const NearRec* d_scr, unsigned long long* d_free, unsigned long long* d_work,
-                         unsigned long long* d_next) {
-  cudaError_t e = cudaFuncSetAttribute(k_edges<D, DYN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <int D, int DYN, int PHASE>
+cudaError_t launch_edges_phase(size_t smem, cudaStream_t st, const mpap_roadmap* rm, int cap, const int32_t* d_cnt,
+                               const NearRec* d_scr, unsigned long long* d_free, unsigned long long* d_work,
+                               unsigned long long* d_next) {
+  cudaError_t e = cudaFuncSetAttribute(k_edges<D, DYN, PHASE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)std::max<size_t>(smem, 1));
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_edges<D, DYN>, kWarps * 32, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_edges<D, DYN, PHASE>, kWarps * 32, smem);
   if (e != cudaSuccess) return e;
   const int64_t N = rm->node_base[rm->B];
   const int64_t need = (N + kWarps - 1) / kWarps;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(per_sm, 1), need));
-  k_edges<D, DYN><<<grid, kWarps * 32, smem, st>>>(rm->d_samples, rm->d_node_base, rm->B, rm->d_obst,
-                                                   rm->d_obst_base, rm->d_feat, rm->d_feat_base, rm->prm, cap,
-                                                   rm->o_max, rm->f_max, d_cnt, d_scr, rm->d_row_ptr, rm->d_edges,
-                                                   d_free, d_work, d_next);
+  k_edges<D, DYN, PHASE><<<grid, kWarps * 32, smem, st>>>(rm->d_samples, rm->d_node_base, rm->B, rm->d_obst,
+                                                          rm->d_obst_base, rm->d_feat, rm->d_feat_base, rm->prm,
+                                                          cap, rm->o_max, rm->f_max, d_cnt, d_scr, rm->d_row_ptr,
+                                                          rm->d_edges, d_free, d_work, d_next);
   return cudaGetLastError();
+}
+
+template <int D, int DYN>
+cudaError_t launch_edges(int phase, size_t smem, cudaStream_t st, const mpap_roadmap* rm, int cap,
+                         const int32_t* d_cnt, const NearRec* d_scr, unsigned long long* d_free,
+                         unsigned long long* d_work, unsigned long long* d_next) {
+  return phase == 0 ? launch_edges_phase<D, DYN, 0>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next)
+                    : launch_edges_phase<D, DYN, 1>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next + 1);
 }
 }  // namespace
 
 mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
+  HostTimer total("build_roadmap_device total");
   const int B = rm->B;
   const int64_t N = rm->node_base[B];
   const int d = rm->prm.pos_dim;
@@ -1097,10 +1120,14 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
     note_launch();
     int over = 0;
     CK(cudaMemcpyAsync(&over, d_over, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    {
+      HostTimer tn("near sync");
+      CK(cudaStreamSynchronize(st));
+    }
     if (over == 0) break;
     cap = ((over + 31) / 32) * 32;   // exact regrow: re-run with room for the widest row
   }
+  HostTimer tnear_done("after near loop -> end");
   {
     ProfScope ps("k_scan", st);
     k_scan<<<1, 1024, 0, st>>>(d_cnt, N, rm->d_row_ptr);
@@ -1112,28 +1139,32 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
     CK(cudaMemcpyAsync(&bounds[b], rm->d_row_ptr + rm->node_base[b], sizeof(int64_t), cudaMemcpyDeviceToHost,
                        st));
   }
-  CK(cudaStreamSynchronize(st));
+  {
+    HostTimer tb("bounds sync");
+    CK(cudaStreamSynchronize(st));
+  }
   rm->edge_base = bounds;
   rm->nnz_total = bounds[B];
+  HostTimer te("edges alloc");
   if (cudaMallocAsync(&rm->d_edges, sizeof(EdgeRec) * std::max<int64_t>(rm->nnz_total, 1), st) != cudaSuccess) {
     cudaGetLastError();
     return set_error(MPAP_ERR_OUT_OF_MEMORY, "edge array allocation failed");
   }
   const size_t smem = sizeof(double) * (size_t)kWarps * ((size_t)rm->f_max * (d + 1) + (size_t)rm->o_max * 2 * d);
   unsigned long long* d_next = nullptr;
-  CK(cudaMallocAsync(&d_next, sizeof(unsigned long long), st));
-  CK(cudaMemsetAsync(d_next, 0, sizeof(unsigned long long), st));
+  CK(cudaMallocAsync(&d_next, 2 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(d_next, 0, 2 * sizeof(unsigned long long), st));
   if (rm->nnz_total > 0) {
-    {
-      ProfScope ps("k_edges", st);
+    for (int phase = 0; phase < 2; ++phase) {
+      ProfScope ps(phase == 0 ? "k_collide" : "k_heuristic", st);
       cudaError_t e;
-      if (d == 2) e = dyn ? launch_edges<2, 1>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next)
-                          : launch_edges<2, 0>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next);
-      else e = dyn ? launch_edges<3, 1>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next)
-                   : launch_edges<3, 0>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next);
+      if (d == 2) e = dyn ? launch_edges<2, 1>(phase, smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next)
+                          : launch_edges<2, 0>(phase, smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next);
+      else e = dyn ? launch_edges<3, 1>(phase, smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next)
+                   : launch_edges<3, 0>(phase, smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next);
       CK(e);
+      note_launch();
     }
-    note_launch();
   }
   std::vector<unsigned long long> fr(B);
   CK(cudaMemcpyAsync(fr.data(), d_free, sizeof(unsigned long long) * B, cudaMemcpyDeviceToHost, st));
@@ -1144,7 +1175,10 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
   CK(cudaFreeAsync(d_work, st));
   CK(cudaFreeAsync(d_next, st));
   CK(cudaFreeAsync(d_n, st));
-  CK(cudaStreamSynchronize(st));
+  {
+    HostTimer tf("final sync");
+    CK(cudaStreamSynchronize(st));
+  }
   rm->nnz_free.assign(fr.begin(), fr.end());
   return MPAP_OK;
 }

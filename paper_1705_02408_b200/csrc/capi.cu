@@ -254,6 +254,7 @@ mpap_status mpap_build_roadmap_batch(int32_t n_envs, const double* samples, cons
         if (!(obstacles[o * 2 * d + k] < obstacles[o * 2 * d + d + k]))
           return set_error(MPAP_ERR_INVALID_ARGUMENT, "obstacle with lo >= hi");
   }
+  HostTimer tall("mpap_build_roadmap_batch total");
   mpap_roadmap* rm = new (std::nothrow) mpap_roadmap();
   if (!rm) return set_error(MPAP_ERR_OUT_OF_MEMORY, "host allocation failed");
   CKC(cudaGetDevice(&rm->device));

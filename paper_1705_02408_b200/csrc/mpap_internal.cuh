@@ -5,6 +5,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -68,6 +71,23 @@ struct mpap_roadmap {
 };
 
 namespace mpap {
+// MPAP_DEBUG_TIMING=1 prints host-side phase times to stderr (tuning aid).
+struct HostTimer {
+  const char* what;
+  std::chrono::steady_clock::time_point t0;
+  static bool on() {
+    static int v = -1;
+    if (v < 0) v = getenv("MPAP_DEBUG_TIMING") ? 1 : 0;
+    return v == 1;
+  }
+  explicit HostTimer(const char* w) : what(w), t0(std::chrono::steady_clock::now()) {}
+  ~HostTimer() {
+    if (on())
+      fprintf(stderr, "[mpap] %s %.3f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+
 // launch bookkeeping shared by the translation units (host side)
 void note_launch(int k = 1);
 

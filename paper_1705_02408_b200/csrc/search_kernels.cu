@@ -632,23 +632,6 @@ size_t carve(SearchArgs* A, const SlotCaps& c, int nslots, char* base) {
 }
 }  // namespace
 
-namespace {
-struct HostTimer {
-  const char* what;
-  std::chrono::steady_clock::time_point t0;
-  static bool on() {
-    static int v = -1;
-    if (v < 0) v = getenv("MPAP_DEBUG_TIMING") ? 1 : 0;
-    return v == 1;
-  }
-  explicit HostTimer(const char* w) : what(w), t0(std::chrono::steady_clock::now()) {}
-  ~HostTimer() {
-    if (on())
-      fprintf(stderr, "[mpap] %s %.3f ms\n", what,
-              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-  }
-};
-}  // namespace
 
 mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryDesc* h_queries, double lambda,
                                 int32_t* paths, int32_t path_cap, mpap_result* results, mpap_wave* h_waves,

@@ -1,3 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -3
-timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench3.json 2> gpurun_out/bench3.err; echo bench=$?; cat gpurun_out/bench3.json; tail -3 gpurun_out/bench3.err
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/plain_launch.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r1b.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1; echo ncu=$?
+MPAP_DEBUG_TIMING=1 timeout 300 python tools/bench_build.py 64 2 2>&1 | tail -30 | cut -c1-300
