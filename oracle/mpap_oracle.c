@@ -23,8 +23,10 @@
  * "parity unpinned".
  *
  * Compile: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared
- * (no FMA contraction, no fast-math: every + - * / sqrt is one correctly
- * rounded IEEE-754 binary64 / binary32 operation, N2/N5).
+ * (no implicit FMA contraction, no fast-math: every + - * / sqrt is one
+ * correctly rounded IEEE-754 binary64 / binary32 operation, and the explicit
+ * fma() calls the contract writes are single correctly rounded fused
+ * operations, N2/N5).
  */
 #include <math.h>
 #include <stdint.h>
@@ -221,12 +223,12 @@ static void di_traj(const double *su, const double *sv, int d, double tau, doubl
 
 static void di_pos(const double *su, const double *c2, const double *c3, int d, double t, double *x) {
   const double *p0 = su, *v0 = su + d;
-  for (int j = 0; j < d; ++j) x[j] = p0[j] + t * (v0[j] + t * (c2[j] + t * c3[j]));
+  for (int j = 0; j < d; ++j) x[j] = fma(t, fma(t, fma(t, c3[j], c2[j]), v0[j]), p0[j]);
 }
 
 static void di_vel(const double *su, const double *c2, const double *c3, int d, double t, double *v) {
   const double *v0 = su + d;
-  for (int j = 0; j < d; ++j) v[j] = v0[j] + t * (2.0 * c2[j] + t * (3.0 * c3[j]));
+  for (int j = 0; j < d; ++j) v[j] = fma(t, fma(t, 3.0 * c3[j], 2.0 * c2[j]), v0[j]);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -272,12 +274,12 @@ int orc_visible_count(const orc_env *E, const orc_params *prm, const double *x, 
     const double *F = E->features + (size_t)f * d;
     double dl[3];
     double dd = 0.0;
-    for (int j = 0; j < d; ++j) { dl[j] = F[j] - x[j]; dd = dd + dl[j] * dl[j]; }
+    for (int j = 0; j < d; ++j) { dl[j] = F[j] - x[j]; dd = fma(dl[j], dl[j], dd); }
     if (dd > R2) continue;                                   /* in range */
     if (prm->heuristic != 0) {                               /* in FOV cone */
       double hh = 0.0, dot = 0.0;
-      for (int j = 0; j < d; ++j) hh = hh + hv[j] * hv[j];
-      for (int j = 0; j < d; ++j) dot = dot + hv[j] * dl[j];
+      for (int j = 0; j < d; ++j) hh = fma(hv[j], hv[j], hh);
+      for (int j = 0; j < d; ++j) dot = fma(hv[j], dl[j], dot);
       if (!(hh > 0.0)) continue;
       if (dot < 0.0) continue;
       if (dot * dot < cos2 * (hh * dd)) continue;
@@ -294,18 +296,18 @@ static double mlp_out0(const double *w, double z0, double z1, double z2) {
   double h1[8], h2[8];
   for (int i = 0; i < 8; ++i) {
     double a = b1[i];
-    a = a + W1[i * 3 + 0] * z0;
-    a = a + W1[i * 3 + 1] * z1;
-    a = a + W1[i * 3 + 2] * z2;
+    a = fma(W1[i * 3 + 0], z0, a);
+    a = fma(W1[i * 3 + 1], z1, a);
+    a = fma(W1[i * 3 + 2], z2, a);
     h1[i] = (a > 0.0) ? a : 0.0;
   }
   for (int i = 0; i < 8; ++i) {
     double a = b2[i];
-    for (int j = 0; j < 8; ++j) a = a + W2[i * 8 + j] * h1[j];
+    for (int j = 0; j < 8; ++j) a = fma(W2[i * 8 + j], h1[j], a);
     h2[i] = (a > 0.0) ? a : 0.0;
   }
   double o = b3[0];
-  for (int j = 0; j < 8; ++j) o = o + W3[0 * 8 + j] * h2[j];
+  for (int j = 0; j < 8; ++j) o = fma(W3[0 * 8 + j], h2[j], o);
   return o;
 }
 
@@ -333,7 +335,7 @@ int orc_edge_increments(const orc_env *E, const orc_params *prm, int u, int v,
     double x[3], hv[3] = {0, 0, 0}, vel[3] = {0, 0, 0};
     if (prm->dynamics == 0) {
       double s = t / T;
-      for (int j = 0; j < d; ++j) x[j] = su[j] + s * (sv[j] - su[j]);
+      for (int j = 0; j < d; ++j) x[j] = fma(s, sv[j] - su[j], su[j]);
     } else {
       di_pos(su, c2, c3, d, t, x);
       di_vel(su, c2, c3, d, t, vel);
@@ -343,8 +345,8 @@ int orc_edge_increments(const orc_env *E, const orc_params *prm, int u, int v,
       else { for (int j = 0; j < d; ++j) hv[j] = sv[j] - su[j]; }
     } else if (prm->heuristic >= 2) {
       double s = t / T;
-      hv[0] = (1.0 - s) * su[hoff] + s * sv[hoff];
-      hv[1] = (1.0 - s) * su[hoff + 1] + s * sv[hoff + 1];
+      hv[0] = fma(s, sv[hoff], (1.0 - s) * su[hoff]);
+      hv[1] = fma(s, sv[hoff + 1], (1.0 - s) * su[hoff + 1]);
       if (d == 3) hv[2] = 0.0;
     }
     int kv = orc_visible_count(E, prm, x, hv);
@@ -353,7 +355,7 @@ int orc_edge_increments(const orc_env *E, const orc_params *prm, int u, int v,
       double speed;
       if (prm->dynamics == 1) {
         double ss = 0.0;
-        for (int j = 0; j < d; ++j) ss = ss + vel[j] * vel[j];
+        for (int j = 0; j < d; ++j) ss = fma(vel[j], vel[j], ss);
         speed = sqrt(ss);
       } else {
         speed = prm->nominal_speed;

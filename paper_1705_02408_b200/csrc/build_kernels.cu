@@ -35,8 +35,11 @@
 namespace mpap {
 
 #define FULL 0xffffffffu
+#ifndef MPAP_LAZY_INV
+#define MPAP_LAZY_INV 0
+#endif
 #ifndef MPAP_EDGES_MIN_BLOCKS
-#define MPAP_EDGES_MIN_BLOCKS 1
+#define MPAP_EDGES_MIN_BLOCKS 2
 #endif
 constexpr int kWarps = 8;                 // warps per block in the build kernels
 constexpr double kCullMargin = 1e-6;      // absolute; >> rounding of O(100) coordinates
@@ -190,13 +193,13 @@ __device__ __forceinline__ void di_traj(const double* su, const double* sv, doub
 template <int D>
 __device__ __forceinline__ void di_pos(const double* su, const double* c2, const double* c3, double t, double* x) {
 #pragma unroll
-  for (int j = 0; j < D; ++j) x[j] = su[j] + t * (su[D + j] + t * (c2[j] + t * c3[j]));
+  for (int j = 0; j < D; ++j) x[j] = fma(t, fma(t, fma(t, c3[j], c2[j]), su[D + j]), su[j]);
 }
 
 template <int D>
 __device__ __forceinline__ void di_vel(const double* su, const double* c2, const double* c3, double t, double* v) {
 #pragma unroll
-  for (int j = 0; j < D; ++j) v[j] = su[D + j] + t * (2.0 * c2[j] + t * (3.0 * c3[j]));
+  for (int j = 0; j < D; ++j) v[j] = fma(t, fma(t, 3.0 * c3[j], 2.0 * c2[j]), su[D + j]);
 }
 
 // Work counters (always on; one atomicAdd per row per counter).
@@ -303,22 +306,27 @@ __global__ void __launch_bounds__(kWarps * 32) k_near(const double* __restrict__
         pf = !(dp2 > bp2 || dv2 > bv2);
         if (pf) {
           // level 2: c(tau) = tau + r_u (12 |a - s tau/2|^2 / tau^3 + |dv|^2 / tau)
-          // (a = p1 - p0, s = v0 + v1) is bounded below on [ta, tb] by
-          // ta + r_u (12 max(0, |a| - |s| tb/2)^2 / tb^3 + |dv|^2 / tb);
-          // a pair whose bound reaches r on every interval has no edge.
-          double ss = 0.0;
+          // (a = p1 - p0, s = v0 + v1).  On [ta, tb]: tau >= ta, |dv|^2/tau >=
+          // |dv|^2/tb, and |a - s tau/2|^2 = aa - tau a.s + tau^2 ss/4 is a
+          // convex quadratic whose minimum over [ta, tb] is taken at the
+          // clamped vertex.  A pair whose bound reaches r on every interval
+          // has no edge.
+          double ss = 0.0, as = 0.0;
 #pragma unroll
           for (int j = 0; j < D; ++j) {
             const double e = sv[D + j] + su[D + j];
+            const double a = sv[j] - su[j];
             ss += e * e;
+            as += a * e;
           }
-          const double na = sqrt(dp2), ns = sqrt(ss);
+          const double tv = (ss > 0.0) ? 2.0 * as / ss : 0.0;   // vertex of the quadratic
           bool possible = false;
           for (int jj = 0; jj < kNearIntervals && !possible; ++jj) {
             const double ta = r * (double)jj / (double)kNearIntervals;
             const double tb = r * (double)(jj + 1) / (double)kNearIntervals;
-            const double g = fmax(na - ns * tb * 0.5, 0.0);
-            const double L = ta + ru * (12.0 * g * g / (tb * tb * tb) + dv2 / tb);
+            const double tq = fmin(fmax(tv, ta), tb);
+            const double g2 = fmax(dp2 - tq * as + tq * tq * ss * 0.25, 0.0);
+            const double L = ta + ru * (12.0 * g2 / (tb * tb * tb) + dv2 / tb);
             possible = L * (1.0 - 1e-9) < r;
           }
           pf = possible;
@@ -481,10 +489,11 @@ __device__ __forceinline__ unsigned seg_hits_boxes(const double* A, const double
   double inv[D], slo[D], shi[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    inv[k] = (Dv[k] != 0.0) ? 1.0 / Dv[k] : 0.0;
+    inv[k] = (!MPAP_LAZY_INV && Dv[k] != 0.0) ? 1.0 / Dv[k] : 0.0;
     slo[k] = fmin(A[k], B[k]) - kCullMargin;
     shi[k] = fmax(A[k], B[k]) + kCullMargin;
   }
+  bool have_inv = !MPAP_LAZY_INV;   // reciprocals formed only if some box survives the prefilter
   unsigned tests = 0;
   int i = -1;
   for (;;) {
@@ -501,6 +510,11 @@ __device__ __forceinline__ unsigned seg_hits_boxes(const double* A, const double
     for (int k = 0; k < D; ++k)
       if (bx[k] > shi[k] || bx[D + k] < slo[k]) sep = true;
     if (sep) continue;
+    if (!have_inv) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) inv[k] = (Dv[k] != 0.0) ? 1.0 / Dv[k] : 0.0;
+      have_inv = true;
+    }
     ++tests;
     double t0 = 0.0, t1 = 1.0;
     bool hit = true;
@@ -600,9 +614,9 @@ __device__ __noinline__ double mlp_out0(const double* w, double z0, double z1, d
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     double a = b1[i];
-    a = a + W1[i * 3 + 0] * z0;
-    a = a + W1[i * 3 + 1] * z1;
-    a = a + W1[i * 3 + 2] * z2;
+    a = fma(W1[i * 3 + 0], z0, a);
+    a = fma(W1[i * 3 + 1], z1, a);
+    a = fma(W1[i * 3 + 2], z2, a);
     h1[i] = (a > 0.0) ? a : 0.0;
   }
   // output sum o = b3[0] + sum_i W3[i] h2[i] accumulated in index order as
@@ -612,9 +626,9 @@ __device__ __noinline__ double mlp_out0(const double* w, double z0, double z1, d
   for (int i = 0; i < 8; ++i) {
     double a = b2[i];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) a = a + W2[i * 8 + j] * h1[j];
+    for (int j = 0; j < 8; ++j) a = fma(W2[i * 8 + j], h1[j], a);
     const double h2 = (a > 0.0) ? a : 0.0;
-    o = o + W3[i] * h2;
+    o = fma(W3[i], h2, o);
   }
   return o;
 }
@@ -636,8 +650,8 @@ __device__ __forceinline__ void chunk_bbox(const double* su, const double* sv, c
     const double sa = ta / T, sb = tb / T;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      xa[j] = su[j] + sa * (sv[j] - su[j]);
-      xb[j] = su[j] + sb * (sv[j] - su[j]);
+      xa[j] = fma(sa, sv[j] - su[j], su[j]);
+      xb[j] = fma(sb, sv[j] - su[j], su[j]);
     }
   } else {
     di_pos<D>(su, c2, c3, ta, xa);
@@ -662,12 +676,12 @@ __device__ __forceinline__ void chunk_bbox(const double* su, const double* sv, c
         r0 = -Cq / Bq;
       }
       if (r0 > ta && r0 < tb) {
-        const double x = su[j] + r0 * (su[D + j] + r0 * (c2[j] + r0 * c3[j]));
+        const double x = fma(r0, fma(r0, fma(r0, c3[j], c2[j]), su[D + j]), su[j]);
         lo[j] = fmin(lo[j], x);
         hi[j] = fmax(hi[j], x);
       }
       if (r1 > ta && r1 < tb) {
-        const double x = su[j] + r1 * (su[D + j] + r1 * (c2[j] + r1 * c3[j]));
+        const double x = fma(r1, fma(r1, fma(r1, c3[j], c2[j]), su[D + j]), su[j]);
         lo[j] = fmin(lo[j], x);
         hi[j] = fmax(hi[j], x);
       }
@@ -682,7 +696,7 @@ __device__ __forceinline__ void chunk_bbox(const double* su, const double* sv, c
 // a sight line into shared memory (ballot compaction); each lane then counts
 // the visible features of its step, and the per-step increments are folded in
 // time order from shared memory (every lane folds the same sequence).
-template <int D, int DYN>
+template <int D, int DYN, int HEUR>
 __device__ void edge_heuristic(const DevParams& P, const double* su, const double* sv, double T,
                                const double* __restrict__ feat, int F, const double* __restrict__ box, int O,
                                WarpLists<D>& L, double* fold, int lane, double& s_out, double& c_out, Work& W) {
@@ -705,7 +719,7 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
   const double m = R + kCullMargin;
   const double R2 = R * R;
   const double cos2 = P.fov_cos_half * P.fov_cos_half;
-  const int heur = P.heuristic;
+  constexpr int heur = HEUR;
   const float half_fov = acosf((float)P.fov_cos_half);
   const unsigned lt = lanemask_lt();
   double s = 0.0, c = 0.0;
@@ -842,7 +856,7 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
       if (DYN == 0) {
         const double sp = t / T;
 #pragma unroll
-        for (int j = 0; j < D; ++j) x[j] = su[j] + sp * (sv[j] - su[j]);
+        for (int j = 0; j < D; ++j) x[j] = fma(sp, sv[j] - su[j], su[j]);
         if (heur == 1) {
 #pragma unroll
           for (int j = 0; j < D; ++j) hv[j] = sv[j] - su[j];
@@ -854,7 +868,7 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
         if (heur == 3) {
           double ss = 0.0;
 #pragma unroll
-          for (int j = 0; j < D; ++j) ss = ss + vel[j] * vel[j];
+          for (int j = 0; j < D; ++j) ss = fma(vel[j], vel[j], ss);
           speed = sqrt(ss);
         }
         if (heur == 1) {
@@ -864,23 +878,23 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
       }
       if (heur >= 2) {
         const double sp = t / T;
-        hv[0] = (1.0 - sp) * hu0 + sp * hv0;
-        hv[1] = (1.0 - sp) * hu1 + sp * hv1;
+        hv[0] = fma(sp, hv0, (1.0 - sp) * hu0);
+        hv[1] = fma(sp, hv1, (1.0 - sp) * hu1);
       }
       double hh = 0.0;
 #pragma unroll
-      for (int j = 0; j < D; ++j) hh = hh + hv[j] * hv[j];
+      for (int j = 0; j < D; ++j) hh = fma(hv[j], hv[j], hh);
       int kv = 0;
       for (int i = 0; i < nf; ++i) {
         double dl[D];
         double dd = 0.0;
 #pragma unroll
-        for (int j = 0; j < D; ++j) { dl[j] = L.f[j][i] - x[j]; dd = dd + dl[j] * dl[j]; }
+        for (int j = 0; j < D; ++j) { dl[j] = L.f[j][i] - x[j]; dd = fma(dl[j], dl[j], dd); }
         if (dd > R2) continue;
         if (heur != 0) {
           double dot = 0.0;
 #pragma unroll
-          for (int j = 0; j < D; ++j) dot = dot + hv[j] * dl[j];
+          for (int j = 0; j < D; ++j) dot = fma(hv[j], dl[j], dot);
           if (!(hh > 0.0)) continue;
           if (dot < 0.0) continue;
           if (dot * dot < cos2 * (hh * dd)) continue;
@@ -925,7 +939,7 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
 template <int PHASE>
 struct EdgeBounds { static constexpr int kMin = (PHASE == 0) ? 2 : MPAP_EDGES_MIN_BLOCKS; };
 
-template <int D, int DYN, int PHASE>
+template <int D, int DYN, int PHASE, int HEUR>
 __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(const double* __restrict__ samples,
                                                           const int64_t* __restrict__ node_base, int B,
                                                           const double* __restrict__ obst,
@@ -1014,7 +1028,7 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
         if (lane < NS) sv[lane] = (lane < stride) ? envs[(int64_t)rec.v * stride + lane] : 0.0;
         __syncwarp();
         double s64, c64;
-        edge_heuristic<D, DYN>(P, su, sv, rec.tau, efeat, F, ebox, O, L, s_fold[warp], lane, s64, c64, W);
+        edge_heuristic<D, DYN, HEUR>(P, su, sv, rec.tau, efeat, F, ebox, O, L, s_fold[warp], lane, s64, c64, W);
         W.flush(lane);
         if (lane == 0) *reinterpret_cast<float2*>(&edges[e0 + j].s) = make_float2((float)s64, (float)c64);
       }
@@ -1047,25 +1061,25 @@ cudaError_t launch_near(dim3 grid, cudaStream_t st, const mpap_roadmap* rm, cons
   return cudaGetLastError();
 }
 
-template <int D, int DYN, int PHASE>
+template <int D, int DYN, int PHASE, int HEUR>
 cudaError_t launch_edges_phase(size_t smem, cudaStream_t st, const mpap_roadmap* rm, int cap, const int32_t* d_cnt,
                                const NearRec* d_scr, unsigned long long* d_free, unsigned long long* d_work,
                                unsigned long long* d_next) {
-  cudaError_t e = cudaFuncSetAttribute(k_edges<D, DYN, PHASE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto kern = k_edges<D, DYN, PHASE, HEUR>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)std::max<size_t>(smem, 1));
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_edges<D, DYN, PHASE>, kWarps * 32, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
   if (e != cudaSuccess) return e;
   const int64_t N = rm->node_base[rm->B];
   const int64_t need = (N + kWarps - 1) / kWarps;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(per_sm, 1), need));
-  k_edges<D, DYN, PHASE><<<grid, kWarps * 32, smem, st>>>(rm->d_samples, rm->d_node_base, rm->B, rm->d_obst,
-                                                          rm->d_obst_base, rm->d_feat, rm->d_feat_base, rm->prm,
-                                                          cap, rm->o_max, rm->f_max, d_cnt, d_scr, rm->d_row_ptr,
-                                                          rm->d_edges, d_free, d_work, d_next);
+  kern<<<grid, kWarps * 32, smem, st>>>(rm->d_samples, rm->d_node_base, rm->B, rm->d_obst, rm->d_obst_base,
+                                        rm->d_feat, rm->d_feat_base, rm->prm, cap, rm->o_max, rm->f_max, d_cnt,
+                                        d_scr, rm->d_row_ptr, rm->d_edges, d_free, d_work, d_next);
   return cudaGetLastError();
 }
 
@@ -1073,8 +1087,14 @@ template <int D, int DYN>
 cudaError_t launch_edges(int phase, size_t smem, cudaStream_t st, const mpap_roadmap* rm, int cap,
                          const int32_t* d_cnt, const NearRec* d_scr, unsigned long long* d_free,
                          unsigned long long* d_work, unsigned long long* d_next) {
-  return phase == 0 ? launch_edges_phase<D, DYN, 0>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next)
-                    : launch_edges_phase<D, DYN, 1>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next + 1);
+  if (phase == 0)
+    return launch_edges_phase<D, DYN, 0, 0>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next);
+  switch (rm->prm.heuristic) {
+    case 0: return launch_edges_phase<D, DYN, 1, 0>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next + 1);
+    case 1: return launch_edges_phase<D, DYN, 1, 1>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next + 1);
+    case 2: return launch_edges_phase<D, DYN, 1, 2>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next + 1);
+    default: return launch_edges_phase<D, DYN, 1, 3>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next + 1);
+  }
 }
 }  // namespace
 
