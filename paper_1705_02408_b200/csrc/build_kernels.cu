@@ -633,10 +633,6 @@ __device__ __noinline__ double mlp_out0(const double* w, double z0, double z1, d
   return o;
 }
 
-#ifndef MPAP_FEAT_UNROLL
-#define MPAP_FEAT_UNROLL 1
-#endif
-constexpr int kFeatUnroll = MPAP_FEAT_UNROLL;   // features tested per inner iteration (ILP)
 
 // Bounding box of the positions of steps t in [ta, tb] along the edge, computed
 // analytically by every lane (no shuffles): endpoints plus, for the cubic, the

@@ -68,6 +68,9 @@ struct mpap_roadmap {
   int64_t nnz_total = 0;
   unsigned long long work[mpap::kWorkCounters] = {};  // build work counters (mpap_roadmap_work)
   cudaStream_t alloc_stream = nullptr;                 // stream the device arrays were allocated on
+  // search capacities learned from earlier regrow-and-retry rounds on this
+  // roadmap (staircase slots, labels, candidates); 0 = default
+  mutable int hint_K = 0, hint_L = 0, hint_C = 0;
 };
 
 namespace mpap {

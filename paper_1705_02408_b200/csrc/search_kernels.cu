@@ -1,9 +1,11 @@
 // paper_1705_02408_b200/csrc/search_kernels.cu -- Alg. 3 Explore on sm_100a.
 //
 // The group-marching multiobjective search of PAPER.md P:237-265 (text
-// P:227-235), one persistent CTA per query at a time (queries are pulled from
-// an atomic work counter, so a batch of independent queries load-balances
-// across the 148 SMs).  Per wave (one non-empty group G_i):
+// P:227-235).  A "team" runs one query: for a batch, one persistent CTA per
+// query at a time (queries are pulled from an atomic work counter, so
+// independent queries load-balance across the 148 SMs); for a single
+// latency-bound query, the whole grid of a cooperative launch (grid.sync
+// between phases).  Per wave (one non-empty group G_i):
 //
 //   expand   warp per plan p of G_i; the head's CSR row is streamed 32 edges
 //            at a time with one 16-byte load per lane (A3.6-A3.8):
@@ -12,8 +14,8 @@
 //            node's current non-dominated staircase is dropped on the spot
 //            (it cannot survive RemoveDominated); survivors are
 //            appended with warp-aggregated atomics (ballot + popc).
-//   group    per-destination counts -> block scan -> scatter, so each touched
-//            node's candidates are contiguous.
+//   group    per-destination counts -> atomic range allocation -> scatter,
+//            so each touched node's candidates are contiguous.
 //   merge    warp per touched node: RemoveDominated (A3.15) as a set
 //            operation -- old staircase entries dominated by a candidate die
 //            (open ones are removed from P_open), candidates dominated by
@@ -26,6 +28,7 @@
 // result is the minimum (cost, h, node sequence) plan over the goal nodes'
 // staircases (A3.20-A3.21; R16).  Every per-wave decision depends only on
 // sets, never on thread order (R14), so plans are bit-identical to the oracle.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -39,10 +42,10 @@
 #include "mpap_internal.cuh"
 
 namespace mpap {
+namespace cg = cooperative_groups;
 
 #define FULLM 0xffffffffu
 constexpr int kST = 512;              // threads per search CTA
-constexpr int kSW = kST / 32;         // warps per search CTA
 enum : uint8_t { L_OPEN = 0, L_CLOSED = 1, L_DEAD = 2 };
 enum { OVF_LABELS = 1, OVF_CAND = 2, OVF_STAIR = 4 };
 constexpr int kRetryBase = 100;       // result.status = kRetryBase + OVF_* mask
@@ -94,7 +97,7 @@ struct SearchArgs {
 };
 
 struct Ctl {
-  int q, gsize, psize, nsize, ncand, ntouched, nlabels, goal_in_g, overflow, any_goal;
+  int q, gsize, psize, nsize, ncand, ntouched, nlabels, goal_in_g, overflow, any_goal, calloc;
   long long i, minb;
   unsigned long long relax, bpass, tcount, ssum, inserted, killed;
   unsigned long long relax_total, inserted_total;
@@ -103,6 +106,27 @@ struct Ctl {
   int nties;
   int ties[32];
 };
+
+// A team runs one query: a CTA (batched queries, __syncthreads) or the whole
+// grid of a cooperative launch (a single latency-bound query, grid.sync).
+struct CtaTeam {
+  __device__ __forceinline__ int rank() const { return threadIdx.x; }
+  __device__ __forceinline__ int size() const { return blockDim.x; }
+  __device__ __forceinline__ int warp() const { return threadIdx.x >> 5; }
+  __device__ __forceinline__ int nwarps() const { return blockDim.x >> 5; }
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
+struct GridTeam {
+  __device__ __forceinline__ int rank() const { return blockIdx.x * blockDim.x + threadIdx.x; }
+  __device__ __forceinline__ int size() const { return gridDim.x * blockDim.x; }
+  __device__ __forceinline__ int warp() const { return rank() >> 5; }
+  __device__ __forceinline__ int nwarps() const { return size() >> 5; }
+  __device__ __forceinline__ void sync() const { cg::this_grid().sync(); }
+};
+
+// control words are re-read after every team barrier
+template <typename T>
+__device__ __forceinline__ T vld(const T& x) { return *(const volatile T*)&x; }
 
 __device__ __forceinline__ unsigned lane_lt() {
   unsigned m;
@@ -119,47 +143,18 @@ __device__ __forceinline__ long long bucket_of(float cost, double T) {
   return b;
 }
 
-// Block-wide exclusive scan of cand_cnt over the touched list -> cand_off.
-__device__ void scan_touched(int nt, const int32_t* touched, const int32_t* cnt, int32_t* off, int* s_wsum) {
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int chunk = (nt + kST - 1) / kST;
-  const int lo = t * chunk, hi = min(nt, lo + chunk);
-  int s = 0;
-  for (int k = lo; k < hi; ++k) s += cnt[touched[k]];
-  int x = s;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(FULLM, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) s_wsum[w] = x;
-  __syncthreads();
-  if (w == 0) {
-    int y = (lane < kSW) ? s_wsum[lane] : 0;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int z = __shfl_up_sync(FULLM, y, o);
-      if (lane >= o) y += z;
-    }
-    if (lane < kSW) s_wsum[lane] = y;
-  }
-  __syncthreads();
-  int excl = x - s + (w > 0 ? s_wsum[w - 1] : 0);
-  for (int k = lo; k < hi; ++k) {
-    const int xk = touched[k];
-    off[xk] = excl;
-    excl += cnt[xk];
-  }
-}
-
 // Partition src -> (G if cost <= inext*T else dst).  Tracks the goal flag of
 // G and the minimum bucket of dst.  Dead labels are dropped (lazy deletion).
-__device__ void partition(const SearchArgs& A, Ctl& S, const int32_t* src, int nsrc, int32_t* G, int32_t* dst,
-                          long long inext, const int4* labels, const uint8_t* lstate, const uint8_t* goal) {
+template <typename Team>
+__device__ void partition(const Team& team, const SearchArgs& A, Ctl* S, const int32_t* src, int nsrc, int32_t* G,
+                          int32_t* dst, long long inext, const int4* labels, const uint8_t* lstate,
+                          const uint8_t* goal) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = lane_lt();
   const double thr = (double)inext * A.T;
   long long myminb = LLONG_MAX;
   bool mygoal = false;
-  for (int k0 = (threadIdx.x >> 5) * 32; k0 < nsrc; k0 += kST) {
+  for (int k0 = team.warp() * 32; k0 < nsrc; k0 += team.nwarps() * 32) {
     const int k = k0 + lane;
     bool toG = false, toD = false;
     int id = -1;
@@ -181,23 +176,25 @@ __device__ void partition(const SearchArgs& A, Ctl& S, const int32_t* src, int n
     const unsigned md = __ballot_sync(FULLM, toD);
     int bg = 0, bd = 0;
     if (lane == 0) {
-      if (mg) bg = atomicAdd(&S.gsize, __popc(mg));
-      if (md) bd = atomicAdd(&S.nsize, __popc(md));
+      if (mg) bg = atomicAdd(&S->gsize, __popc(mg));
+      if (md) bd = atomicAdd(&S->nsize, __popc(md));
     }
     bg = __shfl_sync(FULLM, bg, 0);
     bd = __shfl_sync(FULLM, bd, 0);
     if (toG) G[bg + __popc(mg & lt)] = id;
     if (toD) dst[bd + __popc(md & lt)] = id;
   }
-  if (mygoal) S.goal_in_g = 1;
-  if (myminb != LLONG_MAX) atomicMin(&S.minb, myminb);
+  if (mygoal) S->goal_in_g = 1;
+  if (myminb != LLONG_MAX) atomicMin(&S->minb, myminb);
 }
 
-template <bool TRACE>
-__device__ void run_query(const SearchArgs& A, Ctl& S, int* s_wsum, int slot, int qpos) {
+template <bool TRACE, typename Team>
+__device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slot, int qpos) {
   const int q = A.qidx[qpos];
   const QueryDesc Q = A.queries[q];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = team.rank(), lane = threadIdx.x & 31;
+  const int nthr = team.size(), warp = team.warp(), nw = team.nwarps();
+  const bool leader = (tid == 0);
   const unsigned lt = lane_lt();
   const SlotCaps C = A.caps;
   const int env = Q.env;
@@ -222,16 +219,17 @@ __device__ void run_query(const SearchArgs& A, Ctl& S, int* s_wsum, int slot, in
   uint8_t* goal = A.goal + (size_t)slot * C.n;
   const double beta = Q.beta;
   const int d = A.pos_dim;
+  mpap_result* R = A.results + q;
 
   // ---- a5: init (A3.1-A3.4) ----
-  if (tid == 0) {
-    S.gsize = 1; S.psize = 0; S.nsize = 0; S.ncand = 0; S.ntouched = 0; S.nlabels = 1;
-    S.goal_in_g = 0; S.overflow = 0; S.any_goal = 0; S.i = 0; S.minb = LLONG_MAX;
-    S.relax_total = 0; S.inserted_total = 0; S.waves = 0;
+  if (leader) {
+    S->gsize = 1; S->psize = 0; S->nsize = 0; S->ncand = 0; S->ntouched = 0; S->nlabels = 1; S->calloc = 0;
+    S->goal_in_g = 0; S->overflow = 0; S->any_goal = 0; S->i = 0; S->minb = LLONG_MAX;
+    S->relax_total = 0; S->inserted_total = 0; S->waves = 0;
   }
-  __syncthreads();
+  team.sync();
   bool mygoal = false;
-  for (int x = tid; x < n; x += kST) {
+  for (int x = tid; x < n; x += nthr) {
     sn[x] = 0;
     ccnt[x] = 0;
     if (TRACE) stamp[x] = -1;
@@ -242,21 +240,20 @@ __device__ void run_query(const SearchArgs& A, Ctl& S, int* s_wsum, int slot, in
     goal[x] = in ? 1 : 0;
     mygoal |= in;
   }
-  if (__any_sync(FULLM, mygoal) && lane == 0) S.any_goal = 1;
-  __syncthreads();
-  if (tid == 0) {
+  if (__any_sync(FULLM, mygoal) && lane == 0) S->any_goal = 1;
+  team.sync();
+  if (leader) {
     labels[0] = make_int4(Q.start, -1, __float_as_int(0.0f), __float_as_int(0.0f));
     lstate[0] = L_OPEN;
     sch[(size_t)Q.start * C.K] = make_float2(0.0f, 0.0f);
     sid[(size_t)Q.start * C.K] = 0;
     sn[Q.start] = 1;
     G[0] = 0;
-    S.goal_in_g = goal[Q.start];
+    S->goal_in_g = goal[Q.start];
   }
-  __syncthreads();
-  mpap_result* R = A.results + q;
-  if (!S.any_goal) {
-    if (tid == 0) {
+  team.sync();
+  if (!vld(S->any_goal)) {
+    if (leader) {
       mpap_result r{};
       r.status = MPAP_ERR_NO_GOAL_NODE;
       *R = r;
@@ -267,18 +264,19 @@ __device__ void run_query(const SearchArgs& A, Ctl& S, int* s_wsum, int slot, in
   // ---- wave loop (A3.5-A3.19) ----
   int wave = 0;
   while (true) {
-    if (S.goal_in_g || S.gsize == 0) break;     // A3.5 (G = {} <=> P_open = {} here)
-    const int gsize = S.gsize;
-    const long long i_cur = S.i;
-    if (tid == 0) {
-      S.relax = 0; S.bpass = 0; S.tcount = 0; S.ssum = 0; S.inserted = 0; S.killed = 0;
-      S.ncand = 0; S.ntouched = 0;
+    if (vld(S->goal_in_g) || vld(S->gsize) == 0) break;     // A3.5 (G = {} <=> P_open = {} here)
+    const int gsize = vld(S->gsize);
+    const long long i_cur = vld(S->i);
+    team.sync();
+    if (leader) {
+      S->relax = 0; S->bpass = 0; S->tcount = 0; S->ssum = 0; S->inserted = 0; S->killed = 0;
+      S->ncand = 0; S->ntouched = 0; S->calloc = 0;
     }
-    __syncthreads();
-    // ---- a7 expand (A3.6-A3.11) ----
+    team.sync();
+    // ---- a7 expand (A3.6-A3.11): warp per plan of G_i, 32 edges per step ----
     {
       unsigned long long my_relax = 0, my_bpass = 0, my_t = 0, my_ss = 0;
-      for (int k = warp; k < gsize; k += kSW) {
+      for (int k = warp; k < gsize; k += nw) {
         const int p = G[k];
         const int4 lb = labels[p];
         const int u = lb.x;
@@ -304,6 +302,8 @@ __device__ void run_query(const SearchArgs& A, Ctl& S, int* s_wsum, int slot, in
                 if (TRACE) {
                   if (atomicExch(&stamp[x], wave) != wave) { ++my_t; my_ss += (unsigned long long)m; }
                 }
+                // dominated by the node's non-dominated staircase?  Such a
+                // candidate cannot survive RemoveDominated (transitivity).
                 bool dom = false;
                 const float2* st = sch + (size_t)x * C.K;
                 for (int j = 0; j < m; ++j) {
@@ -318,44 +318,47 @@ __device__ void run_query(const SearchArgs& A, Ctl& S, int* s_wsum, int slot, in
           const unsigned em = __ballot_sync(FULLM, emit);
           if (em) {
             int base = 0;
-            if (lane == 0) base = atomicAdd(&S.ncand, __popc(em));
+            if (lane == 0) base = atomicAdd(&S->ncand, __popc(em));
             base = __shfl_sync(FULLM, base, 0);
             if (emit) {
               const int idx = base + __popc(em & lt);
               if (idx < C.C) {
                 cand[idx] = make_int4(x, __float_as_int(qc), __float_as_int(qh), p);
-                if (atomicAdd(&ccnt[x], 1) == 0) touched[atomicAdd(&S.ntouched, 1)] = x;
+                if (atomicAdd(&ccnt[x], 1) == 0) touched[atomicAdd(&S->ntouched, 1)] = x;
               } else {
-                atomicOr(&S.overflow, OVF_CAND);
+                atomicOr(&S->overflow, OVF_CAND);
               }
             }
           }
         }
       }
-      if (my_relax) atomicAdd(&S.relax, my_relax);
-      if (my_bpass) atomicAdd(&S.bpass, my_bpass);
+      if (my_relax) atomicAdd(&S->relax, my_relax);
+      if (my_bpass) atomicAdd(&S->bpass, my_bpass);
       if (TRACE) {
-        if (my_t) atomicAdd(&S.tcount, my_t);
-        if (my_ss) atomicAdd(&S.ssum, my_ss);
+        if (my_t) atomicAdd(&S->tcount, my_t);
+        if (my_ss) atomicAdd(&S->ssum, my_ss);
       }
     }
-    __syncthreads();
-    if (S.overflow) break;
-    const int nt = S.ntouched;
-    const int ncand = S.ncand;
-    // ---- group candidates by destination ----
-    scan_touched(nt, touched, ccnt, coff, s_wsum);
-    __syncthreads();
-    for (int k = tid; k < ncand; k += kST) {
+    team.sync();
+    if (vld(S->overflow)) break;
+    const int nt = vld(S->ntouched);
+    const int ncand = vld(S->ncand);
+    // ---- group candidates by destination: contiguous range per touched node ----
+    for (int t = tid; t < nt; t += nthr) {
+      const int x = touched[t];
+      coff[x] = atomicAdd(&S->calloc, ccnt[x]);
+    }
+    team.sync();
+    for (int k = tid; k < ncand; k += nthr) {
       const int4 cq = cand[k];
       const int pos = atomicAdd(&coff[cq.x], 1);
       cs[pos] = cq;
     }
-    __syncthreads();
-    // ---- a8 RemoveDominated + insert (A3.10-A3.15) ----
+    team.sync();
+    // ---- a8 RemoveDominated + insert (A3.10-A3.15): warp per touched node ----
     {
       unsigned long long my_ins = 0, my_kill = 0;
-      for (int t = warp; t < nt; t += kSW) {
+      for (int t = warp; t < nt; t += nw) {
         const int x = touched[t];
         const int kc = ccnt[x];
         const int beg = coff[x] - kc;
@@ -410,13 +413,13 @@ __device__ void run_query(const SearchArgs& A, Ctl& S, int* s_wsum, int slot, in
           if (sm) {
             int lbase = 0, pbase = 0;
             if (lane == 0) {
-              lbase = atomicAdd(&S.nlabels, __popc(sm));
-              pbase = atomicAdd(&S.psize, __popc(sm));
+              lbase = atomicAdd(&S->nlabels, __popc(sm));
+              pbase = atomicAdd(&S->psize, __popc(sm));
             }
             lbase = __shfl_sync(FULLM, lbase, 0);
             pbase = __shfl_sync(FULLM, pbase, 0);
             if (lbase + __popc(sm) > C.L) {
-              if (lane == 0) atomicOr(&S.overflow, OVF_LABELS);
+              if (lane == 0) atomicOr(&S->overflow, OVF_LABELS);
             } else if (surv) {
               const int rk = __popc(sm & lt);
               const int id = lbase + rk;
@@ -434,111 +437,114 @@ __device__ void run_query(const SearchArgs& A, Ctl& S, int* s_wsum, int slot, in
           }
         }
         if (lane == 0) {
-          if (newm > C.K) atomicOr(&S.overflow, OVF_STAIR);
+          if (newm > C.K) atomicOr(&S->overflow, OVF_STAIR);
           sn[x] = min(newm, C.K);
         }
       }
-      if (my_kill) atomicAdd(&S.killed, my_kill);
-      if (my_ins) atomicAdd(&S.inserted, my_ins);
+      if (my_kill) atomicAdd(&S->killed, my_kill);
+      if (my_ins) atomicAdd(&S->inserted, my_ins);
     }
-    __syncthreads();
-    if (S.overflow) break;
+    team.sync();
+    if (vld(S->overflow)) break;
     // reset per-node candidate counters of touched nodes
-    for (int t = tid; t < nt; t += kST) ccnt[touched[t]] = 0;
+    for (int t = tid; t < nt; t += nthr) ccnt[touched[t]] = 0;
     // ---- a9 retire G_i (A3.16), i <- i+1 (A3.17) ----
-    for (int k = tid; k < gsize; k += kST) {
+    for (int k = tid; k < gsize; k += nthr) {
       const int p = G[k];
       if (lstate[p] == L_OPEN) lstate[p] = L_CLOSED;
     }
-    if (tid == 0) {
+    if (leader) {
       if (TRACE && wave < A.waves_cap) {
         mpap_wave wv;
-        wv.i = i_cur; wv.group = gsize; wv.relax = (long long)S.relax; wv.beta_pass = (long long)S.bpass;
-        wv.inserted = (long long)S.inserted; wv.killed = (long long)S.killed; wv.touched = (long long)S.tcount;
-        wv.stair_sum = (long long)S.ssum;
+        wv.i = i_cur; wv.group = gsize; wv.relax = (long long)vld(S->relax);
+        wv.beta_pass = (long long)vld(S->bpass); wv.inserted = (long long)vld(S->inserted);
+        wv.killed = (long long)vld(S->killed); wv.touched = (long long)vld(S->tcount);
+        wv.stair_sum = (long long)vld(S->ssum);
         A.waves[(size_t)q * A.waves_cap + wave] = wv;
       }
-      S.relax_total += S.relax;
-      S.inserted_total += S.inserted;
-      S.waves = wave + 1;
-      S.gsize = 0; S.nsize = 0; S.goal_in_g = 0; S.minb = LLONG_MAX;
+      S->relax_total += vld(S->relax);
+      S->inserted_total += vld(S->inserted);
+      S->waves = wave + 1;
+      S->gsize = 0; S->nsize = 0; S->goal_in_g = 0; S->minb = LLONG_MAX;
     }
-    __syncthreads();
+    team.sync();
     // ---- a6 G_{i+1} (A3.18), with the exact empty-group skip (R24) ----
-    const int np = S.psize;
+    const int np = vld(S->psize);
     long long inext = i_cur + 1;
-    partition(A, S, pend, np, G, pend2, inext, labels, lstate, goal);
-    __syncthreads();
-    if (S.gsize == 0 && S.nsize > 0) {
-      inext = S.minb;
-      const int n2 = S.nsize;
-      __syncthreads();
-      if (tid == 0) { S.nsize = 0; S.minb = LLONG_MAX; }
-      __syncthreads();
-      partition(A, S, pend2, n2, G, pend, inext, labels, lstate, goal);
-      __syncthreads();
-      if (tid == 0) { S.psize = S.nsize; S.i = inext; }
+    partition(team, A, S, pend, np, G, pend2, inext, labels, lstate, goal);
+    team.sync();
+    if (vld(S->gsize) == 0 && vld(S->nsize) > 0) {
+      inext = vld(S->minb);
+      const int n2 = vld(S->nsize);
+      team.sync();
+      if (leader) { S->nsize = 0; S->minb = LLONG_MAX; }
+      team.sync();
+      partition(team, A, S, pend2, n2, G, pend, inext, labels, lstate, goal);
+      team.sync();
+      if (leader) { S->psize = vld(S->nsize); S->i = inext; }
     } else {
       // swap pending lists
-      if (tid == 0) { S.psize = S.nsize; S.i = inext; }
+      if (leader) { S->psize = vld(S->nsize); S->i = inext; }
       int32_t* tmp = pend; pend = pend2; pend2 = tmp;
     }
-    __syncthreads();
+    team.sync();
     ++wave;
   }
 
   // ---- a10 goal extraction (A3.20-A3.21) ----
-  if (S.overflow) {
-    if (tid == 0) {
+  if (vld(S->overflow)) {
+    if (leader) {
       mpap_result r{};
-      r.status = kRetryBase + S.overflow;
+      r.status = kRetryBase + vld(S->overflow);
       *R = r;
     }
     return;
   }
-  if (!S.goal_in_g) {   // P_open emptied: no feasible plan
-    if (tid == 0) {
+  if (!vld(S->goal_in_g)) {   // P_open emptied: no feasible plan
+    if (leader) {
       mpap_result r{};
       r.status = MPAP_ERR_NO_FEASIBLE_PLAN;
-      r.waves = S.waves;
-      r.relaxations = (int64_t)S.relax_total;
-      r.labels_inserted = (int64_t)S.inserted_total;
+      r.waves = vld(S->waves);
+      r.relaxations = (int64_t)vld(S->relax_total);
+      r.labels_inserted = (int64_t)vld(S->inserted_total);
       *R = r;
     }
     return;
   }
-  if (tid == 0) { S.best_key = ~0ull; S.nties = 0; }
-  __syncthreads();
-  for (int x = tid; x < n; x += kST) {
+  team.sync();
+  if (leader) { S->best_key = ~0ull; S->nties = 0; }
+  team.sync();
+  for (int x = tid; x < n; x += nthr) {
     if (!goal[x]) continue;
     const int m = sn[x];
     for (int j = 0; j < m; ++j) {
       const float2 ch = sch[(size_t)x * C.K + j];
       const unsigned long long key = ((unsigned long long)__float_as_uint(ch.x) << 32) | __float_as_uint(ch.y);
-      atomicMin(&S.best_key, key);
+      atomicMin(&S->best_key, key);
     }
   }
-  __syncthreads();
-  for (int x = tid; x < n; x += kST) {
+  team.sync();
+  const unsigned long long best_key = vld(S->best_key);
+  for (int x = tid; x < n; x += nthr) {
     if (!goal[x]) continue;
     const int m = sn[x];
     for (int j = 0; j < m; ++j) {
       const float2 ch = sch[(size_t)x * C.K + j];
       const unsigned long long key = ((unsigned long long)__float_as_uint(ch.x) << 32) | __float_as_uint(ch.y);
-      if (key == S.best_key) {
-        const int slot_t = atomicAdd(&S.nties, 1);
-        if (slot_t < 32) S.ties[slot_t] = sid[(size_t)x * C.K + j];
+      if (key == best_key) {
+        const int slot_t = atomicAdd(&S->nties, 1);
+        if (slot_t < 32) S->ties[slot_t] = sid[(size_t)x * C.K + j];
       }
     }
   }
-  __syncthreads();
-  if (tid == 0) {
+  team.sync();
+  if (leader) {
     // lexicographic tie-break on node sequences (R16); chains reversed into
     // the (now unused) G / pend2 arrays
-    int best = S.ties[0];
-    const int nties = min(S.nties, 32);
+    int best = vld(S->ties[0]);
+    const int nties = min(vld(S->nties), 32);
     for (int k = 1; k < nties; ++k) {
-      const int cand_id = S.ties[k];
+      const int cand_id = vld(S->ties[k]);
       int la = 0, lb = 0;
       for (int x = cand_id; x >= 0; x = labels[x].y) G[la++] = labels[x].x;
       for (int x = best; x >= 0; x = labels[x].y) pend2[lb++] = labels[x].x;
@@ -558,9 +564,9 @@ __device__ void run_query(const SearchArgs& A, Ctl& S, int* s_wsum, int slot, in
       if (hx > hp) hp = hx;
     }
     mpap_result r{};
-    r.waves = S.waves;
-    r.relaxations = (int64_t)S.relax_total;
-    r.labels_inserted = (int64_t)S.inserted_total;
+    r.waves = vld(S->waves);
+    r.relaxations = (int64_t)vld(S->relax_total);
+    r.labels_inserted = (int64_t)vld(S->inserted_total);
     r.cost = __int_as_float(labels[best].z);
     r.h = __int_as_float(labels[best].w);
     r.h_peak = hp;
@@ -577,19 +583,29 @@ __device__ void run_query(const SearchArgs& A, Ctl& S, int* s_wsum, int slot, in
   }
 }
 
+// Batched queries: one CTA per query at a time, queries pulled from a counter.
 template <bool TRACE>
 __global__ void __launch_bounds__(kST) k_search(SearchArgs A) {
   __shared__ Ctl S;
-  __shared__ int s_wsum[32];
+  __shared__ int s_q;
+  const CtaTeam team;
   while (true) {
-    if (threadIdx.x == 0) S.q = atomicAdd(A.work, 1);
+    if (threadIdx.x == 0) s_q = atomicAdd(A.work, 1);
     __syncthreads();
-    const int qpos = S.q;
+    const int qpos = s_q;
     __syncthreads();
     if (qpos >= A.nq) break;
-    run_query<TRACE>(A, S, s_wsum, blockIdx.x, qpos);
+    run_query<TRACE>(team, A, &S, blockIdx.x, qpos);
     __syncthreads();
   }
+}
+
+// A single query over the whole grid (cooperative launch; grid.sync between
+// the phases of each wave).  Control words live in global memory.
+template <bool TRACE>
+__global__ void __launch_bounds__(kST) k_search_grid(SearchArgs A, Ctl* S) {
+  const GridTeam team;
+  run_query<TRACE>(team, A, S, 0, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -646,11 +662,16 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
   if (trace) CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_search<true>, kST, 0));
   else CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_search<false>, kST, 0));
   occ = std::max(occ, 1);
+  int occ_grid = 1, coop = 0;
+  CKS(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  if (trace) CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_grid, k_search_grid<true>, kST, 0));
+  else CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_grid, k_search_grid<false>, kST, 0));
+  const bool use_grid = coop && occ_grid > 0 && getenv("MPAP_SEARCH_CTA") == nullptr;
   SlotCaps caps;
   caps.n = rm->n_max;
-  caps.K = 64;
-  caps.L = std::max(1 << 17, 64 * rm->n_max);
-  caps.C = caps.L;
+  caps.K = std::max(64, rm->hint_K);
+  caps.L = std::max(std::max(1 << 17, 64 * rm->n_max), rm->hint_L);
+  caps.C = std::max(caps.L, rm->hint_C);
 
   // device copies of the queries and outputs
   QueryDesc* d_q = nullptr;
@@ -679,8 +700,12 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
   mpap_status status = MPAP_OK;
   for (int round = 0; round < 12 && !todo.empty(); ++round) {
     const int nrun = (int)todo.size();
-    const int nslots = std::min(nrun, nsm * occ);
-    const size_t sb = carve(nullptr, caps, nslots, nullptr);
+    // one query: the whole grid works on it (cooperative launch); otherwise one
+    // CTA per query and as many slots as resident CTAs
+    const bool grid_mode = (nrun == 1) && use_grid;
+    const int nslots = grid_mode ? 1 : std::min(nrun, nsm * occ);
+    const size_t sb_slots = carve(nullptr, caps, nslots, nullptr);
+    const size_t sb = sb_slots + sizeof(Ctl) + 256;
     HostTimer ta("slot arena");
     void* base = workspace(st, WS_SEARCH, sb);
     if (!base) {
@@ -716,8 +741,16 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     CKS(cudaMemsetAsync(d_work, 0, sizeof(int), st));
     {
       ProfScope ps("k_search", st);
-      if (trace) k_search<true><<<nslots, kST, 0, st>>>(A);
-      else k_search<false><<<nslots, kST, 0, st>>>(A);
+      if (grid_mode) {
+        Ctl* d_ctl = reinterpret_cast<Ctl*>(static_cast<char*>(base) + ((sb_slots + 255) & ~size_t(255)));
+        void* args[] = {&A, &d_ctl};
+        const void* fn = trace ? (const void*)k_search_grid<true> : (const void*)k_search_grid<false>;
+        CKS(cudaLaunchCooperativeKernel(fn, dim3(nsm * occ_grid), dim3(kST), args, 0, st));
+      } else if (trace) {
+        k_search<true><<<nslots, kST, 0, st>>>(A);
+      } else {
+        k_search<false><<<nslots, kST, 0, st>>>(A);
+      }
     }
     note_launch();
     CKS(cudaGetLastError());
@@ -739,6 +772,9 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     if (mask & OVF_STAIR) caps.K *= 2;
     if (mask & OVF_LABELS) caps.L *= 2;
     if (mask & OVF_CAND) caps.C *= 2;
+    rm->hint_K = std::max(rm->hint_K, caps.K);   // later searches on this roadmap start there
+    rm->hint_L = std::max(rm->hint_L, caps.L);
+    rm->hint_C = std::max(rm->hint_C, caps.C);
     todo.swap(again);
   }
   if (status == MPAP_OK && !todo.empty()) status = set_error(MPAP_ERR_OUT_OF_MEMORY, "search capacity regrow limit");
