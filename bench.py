@@ -326,6 +326,7 @@ def main():
     dom_ms, dom_n = kern[dom]
     roof = roofline(dom, dom_ms, dom_n, last_work, B, res, peaks, peak_src)
     roof["share_of_step"] = dom_ms / tot_ms if tot_ms > 0 else None
+    roof["traffic"] = committed_traffic(dom, Q)
 
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
@@ -345,6 +346,7 @@ def main():
         "kernels_ms_per_step": {k: kern[k][0] / args.steps for k in mp.KERNELS},
         "feasible_fraction": feasible_all / (world * Q), "all_status_ok": ok,
         "roofline": roof, "gpu_launches": int(launches), "clocks": clocks, "wall_s": wall,
+        "step_ms": [round(x, 3) for x in step_ms],
     }
     if e2e:
         line["e2e"] = e2e
@@ -370,6 +372,20 @@ def fp64_ops(kernel: str, w: dict, D: int = 3) -> float:
         return (per_step * w["steps"] + 205 * w["mlp"] + 3 * D * w["range_tests"] + (2 * D + 3) * w["fov_tests"]
                 + D * w["occl_segs"] + 4 * D * w["occl_box_tests"] + 40 * w["free_edges"])
     return 0.0
+
+
+def committed_traffic(kernel: str, Q: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu --set full capture in the bench's launch configuration
+    (profiles/traffic.json), or None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        e = t.get(kernel)
+        if e and int(e.get("queries_per_gpu", -1)) == Q:
+            return float(e["dram_bytes"])
+    except Exception:
+        pass
+    return None
 
 
 def roofline(kernel, ms, launches, work, B, res, peaks, peak_src):

@@ -1,2 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -3
-timeout 600 python tools/bench_search.py c1 --reps 3 2>&1 | tail -4
+timeout 300 python tools/bench_build.py 64 3 > gpurun_out/bb.log 2>&1; tail -5 gpurun_out/bb.log | cut -c1-400
