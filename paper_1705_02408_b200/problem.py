@@ -65,3 +65,47 @@ class Batch:
         envs = np.arange(len(self.probs), dtype=np.int32)
         return mpap_search_batch(rm, envs, self.starts, self.goals_lo, self.goals_hi, betas, self.lam,
                                  path_capacity, paths=paths, results=results, stream=stream)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2: batched perception-bound sweep and refinement.
+# Alg. 1 line 4 re-runs Explore with an updated beta; with one
+# roadmap resident, many betas run as one batched launch (one CTA per beta).
+# ---------------------------------------------------------------------------
+
+def beta_sweep(rm: Roadmap, prob, betas: Sequence[float], env: int = 0, path_capacity: int = 1024,
+               stream=None):
+    """Explore (Alg. 3) for every beta in one batched launch on one roadmap;
+    returns (paths [len(betas), cap], result records)."""
+    nb = len(betas)
+    envs = np.full(nb, env, dtype=np.int32)
+    starts = np.full(nb, prob.start, dtype=np.int32)
+    return mpap_search_batch(rm, envs, starts, [prob.goal_lo] * nb, [prob.goal_hi] * nb,
+                             np.asarray(betas, dtype=np.float64), prob.lam, path_capacity, stream=stream)
+
+
+def refine_beta_min(rm: Roadmap, prob, hi: float, rel_tol: float = 1e-3, per_round: int = 32, env: int = 0,
+                    max_rounds: int = 20):
+    """Smallest perception bound with a feasible plan, to `rel_tol` relative:
+    each round evaluates `per_round` equally spaced bounds in [lo, hi] with one
+    batched launch and keeps the bracket around the feasibility switch
+    (Explore feasibility is monotone in beta).  Returns (lo, hi, rounds):
+    infeasible at lo (or lo == 0), feasible at hi."""
+    _, r = beta_sweep(rm, prob, [hi], env)
+    if r[0]["status"] != 0:
+        raise ValueError("no feasible plan even at the upper bound")
+    _, r0 = beta_sweep(rm, prob, [0.0], env)
+    if r0[0]["status"] == 0:
+        return 0.0, 0.0, 1
+    lo = 0.0
+    rounds = 0
+    while hi - lo > rel_tol * hi and rounds < max_rounds:
+        grid = lo + (hi - lo) * np.arange(1, per_round + 1) / (per_round + 1)
+        _, res = beta_sweep(rm, prob, grid, env)
+        feas = res["status"] == 0
+        k = int(np.argmax(feas)) if feas.any() else per_round
+        new_hi = grid[k] if k < per_round else hi
+        new_lo = grid[k - 1] if k > 0 else lo
+        lo, hi = float(new_lo), float(new_hi)
+        rounds += 1
+    return lo, hi, rounds

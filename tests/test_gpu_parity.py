@@ -332,3 +332,34 @@ def test_device_resident_inputs_equal_host(mp):
     for e in range(3):   # rows beyond path_len are unspecified (include/mpap.h)
         n = rh[e]["path_len"]
         assert np.array_equal(pd[e, :n], ph[e, :n])
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2: batched beta sweep / refinement on one roadmap
+# ---------------------------------------------------------------------------
+
+def test_beta_sweep_equals_single_and_oracle(mp, orc):
+    prob = make_problem(load_config("c2"))
+    rm = mp.pb.build_problem(prob)
+    orm = orc.build_roadmap(prob)
+    betas = [INF, 2.0, 1.5, 1.1762, 1.0, 0.9598, 0.93, 0.9, 0.5, 0.0]
+    paths, res = mp.pb.beta_sweep(rm, prob, betas)
+    for k, beta in enumerate(betas):
+        o = orc.search(orm, prob, beta)
+        assert res[k]["status"] == o["status"]
+        assert res[k]["relaxations"] == o["relaxations"] and res[k]["waves"] == o["waves"]
+        if o["status"] == 0:
+            assert paths[k, : res[k]["path_len"]].tolist() == o["path"].tolist()
+            assert np.float32(res[k]["cost"]) == o["cost"] and np.float32(res[k]["h"]) == o["h"]
+
+
+def test_refine_beta_min_brackets_oracle_feasibility(mp, orc):
+    """The refined bracket agrees with the oracle: infeasible at lo, feasible
+    at hi (Explore feasibility is decided identically on both sides)."""
+    prob = make_problem(load_config("c1"))
+    rm = mp.pb.build_problem(prob)
+    orm = orc.build_roadmap(prob)
+    lo, hi, rounds = mp.pb.refine_beta_min(rm, prob, hi=1.0, rel_tol=1e-4)
+    assert hi - lo <= 1e-4 * hi and rounds <= 6
+    assert orc.search(orm, prob, hi)["status"] == 0
+    assert orc.search(orm, prob, lo)["status"] == 3
