@@ -46,6 +46,7 @@ namespace cg = cooperative_groups;
 
 #define FULLM 0xffffffffu
 constexpr int kST = 512;              // threads per search CTA
+constexpr int kCluster = 8;           // CTAs per query in cluster mode (portable cluster size)
 enum : uint8_t { L_OPEN = 0, L_CLOSED = 1, L_DEAD = 2 };
 enum { OVF_LABELS = 1, OVF_CAND = 2, OVF_STAIR = 4 };
 constexpr int kRetryBase = 100;       // result.status = kRetryBase + OVF_* mask
@@ -75,9 +76,9 @@ struct SearchArgs {
   SlotCaps caps;
   int4* labels;
   uint8_t* lstate;
-  float2* stair_ch;
+  float2* stair_ch;    // two buffers per node (double-buffered merge)
   int32_t* stair_id;
-  int32_t* stair_n;
+  int32_t* stair_n;    // count | buffer parity << 30
   int32_t* cand_cnt;
   int32_t* cand_off;
   int4* cand;
@@ -122,6 +123,18 @@ struct GridTeam {
   __device__ __forceinline__ int warp() const { return rank() >> 5; }
   __device__ __forceinline__ int nwarps() const { return size() >> 5; }
   __device__ __forceinline__ void sync() const { cg::this_grid().sync(); }
+};
+
+// A thread-block cluster (hardware barrier across its CTAs, which run on
+// different SMs); used for batches with fewer queries than resident CTAs.
+struct ClusterTeam {
+  __device__ __forceinline__ int rank() const {
+    return (int)cg::this_cluster().block_rank() * blockDim.x + threadIdx.x;
+  }
+  __device__ __forceinline__ int size() const { return (int)cg::this_cluster().num_blocks() * blockDim.x; }
+  __device__ __forceinline__ int warp() const { return rank() >> 5; }
+  __device__ __forceinline__ int nwarps() const { return size() >> 5; }
+  __device__ __forceinline__ void sync() const { cg::this_cluster().sync(); }
 };
 
 // control words are re-read after every team barrier
@@ -188,6 +201,18 @@ __device__ void partition(const Team& team, const SearchArgs& A, Ctl* S, const i
   if (myminb != LLONG_MAX) atomicMin(&S->minb, myminb);
 }
 
+// Staircase of node x: count and buffer from sn[x]; entries sorted by
+// (cost ascending, h descending).  In a non-dominated set the h values of
+// successive cost groups strictly decrease, so min{h : cost < c} is the h of
+// the last entry with cost < c.
+constexpr int kStairCountMask = (1 << 30) - 1;
+__device__ __forceinline__ size_t stair_base(int snx, int x, int n, int K) {
+  return ((size_t)(snx >> 30) * n + x) * (size_t)K;
+}
+__device__ __forceinline__ bool key_less(float ac, float ah, float bc, float bh) {
+  return ac < bc || (ac == bc && ah > bh);
+}
+
 template <bool TRACE, typename Team>
 __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slot, int qpos) {
   const int q = A.qidx[qpos];
@@ -204,8 +229,8 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
   // slot views
   int4* labels = A.labels + (size_t)slot * C.L;
   uint8_t* lstate = A.lstate + (size_t)slot * C.L;
-  float2* sch = A.stair_ch + (size_t)slot * C.n * C.K;
-  int32_t* sid = A.stair_id + (size_t)slot * C.n * C.K;
+  float2* sch = A.stair_ch + (size_t)slot * 2 * C.n * C.K;    // buffer b of node x at (b * n + x) * K
+  int32_t* sid = A.stair_id + (size_t)slot * 2 * C.n * C.K;
   int32_t* sn = A.stair_n + (size_t)slot * C.n;
   int32_t* ccnt = A.cand_cnt + (size_t)slot * C.n;
   int32_t* coff = A.cand_off + (size_t)slot * C.n;
@@ -245,7 +270,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
   if (leader) {
     labels[0] = make_int4(Q.start, -1, __float_as_int(0.0f), __float_as_int(0.0f));
     lstate[0] = L_OPEN;
-    sch[(size_t)Q.start * C.K] = make_float2(0.0f, 0.0f);
+    sch[(size_t)Q.start * C.K] = make_float2(0.0f, 0.0f);   // buffer 0
     sid[(size_t)Q.start * C.K] = 0;
     sn[Q.start] = 1;
     G[0] = 0;
@@ -298,18 +323,21 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
               qh = (t > cc) ? t : cc;
               if ((double)qh <= beta) {
                 ++my_bpass;
-                const int m = sn[x];
+                const int snx = sn[x];
+                const int m = snx & kStairCountMask;
                 if (TRACE) {
                   if (atomicExch(&stamp[x], wave) != wave) { ++my_t; my_ss += (unsigned long long)m; }
                 }
                 // dominated by the node's non-dominated staircase?  Such a
-                // candidate cannot survive RemoveDominated (transitivity).
-                bool dom = false;
-                const float2* st = sch + (size_t)x * C.K;
-                for (int j = 0; j < m; ++j) {
-                  const float2 b = st[j];
-                  if (b.x < qc && b.y <= qh) { dom = true; break; }
+                // candidate cannot survive RemoveDominated (transitivity).  With
+                // the staircase sorted, only the last entry of cost < qc matters.
+                const float2* st = sch + stair_base(snx, x, n, C.K);
+                int lo = 0, hi = m;   // first index with cost >= qc
+                while (lo < hi) {
+                  const int mid = (lo + hi) >> 1;
+                  if (st[mid].x < qc) lo = mid + 1; else hi = mid;
                 }
+                const bool dom = lo > 0 && st[lo - 1].y <= qh;
                 emit = !dom;
               }
             }
@@ -362,83 +390,135 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
         const int x = touched[t];
         const int kc = ccnt[x];
         const int beg = coff[x] - kc;
-        const int m = sn[x];
-        float2* st = sch + (size_t)x * C.K;
-        int32_t* si = sid + (size_t)x * C.K;
-        int newm = 0;
-        // old staircase entries: killed if a candidate dominates them
-        for (int j0 = 0; j0 < m; j0 += 32) {
-          const int j = j0 + lane;
-          bool alive = false;
-          float2 o = make_float2(0.f, 0.f);
-          int oid = -1;
-          if (j < m) {
-            o = st[j];
-            oid = si[j];
-            alive = true;
+        const int snx = sn[x];
+        const int m = snx & kStairCountMask;
+        const int par = snx >> 30;
+        float2* st = sch + stair_base(snx, x, n, C.K);
+        int32_t* si = sid + stair_base(snx, x, n, C.K);
+        float2* nst = sch + ((size_t)(par ^ 1) * n + x) * (size_t)C.K;
+        int32_t* nsi = sid + ((size_t)(par ^ 1) * n + x) * (size_t)C.K;
+        int4* srt = cand + beg;   // candidate buffer is free after grouping: sorted copy
+        int4* sv = cs + beg;      // then the grouped range holds the sorted survivors
+        // 1. sort the node's candidates by (cost asc, h desc), ties by index
+        for (int q0 = 0; q0 < kc; q0 += 32) {
+          const int qq = q0 + lane;
+          if (qq < kc) {
+            const int4 cq = cs[beg + qq];
+            const float qc = __int_as_float(cq.y), qh = __int_as_float(cq.z);
+            int rank = 0;
             for (int r2 = 0; r2 < kc; ++r2) {
               const int4 cr = cs[beg + r2];
-              if (__int_as_float(cr.y) < o.x && __int_as_float(cr.z) <= o.y) { alive = false; break; }
+              const float rc = __int_as_float(cr.y), rh = __int_as_float(cr.z);
+              if (key_less(rc, rh, qc, qh) || (rc == qc && rh == qh && r2 < qq)) ++rank;
             }
-            if (!alive && lstate[oid] == L_OPEN) {
-              lstate[oid] = L_DEAD;
-              ++my_kill;
-            }
+            srt[rank] = cq;
           }
-          const unsigned am = __ballot_sync(FULLM, alive);
-          __syncwarp();
-          if (alive) {
-            const int pos = newm + __popc(am & lt);
-            st[pos] = o;
-            si[pos] = oid;
-          }
-          newm += __popc(am);
-          __syncwarp();
         }
-        // candidates: survive unless another candidate dominates them
+        __syncwarp();
+        // 2. candidate survivors: not dominated by a cheaper candidate (the
+        //    staircase cannot dominate them: filtered at expansion)
+        int ns = 0;
         for (int q0 = 0; q0 < kc; q0 += 32) {
           const int qq = q0 + lane;
           bool surv = false;
           int4 cq = make_int4(0, 0, 0, 0);
           if (qq < kc) {
-            cq = cs[beg + qq];
+            cq = srt[qq];
             surv = true;
             const float qc = __int_as_float(cq.y), qh = __int_as_float(cq.z);
-            for (int r2 = 0; r2 < kc; ++r2) {
-              const int4 cr = cs[beg + r2];
-              if (__int_as_float(cr.y) < qc && __int_as_float(cr.z) <= qh) { surv = false; break; }
+            for (int r2 = 0; r2 < qq; ++r2) {
+              const int4 cr = srt[r2];
+              if (!(__int_as_float(cr.y) < qc)) break;   // sorted: no cheaper candidate left
+              if (__int_as_float(cr.z) <= qh) { surv = false; break; }
             }
           }
           const unsigned sm = __ballot_sync(FULLM, surv);
-          if (sm) {
-            int lbase = 0, pbase = 0;
-            if (lane == 0) {
-              lbase = atomicAdd(&S->nlabels, __popc(sm));
-              pbase = atomicAdd(&S->psize, __popc(sm));
+          // survivors, in key order, go to the (now free) grouped range
+          if (surv) sv[ns + __popc(sm & lt)] = cq;
+          ns += __popc(sm);
+        }
+        __syncwarp();
+        // 3. old entries killed by a candidate (checking the surviving
+        //    candidates suffices: a dominated candidate's dominator dominates
+        //    too); dead ids marked in place
+        int na = 0;
+        for (int j0 = 0; j0 < m; j0 += 32) {
+          const int j = j0 + lane;
+          bool alive = false;
+          if (j < m) {
+            const float2 o = st[j];
+            alive = true;
+            for (int r2 = 0; r2 < ns; ++r2) {
+              const int4 cr = sv[r2];
+              if (!(__int_as_float(cr.y) < o.x)) break;
+              if (__int_as_float(cr.z) <= o.y) { alive = false; break; }
             }
-            lbase = __shfl_sync(FULLM, lbase, 0);
-            pbase = __shfl_sync(FULLM, pbase, 0);
-            if (lbase + __popc(sm) > C.L) {
-              if (lane == 0) atomicOr(&S->overflow, OVF_LABELS);
-            } else if (surv) {
-              const int rk = __popc(sm & lt);
-              const int id = lbase + rk;
-              labels[id] = make_int4(x, cq.w, cq.y, cq.z);
-              lstate[id] = L_OPEN;
-              pend[pbase + rk] = id;
-              const int pos = newm + rk;
-              if (pos < C.K) {
-                st[pos] = make_float2(__int_as_float(cq.y), __int_as_float(cq.z));
-                si[pos] = id;
+            if (!alive) {
+              const int oid = si[j];
+              if (lstate[oid] == L_OPEN) {
+                lstate[oid] = L_DEAD;
+                ++my_kill;
               }
             }
-            newm += __popc(sm);
-            if (lane == 0) my_ins += __popc(sm);
           }
+          const unsigned am = __ballot_sync(FULLM, alive);
+          // 4a. old survivor -> rank among old survivors + new survivors before it
+          if (alive) {
+            const float2 o = st[j];
+            int before = 0;
+            for (int r2 = 0; r2 < ns; ++r2) {
+              const int4 cr = sv[r2];
+              if (key_less(__int_as_float(cr.y), __int_as_float(cr.z), o.x, o.y)) ++before; else break;
+            }
+            const int pos = na + __popc(am & lt) + before;
+            if (pos < C.K) {
+              nst[pos] = o;
+              nsi[pos] = si[j];
+            }
+          }
+          na += __popc(am);
+          if (!alive && j < m) si[j] = -1;
+        }
+        __syncwarp();
+        // 4b. new survivors: labels, pending list, position = own rank + old survivors before it
+        for (int q0 = 0; q0 < ns; q0 += 32) {
+          const int qq = q0 + lane;
+          const bool v = qq < ns;
+          const unsigned vm = __ballot_sync(FULLM, v);
+          int lbase = 0, pbase = 0;
+          if (lane == 0) {
+            lbase = atomicAdd(&S->nlabels, __popc(vm));
+            pbase = atomicAdd(&S->psize, __popc(vm));
+          }
+          lbase = __shfl_sync(FULLM, lbase, 0);
+          pbase = __shfl_sync(FULLM, pbase, 0);
+          if (lbase + __popc(vm) > C.L) {
+            if (lane == 0) atomicOr(&S->overflow, OVF_LABELS);
+          } else if (v) {
+            const int4 cq = sv[qq];
+            const float qc = __int_as_float(cq.y), qh = __int_as_float(cq.z);
+            const int id = lbase + lane;
+            labels[id] = make_int4(x, cq.w, cq.y, cq.z);
+            lstate[id] = L_OPEN;
+            pend[pbase + lane] = id;
+            int before = 0;   // alive old entries with key <= (qc, qh)
+            for (int j = 0; j < m; ++j) {
+              const float2 o = st[j];
+              if (key_less(qc, qh, o.x, o.y)) break;
+              if (si[j] >= 0) ++before;
+            }
+            const int pos = qq + before;
+            if (pos < C.K) {
+              nst[pos] = make_float2(qc, qh);
+              nsi[pos] = id;
+            }
+          }
+          if (lane == 0) my_ins += __popc(vm);
         }
         if (lane == 0) {
+          const int newm = na + ns;
           if (newm > C.K) atomicOr(&S->overflow, OVF_STAIR);
-          sn[x] = min(newm, C.K);
+          sn[x] = min(newm, C.K) | ((par ^ 1) << 30);
         }
       }
       if (my_kill) atomicAdd(&S->killed, my_kill);
@@ -516,9 +596,11 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
   team.sync();
   for (int x = tid; x < n; x += nthr) {
     if (!goal[x]) continue;
-    const int m = sn[x];
+    const int snx = sn[x];
+    const int m = snx & kStairCountMask;
+    const float2* st = sch + stair_base(snx, x, n, C.K);
     for (int j = 0; j < m; ++j) {
-      const float2 ch = sch[(size_t)x * C.K + j];
+      const float2 ch = st[j];
       const unsigned long long key = ((unsigned long long)__float_as_uint(ch.x) << 32) | __float_as_uint(ch.y);
       atomicMin(&S->best_key, key);
     }
@@ -527,13 +609,16 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
   const unsigned long long best_key = vld(S->best_key);
   for (int x = tid; x < n; x += nthr) {
     if (!goal[x]) continue;
-    const int m = sn[x];
+    const int snx = sn[x];
+    const int m = snx & kStairCountMask;
+    const float2* st = sch + stair_base(snx, x, n, C.K);
+    const int32_t* si = sid + stair_base(snx, x, n, C.K);
     for (int j = 0; j < m; ++j) {
-      const float2 ch = sch[(size_t)x * C.K + j];
+      const float2 ch = st[j];
       const unsigned long long key = ((unsigned long long)__float_as_uint(ch.x) << 32) | __float_as_uint(ch.y);
       if (key == best_key) {
         const int slot_t = atomicAdd(&S->nties, 1);
-        if (slot_t < 32) S->ties[slot_t] = sid[(size_t)x * C.K + j];
+        if (slot_t < 32) S->ties[slot_t] = si[j];
       }
     }
   }
@@ -600,6 +685,25 @@ __global__ void __launch_bounds__(kST) k_search(SearchArgs A) {
   }
 }
 
+// Batched queries with one thread-block cluster per query at a time (queries
+// pulled from a counter by the cluster's leader).  Control words live in
+// global memory, one Ctl per cluster slot.
+template <bool TRACE>
+__global__ void __launch_bounds__(kST) k_search_cluster(SearchArgs A, Ctl* S_all) {
+  const ClusterTeam team;
+  const int slot = blockIdx.x / cg::this_cluster().num_blocks();
+  Ctl* S = S_all + slot;
+  while (true) {
+    if (team.rank() == 0) S->q = atomicAdd(A.work, 1);
+    team.sync();
+    const int qpos = vld(S->q);
+    team.sync();
+    if (qpos >= A.nq) break;
+    run_query<TRACE>(team, A, S, slot, qpos);
+    team.sync();
+  }
+}
+
 // A single query over the whole grid (cooperative launch; grid.sync between
 // the phases of each wave).  Control words live in global memory.
 template <bool TRACE>
@@ -631,8 +735,8 @@ size_t carve(SearchArgs* A, const SlotCaps& c, int nslots, char* base) {
   void* p;
   p = take(sizeof(int4) * (size_t)c.L);                 if (A) A->labels = (int4*)p;
   p = take((size_t)c.L);                                if (A) A->lstate = (uint8_t*)p;
-  p = take(sizeof(float2) * (size_t)c.n * c.K);         if (A) A->stair_ch = (float2*)p;
-  p = take(sizeof(int32_t) * (size_t)c.n * c.K);        if (A) A->stair_id = (int32_t*)p;
+  p = take(sizeof(float2) * 2 * (size_t)c.n * c.K);     if (A) A->stair_ch = (float2*)p;
+  p = take(sizeof(int32_t) * 2 * (size_t)c.n * c.K);    if (A) A->stair_id = (int32_t*)p;
   p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->stair_n = (int32_t*)p;
   p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->cand_cnt = (int32_t*)p;
   p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->cand_off = (int32_t*)p;
@@ -667,6 +771,7 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
   if (trace) CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_grid, k_search_grid<true>, kST, 0));
   else CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_grid, k_search_grid<false>, kST, 0));
   const bool use_grid = coop && occ_grid > 0 && getenv("MPAP_SEARCH_CTA") == nullptr;
+  const bool use_cluster = getenv("MPAP_SEARCH_CTA") == nullptr && getenv("MPAP_SEARCH_NO_CLUSTER") == nullptr;
   SlotCaps caps;
   caps.n = rm->n_max;
   caps.K = std::max(64, rm->hint_K);
@@ -703,9 +808,11 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     // one query: the whole grid works on it (cooperative launch); otherwise one
     // CTA per query and as many slots as resident CTAs
     const bool grid_mode = (nrun == 1) && use_grid;
-    const int nslots = grid_mode ? 1 : std::min(nrun, nsm * occ);
+    // few queries: one cluster of kCluster CTAs per query; many: one CTA each
+    const bool cluster_mode = !grid_mode && use_cluster && nrun * kCluster <= nsm * occ;
+    const int nslots = grid_mode ? 1 : cluster_mode ? nrun : std::min(nrun, nsm * occ);
     const size_t sb_slots = carve(nullptr, caps, nslots, nullptr);
-    const size_t sb = sb_slots + sizeof(Ctl) + 256;
+    const size_t sb = sb_slots + sizeof(Ctl) * (size_t)nslots + 256;
     HostTimer ta("slot arena");
     void* base = workspace(st, WS_SEARCH, sb);
     if (!base) {
@@ -741,11 +848,26 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     CKS(cudaMemsetAsync(d_work, 0, sizeof(int), st));
     {
       ProfScope ps("k_search", st);
+      Ctl* d_ctl = reinterpret_cast<Ctl*>(static_cast<char*>(base) + ((sb_slots + 255) & ~size_t(255)));
       if (grid_mode) {
-        Ctl* d_ctl = reinterpret_cast<Ctl*>(static_cast<char*>(base) + ((sb_slots + 255) & ~size_t(255)));
         void* args[] = {&A, &d_ctl};
         const void* fn = trace ? (const void*)k_search_grid<true> : (const void*)k_search_grid<false>;
         CKS(cudaLaunchCooperativeKernel(fn, dim3(nsm * occ_grid), dim3(kST), args, 0, st));
+      } else if (cluster_mode) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(nslots * kCluster);
+        cfg.blockDim = dim3(kST);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kCluster;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (trace) CKS(cudaLaunchKernelEx(&cfg, k_search_cluster<true>, A, d_ctl));
+        else CKS(cudaLaunchKernelEx(&cfg, k_search_cluster<false>, A, d_ctl));
       } else if (trace) {
         k_search<true><<<nslots, kST, 0, st>>>(A);
       } else {
