@@ -39,7 +39,7 @@ namespace mpap {
 #define MPAP_LAZY_INV 0
 #endif
 #ifndef MPAP_EDGES_MIN_BLOCKS
-#define MPAP_EDGES_MIN_BLOCKS 2
+#define MPAP_EDGES_MIN_BLOCKS 1
 #endif
 constexpr int kWarps = 8;                 // warps per block in the build kernels
 constexpr double kCullMargin = 1e-6;      // absolute; >> rounding of O(100) coordinates
@@ -634,13 +634,37 @@ __device__ __noinline__ double mlp_out0(const double* w, double z0, double z1, d
 }
 
 
-// Bounding box of the positions of steps t in [ta, tb] along the edge, computed
-// analytically by every lane (no shuffles): endpoints plus, for the cubic, the
-// interior stationary points.  It contains the contract's step positions up to
-// rounding (~1e-15 relative), far inside the culling margins.
+// Stationary points of the cubic position p_j(t) per axis (roots of
+// p'(t) = v0 + 2 c2 t + 3 c3 t^2), computed once per edge; -1 = none.
+template <int D>
+__device__ __forceinline__ void cubic_stationary(const double* su, const double* c2, const double* c3, double* r0,
+                                                 double* r1) {
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const double A = 3.0 * c3[j], Bq = 2.0 * c2[j], Cq = su[D + j];
+    r0[j] = -1.0;
+    r1[j] = -1.0;
+    if (A != 0.0) {
+      const double disc = Bq * Bq - 4.0 * A * Cq;
+      if (disc >= 0.0) {
+        const double sq = sqrt(disc);
+        r0[j] = (-Bq - sq) / (2.0 * A);
+        r1[j] = (-Bq + sq) / (2.0 * A);
+      }
+    } else if (Bq != 0.0) {
+      r0[j] = -Cq / Bq;
+    }
+  }
+}
+
+// Bounding box of the positions of steps t in [ta, tb] along the edge: the
+// endpoints plus the interior stationary points of the cubic.  It contains
+// the contract's step positions up to rounding (~1e-15 relative), far inside
+// the culling margins.  Warp-uniform (every lane computes the same box).
 template <int D, int DYN>
 __device__ __forceinline__ void chunk_bbox(const double* su, const double* sv, const double* c2, const double* c3,
-                                           double T, double ta, double tb, double* lo, double* hi) {
+                                           const double* r0, const double* r1, double T, double ta, double tb,
+                                           double* lo, double* hi) {
   double xa[D], xb[D];
   if (DYN == 0) {
     const double sa = ta / T, sb = tb / T;
@@ -658,26 +682,13 @@ __device__ __forceinline__ void chunk_bbox(const double* su, const double* sv, c
     lo[j] = fmin(xa[j], xb[j]);
     hi[j] = fmax(xa[j], xb[j]);
     if (DYN == 1) {
-      // p'(t) = v0 + 2 c2 t + 3 c3 t^2 = 0
-      const double A = 3.0 * c3[j], Bq = 2.0 * c2[j], Cq = su[D + j];
-      double r0 = -1.0, r1 = -1.0;
-      if (A != 0.0) {
-        const double disc = Bq * Bq - 4.0 * A * Cq;
-        if (disc >= 0.0) {
-          const double sq = sqrt(disc);
-          r0 = (-Bq - sq) / (2.0 * A);
-          r1 = (-Bq + sq) / (2.0 * A);
-        }
-      } else if (Bq != 0.0) {
-        r0 = -Cq / Bq;
-      }
-      if (r0 > ta && r0 < tb) {
-        const double x = fma(r0, fma(r0, fma(r0, c3[j], c2[j]), su[D + j]), su[j]);
+      if (r0[j] > ta && r0[j] < tb) {
+        const double x = fma(r0[j], fma(r0[j], fma(r0[j], c3[j], c2[j]), su[D + j]), su[j]);
         lo[j] = fmin(lo[j], x);
         hi[j] = fmax(hi[j], x);
       }
-      if (r1 > ta && r1 < tb) {
-        const double x = fma(r1, fma(r1, fma(r1, c3[j], c2[j]), su[D + j]), su[j]);
+      if (r1[j] > ta && r1[j] < tb) {
+        const double x = fma(r1[j], fma(r1[j], fma(r1[j], c3[j], c2[j]), su[D + j]), su[j]);
         lo[j] = fmin(lo[j], x);
         hi[j] = fmax(hi[j], x);
       }
@@ -699,10 +710,13 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
   const double kk = ceil(T / P.dt);
   const int K = (kk < 1.0) ? 1 : (int)kk;
   const double Dl = T / (double)K;
-  double c2[D], c3[D];
+  double c2[D], c3[D], r0[D], r1[D];
 #pragma unroll
-  for (int j = 0; j < D; ++j) { c2[j] = 0.0; c3[j] = 0.0; }
-  if (DYN == 1) di_traj<D>(su, sv, T, c2, c3);
+  for (int j = 0; j < D; ++j) { c2[j] = 0.0; c3[j] = 0.0; r0[j] = -1.0; r1[j] = -1.0; }
+  if (DYN == 1) {
+    di_traj<D>(su, sv, T, c2, c3);
+    cubic_stationary<D>(su, c2, c3, r0, r1);
+  }
   const int hoff = P.hoff;
   double omega = 0.0;
   double hu0 = 0.0, hu1 = 0.0, hv0 = 0.0, hv1 = 0.0;
@@ -718,53 +732,47 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
   constexpr int heur = HEUR;
   const float half_fov = acosf((float)P.fov_cos_half);
   const unsigned lt = lanemask_lt();
+  bool ang = false;
+  float ux = 0.0f, uy = 0.0f, c1 = 0.0f, s1 = 0.0f, smax = -1.0f;
+  if (heur >= 2) {
+    const float ax = (float)hu0, ay = (float)hu1;
+    const float sb = (float)(((double)(K - 1) * Dl) / T);
+    const float bx = fmaf(sb, (float)hv0 - ax, ax), by = fmaf(sb, (float)hv1 - ay, ay);
+    const float ex = bx - ax, ey = by - ay;
+    const float ee = ex * ex + ey * ey;
+    float tq = (ee > 0.0f) ? -(ax * ex + ay * ey) / ee : 0.0f;
+    tq = fminf(fmaxf(tq, 0.0f), 1.0f);
+    const float qx = ax + tq * ex, qy = ay + tq * ey;
+    if (qx * qx + qy * qy > 1e-4f) {
+      const float na = rsqrtf(ax * ax + ay * ay), nb = rsqrtf(bx * bx + by * by);
+      const float dax = ax * na, day = ay * na, dbx = bx * nb, dby = by * nb;
+      const float mx = dax + dbx, my = day + dby;
+      const float mn = sqrtf(mx * mx + my * my);
+      if (mn > 1e-2f) {
+        ux = mx / mn;
+        uy = my / mn;
+        const float dev = 0.5f * atan2f(fabsf(dax * dby - day * dbx), dax * dbx + day * dby);
+        const float beta0 = acosf((float)P.fov_cos_half) + dev + 2e-3f;   // half angle + arc + margin
+        const float wmax = 3.1315927f - beta0;                             // keep the total below pi - 0.01
+        if (wmax > 0.0f) {
+          ang = true;
+          c1 = cosf(beta0);
+          s1 = sinf(beta0);
+          smax = (wmax >= 1.5707963f) ? 2.0f : sinf(wmax);
+        }
+      }
+    }
+  }
   double s = 0.0, c = 0.0;
   for (int k0 = 0; k0 < K; k0 += 32) {
     const int nk = min(32, K - k0);
     const double ta = (double)k0 * Dl, tb = (double)(k0 + nk - 1) * Dl;
     double lo[D], hi[D];
-    chunk_bbox<D, DYN>(su, sv, c2, c3, T, ta, tb, lo, hi);
+    chunk_bbox<D, DYN>(su, sv, c2, c3, r0, r1, T, ta, tb, lo, hi);
     // Conservative single-precision culls (only discard features whose exact
     // test provably fails; margins >> float rounding):
     //  * range: distance(feature, chunk box) > R + 1e-3;
-    //  * angle (heading heuristics): the FOV test needs the horizontal angle
-    //    between heading and sight line <= the half angle (the 3D angle is
-    //    never smaller for a horizontal heading).  Headings (1-s) hu + s hv on
-    //    [s0, s1] rotate monotonically between their end directions (a chord);
-    //    sight lines from the chunk's xy-rectangle (circumradius rho inflated
-    //    by 1e-4 m) lie within asin(rho / dc) of the centre direction.
-    bool ang = false;
-    float ux = 0.0f, uy = 0.0f, c1 = 0.0f, s1 = 0.0f, smax = -1.0f;
-    if (heur >= 2) {
-      const float sa = (float)(ta / T), sb = (float)(tb / T);
-      const float ax = (1.0f - sa) * (float)hu0 + sa * (float)hv0, ay = (1.0f - sa) * (float)hu1 + sa * (float)hv1;
-      const float bx = (1.0f - sb) * (float)hu0 + sb * (float)hv0, by = (1.0f - sb) * (float)hu1 + sb * (float)hv1;
-      // distance of the chord [a, b] from the origin (headings must stay away from 0)
-      const float ex = bx - ax, ey = by - ay;
-      const float ee = ex * ex + ey * ey;
-      float tq = (ee > 0.0f) ? -(ax * ex + ay * ey) / ee : 0.0f;
-      tq = fminf(fmaxf(tq, 0.0f), 1.0f);
-      const float qx = ax + tq * ex, qy = ay + tq * ey;
-      if (qx * qx + qy * qy > 1e-4f) {
-        const float na = rsqrtf(ax * ax + ay * ay), nb = rsqrtf(bx * bx + by * by);
-        const float dax = ax * na, day = ay * na, dbx = bx * nb, dby = by * nb;
-        const float mx = dax + dbx, my = day + dby;
-        const float mn = sqrtf(mx * mx + my * my);
-        if (mn > 1e-2f) {
-          ux = mx / mn;
-          uy = my / mn;
-          const float dev = 0.5f * atan2f(fabsf(dax * dby - day * dbx), dax * dbx + day * dby);
-          const float beta0 = half_fov + dev + 2e-3f;   // half angle + arc + margin
-          const float wmax = 3.1315927f - beta0;        // keep the total below pi - 0.01
-          if (wmax > 0.0f) {
-            ang = true;
-            c1 = cosf(beta0);
-            s1 = sinf(beta0);
-            smax = (wmax >= 1.5707963f) ? 2.0f : sinf(wmax);
-          }
-        }
-      }
-    }
+    //  * bearing (heading heuristics): see the per-edge heading arc above.
     const float flx = (float)lo[0], fhx = (float)hi[0], fly = (float)lo[1], fhy = (float)hi[1];
     const float flz = (D == 3) ? (float)lo[D - 1] : 0.0f, fhz = (D == 3) ? (float)hi[D - 1] : 0.0f;
     const float ccx = 0.5f * (flx + fhx), ccy = 0.5f * (fly + fhy);
