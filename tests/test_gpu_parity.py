@@ -363,3 +363,15 @@ def test_refine_beta_min_brackets_oracle_feasibility(mp, orc):
     assert hi - lo <= 1e-4 * hi and rounds <= 6
     assert orc.search(orm, prob, hi)["status"] == 0
     assert orc.search(orm, prob, lo)["status"] == 3
+
+
+def test_search_full_size_c4_golden(mp):
+    """C4 (n = 16001, 200 boxes, 400 features) at BASELINE size: the whole-grid
+    single-query search vs the stored oracle results (beta = inf and
+    2 x beta_min)."""
+    prob = make_problem(load_config("c4"))
+    rm = mp.pb.build_problem(prob)
+    gold = json.load(open(os.path.join(GOLDEN, "c4_full.json")))
+    info = mp.mpap_roadmap_info(rm)
+    assert info["nnz"] == gold["nnz"] and info["nnz_free"] == gold["nnz_free"]
+    _golden_check(mp, rm, prob, gold)

@@ -1,1 +1,1 @@
-for v in libmpap.so libmpap_m1.so; do MPAP_LIB=paper_1705_02408_b200/$v timeout 300 python tools/bench_build.py 64 3 > gpurun_out/bb.log 2>&1; python -c "import json; d=json.loads(open('gpurun_out/bb.log').read().strip().splitlines()[-1]); print(d['lib'], {k: round(v,1) for k,v in d['kernel_ms'].items()})" >> gpurun_out/res.txt; done
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "c4_golden" 2>&1 | tail -3 >> gpurun_out/res.txt
