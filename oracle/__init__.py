@@ -111,6 +111,16 @@ def lib():
                                  C.c_double, C.c_double, i32p, C.c_int32, C.POINTER(OrcResult),
                                  C.POINTER(OrcWave), C.c_int32]
         L.orc_search.restype = C.c_int
+        L.orc_search_ex.argtypes = L.orc_search.argtypes + [f32p, f32p, C.c_int32]
+        L.orc_search_ex.restype = C.c_int
+        L.orc_fold_peak.argtypes = [dp, C.c_int, dp, dp]
+        L.orc_fold_peak.restype = None
+        L.orc_fold_stepwise_peak.argtypes = [C.c_double, dp, C.c_int]
+        L.orc_fold_stepwise_peak.restype = C.c_double
+        L.orc_edge_peak.argtypes = [C.POINTER(OrcEnv), C.POINTER(OrcParams), C.c_int, C.c_int, dp, dp]
+        L.orc_edge_peak.restype = C.c_int
+        L.orc_build_peaks.argtypes = [C.POINTER(OrcEnv), C.POINTER(OrcParams), i32p, i32p, f32p, f32p]
+        L.orc_build_peaks.restype = None
         L.orc_goal_mask.argtypes = [dp, C.c_int32, C.c_int32, C.c_int32, dp, dp, u8p]
         L.orc_goal_mask.restype = None
         _lib = L
@@ -219,6 +229,32 @@ def fold_summary(inc) -> tuple:
     return s.value, c.value
 
 
+def fold_peak(inc) -> tuple:
+    a = np.ascontiguousarray(inc, dtype=np.float64)
+    S = C.c_double()
+    Cc = C.c_double()
+    lib().orc_fold_peak(_ptr(a, C.c_double), len(a), C.byref(S), C.byref(Cc))
+    return S.value, Cc.value
+
+
+def fold_stepwise_peak(h0: float, inc) -> float:
+    a = np.ascontiguousarray(inc, dtype=np.float64)
+    return float(lib().orc_fold_stepwise_peak(h0, _ptr(a, C.c_double), len(a)))
+
+
+def build_peaks(prob, rm) -> tuple:
+    """(S, C) f32 peak summaries of every edge of an oracle roadmap (NEXT-3)."""
+    ctx = _Ctx(prob)
+    nnz = len(rm["dst"])
+    S = np.zeros(max(nnz, 1), np.float32)
+    Cc = np.zeros(max(nnz, 1), np.float32)
+    rp = np.ascontiguousarray(rm["row_ptr"], dtype=np.int32)
+    dst = np.ascontiguousarray(rm["dst"] if nnz else np.zeros(1, np.int32), dtype=np.int32)
+    lib().orc_build_peaks(C.byref(ctx.env), C.byref(ctx.prm), _ptr(rp, C.c_int32), _ptr(dst, C.c_int32),
+                          _ptr(S, C.c_float), _ptr(Cc, C.c_float))
+    return S[:nnz].copy(), Cc[:nnz].copy()
+
+
 def fold_stepwise(h0: float, inc) -> float:
     a = np.ascontiguousarray(inc, dtype=np.float64)
     return float(lib().orc_fold_stepwise(h0, _ptr(a, C.c_double), len(a)))
@@ -280,8 +316,11 @@ STATUS = {0: "OK", 3: "NO_FEASIBLE_PLAN", 4: "BUFFER_TOO_SMALL", 5: "OUT_OF_MEMO
 
 
 def search_csr(n: int, row_ptr, dst, coll, w, s, c, goal, start: int, beta: float, lam: float, r: float,
-               path_cap: int = 65536, waves_cap: int = 100000) -> Dict[str, Any]:
-    """Alg. 3 on an explicit CSR (hand-built graphs or an oracle roadmap)."""
+               path_cap: int = 65536, waves_cap: int = 100000, S=None, Cp=None, forall_t: bool = False
+               ) -> Dict[str, Any]:
+    """Alg. 3 on an explicit CSR (hand-built graphs or an oracle roadmap).
+    With forall_t, the cutoff applies to every step of an edge via the peak
+    summaries (S, Cp) (NEXT-3)."""
     row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int32)
     dst = np.ascontiguousarray(dst, dtype=np.int32)
     coll = np.ascontiguousarray(coll, dtype=np.uint8)
@@ -289,15 +328,23 @@ def search_csr(n: int, row_ptr, dst, coll, w, s, c, goal, start: int, beta: floa
     s = np.ascontiguousarray(s, dtype=np.float32)
     c = np.ascontiguousarray(c, dtype=np.float32)
     goal = np.ascontiguousarray(goal, dtype=np.uint8)
+    if forall_t:
+        S = np.ascontiguousarray(S, dtype=np.float32)
+        Cp = np.ascontiguousarray(Cp, dtype=np.float32)
     if dst.size == 0:  # keep valid pointers
         dst, coll, w, s, c = np.zeros(1, np.int32), np.zeros(1, np.uint8), np.zeros(1, np.float32), \
             np.zeros(1, np.float32), np.zeros(1, np.float32)
+        if forall_t:
+            S, Cp = np.zeros(1, np.float32), np.zeros(1, np.float32)
+    if not forall_t:
+        S = Cp = np.zeros(1, np.float32)
     path = np.zeros(path_cap, dtype=np.int32)
     res = OrcResult()
     waves = (OrcWave * waves_cap)()
-    lib().orc_search(n, _ptr(row_ptr, C.c_int32), _ptr(dst, C.c_int32), _ptr(coll, C.c_uint8), _ptr(w, C.c_float),
-                     _ptr(s, C.c_float), _ptr(c, C.c_float), _ptr(goal, C.c_uint8), start, beta, lam, r,
-                     _ptr(path, C.c_int32), path_cap, C.byref(res), waves, waves_cap)
+    lib().orc_search_ex(n, _ptr(row_ptr, C.c_int32), _ptr(dst, C.c_int32), _ptr(coll, C.c_uint8),
+                        _ptr(w, C.c_float), _ptr(s, C.c_float), _ptr(c, C.c_float), _ptr(goal, C.c_uint8), start,
+                        beta, lam, r, _ptr(path, C.c_int32), path_cap, C.byref(res), waves, waves_cap,
+                        _ptr(S, C.c_float), _ptr(Cp, C.c_float), 1 if forall_t else 0)
     nw = min(res.waves, waves_cap)
     wave_arr = np.array([[getattr(waves[k], f) for f in WAVE_FIELDS] for k in range(nw)], dtype=np.int64).reshape(-1, 8)
     return {
@@ -310,10 +357,15 @@ def search_csr(n: int, row_ptr, dst, coll, w, s, c, goal, start: int, beta: floa
 
 
 def search(rm: Dict[str, np.ndarray], prob, beta: float, lam: Optional[float] = None,
-           r: Optional[float] = None, start: Optional[int] = None) -> Dict[str, Any]:
+           r: Optional[float] = None, start: Optional[int] = None, forall_t: bool = False) -> Dict[str, Any]:
+    S = Cp = None
+    if forall_t:
+        if "S" not in rm:
+            rm["S"], rm["C"] = build_peaks(prob, rm)
+        S, Cp = rm["S"], rm["C"]
     return search_csr(rm["n"], rm["row_ptr"], rm["dst"], rm["coll"], rm["w"], rm["s"], rm["c"], goal_mask(prob),
                       prob.start if start is None else start, beta, prob.lam if lam is None else lam,
-                      prob.r if r is None else r)
+                      prob.r if r is None else r, S=S, Cp=Cp, forall_t=forall_t)
 
 
 # ---------------------------------------------------------------------------

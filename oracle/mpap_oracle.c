@@ -384,6 +384,35 @@ void orc_fold_summary(const double *inc, int K, double *s_out, double *c_out) {
   *c_out = c;
 }
 
+/* Peak summary of an edge (NEXT-3; Eq. 2's "for all t"): the largest
+ * value the per-step fold reaches along the edge, from h0, is
+ * max(C, h0 + S) with S = max over prefixes of s and C = max over prefixes of
+ * c (prefix 0 included: S, C >= 0).  Same fold as orc_fold_summary. */
+void orc_fold_peak(const double *inc, int K, double *S_out, double *C_out) {
+  double s = 0.0, c = 0.0, S = 0.0, C = 0.0;
+  for (int k = 0; k < K; ++k) {
+    double t = c + inc[k];
+    c = (t > 0.0) ? t : 0.0;
+    s = s + inc[k];
+    S = (s > S) ? s : S;
+    C = (c > C) ? c : C;
+  }
+  *S_out = S;
+  *C_out = C;
+}
+
+/* Largest value of the stepwise fold from h0 over the steps (plain definition
+ * for the pins of orc_fold_peak). */
+double orc_fold_stepwise_peak(double h0, const double *inc, int K) {
+  double h = h0, mx = h0;
+  for (int k = 0; k < K; ++k) {
+    double t = h + inc[k];
+    h = (t > 0.0) ? t : 0.0;
+    if (h > mx) mx = h;
+  }
+  return mx;
+}
+
 /* Stepwise clamp fold of P:324-328 from h0 (the plain definition; used by the
  * pins to check the summary). */
 double orc_fold_stepwise(double h0, const double *inc, int K) {
@@ -443,6 +472,35 @@ int orc_edge(const orc_env *E, const orc_params *prm, int u, int v,
     if (inc != stackbuf) free(inc);
   }
   return 1;
+}
+
+/* Peak summary (S, C) of edge u -> v (0, 0 if colliding or not an edge). */
+int orc_edge_peak(const orc_env *E, const orc_params *prm, int u, int v, double *S64, double *C64) {
+  double c64, tau, s64, h64;
+  int cl;
+  *S64 = 0.0;
+  *C64 = 0.0;
+  if (!orc_edge(E, prm, u, v, &c64, &tau, &cl, &s64, &h64)) return 0;
+  if (cl) return 1;
+  int K = orc_edge_increments(E, prm, u, v, c64, tau, NULL, 0);
+  double *inc = (double *)malloc(sizeof(double) * (size_t)(K > 0 ? K : 1));
+  orc_edge_increments(E, prm, u, v, c64, tau, inc, K);
+  orc_fold_peak(inc, K, S64, C64);
+  free(inc);
+  return 1;
+}
+
+/* Peaks of every edge of a built CSR (rows of orc_build). */
+void orc_build_peaks(const orc_env *E, const orc_params *prm, const int32_t *row_ptr, const int32_t *dst,
+                     float *S, float *C) {
+  for (int u = 0; u < E->n; ++u) {
+    for (int32_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) {
+      double S64, C64;
+      orc_edge_peak(E, prm, u, dst[e], &S64, &C64);
+      S[e] = (float)S64;
+      C[e] = (float)C64;
+    }
+  }
 }
 
 /* ------------------------------------------------------------------------ */
@@ -590,11 +648,29 @@ static int path_less(const int32_t *a, int la, const int32_t *b, int lb) {
   return la < lb;
 }
 
+/* forall_t != 0 (NEXT-3): the cutoff A3.9 is applied to every step along
+ * the edge, peak = max(C_e, p.h + S_e) <= beta (f32, same max as PH), instead
+ * of the node value only (reading R11).  Everything else is Alg. 3. */
+int orc_search_ex(int32_t n, const int32_t *row_ptr, const int32_t *dst, const uint8_t *coll,
+                  const float *w, const float *s, const float *c, const uint8_t *goal,
+                  int32_t start, double beta, double lambda, double r,
+                  int32_t *path, int32_t path_cap, orc_result *res,
+                  orc_wave *waves, int32_t waves_cap, const float *S, const float *C, int32_t forall_t);
+
 int orc_search(int32_t n, const int32_t *row_ptr, const int32_t *dst, const uint8_t *coll,
                const float *w, const float *s, const float *c, const uint8_t *goal,
                int32_t start, double beta, double lambda, double r,
                int32_t *path, int32_t path_cap, orc_result *res,
                orc_wave *waves, int32_t waves_cap) {
+  return orc_search_ex(n, row_ptr, dst, coll, w, s, c, goal, start, beta, lambda, r, path, path_cap, res, waves,
+                       waves_cap, NULL, NULL, 0);
+}
+
+int orc_search_ex(int32_t n, const int32_t *row_ptr, const int32_t *dst, const uint8_t *coll,
+                  const float *w, const float *s, const float *c, const uint8_t *goal,
+                  int32_t start, double beta, double lambda, double r,
+                  int32_t *path, int32_t path_cap, orc_result *res,
+                  orc_wave *waves, int32_t waves_cap, const float *S, const float *C, int32_t forall_t) {
   memset(res, 0, sizeof(*res));
   const double T = lambda * r;                    /* threshold step lambda r_n */
   labels_t L;
@@ -643,7 +719,13 @@ int orc_search(int32_t n, const int32_t *row_ptr, const int32_t *dst, const uint
         float qc = pc + w[e];                        /* p.cost + Cost(p.head, x)   */
         float t = ph + s[e];                         /* PH(x, p) = max(c_e, h + s_e) (R10) */
         float qh = (t > c[e]) ? t : c[e];
-        if ((double)qh <= beta) {                    /* A3.9 cutoff                */
+        int ok = (double)qh <= beta;                 /* A3.9 cutoff                */
+        if (forall_t && ok) {                        /* NEXT-3: every step of the edge */
+          float t2 = ph + S[e];
+          float pk = (t2 > C[e]) ? t2 : C[e];
+          ok = (double)pk <= beta;
+        }
+        if (ok) {
           ++wv.beta_pass;
           if (!touched[x]) {
             touched[x] = 1;
