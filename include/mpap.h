@@ -176,6 +176,33 @@ mpap_status mpap_search_batch(const mpap_roadmap *rm, int32_t n_queries, const i
                               void *cuda_stream);
 
 /*
+ * Search flags (mpap_search_ex / mpap_search_batch_ex).
+ *   MPAP_SEARCH_FORALL_T  Eq. 2 bounds the perception heuristic for
+ *       all t, not only at the roadmap nodes (reading R11, SURVEY.md §8(f)
+ *       NEXT-3): an edge is relaxed only if, in addition to the A3.9 cutoff,
+ *       every step of the clamp fold along it stays within the bound:
+ *       max(C_e, h + S_e) <= beta (f32 sum and max, compared in f64), where
+ *       (S_e, C_e) are the prefix maxima of the edge's summary (s, c)
+ *       (mpap_roadmap_export_peaks).  The roadmap must carry peaks (built by
+ *       mpap_build_roadmap*, or set by mpap_roadmap_set_peaks after import),
+ *       else INVALID_ARGUMENT.
+ */
+#define MPAP_SEARCH_FORALL_T 1u
+
+/* mpap_search with flags (0 = mpap_search). */
+mpap_status mpap_search_ex(const mpap_roadmap *rm, int32_t env, int32_t start, const mpap_goal *goal,
+                           double perception_bound, double lambda, uint32_t flags, int32_t *path,
+                           int32_t path_capacity, mpap_result *result, mpap_wave *waves,
+                           int32_t waves_capacity, void *cuda_stream);
+
+/* mpap_search_batch with flags applied to every query (0 = mpap_search_batch). */
+mpap_status mpap_search_batch_ex(const mpap_roadmap *rm, int32_t n_queries, const int32_t *envs,
+                                 const int32_t *starts, const mpap_goal *goals,
+                                 const double *perception_bounds, double lambda, uint32_t flags,
+                                 int32_t *paths, int32_t path_capacity, mpap_result *results, int32_t mem,
+                                 void *cuda_stream);
+
+/*
  * mpap_roadmap_import -- wrap a precomputed single-environment CSR (P:337:
  * neighbours and edge data "precomputed offline") so mpap_search can run on it.
  *   n, pos_dim      node count (>= 1) and position dimension (2 or 3).
@@ -210,6 +237,16 @@ mpap_status mpap_roadmap_work(const mpap_roadmap *rm, uint64_t *counters, int32_
  * offsets), dst_coll[nnz] = dst | coll << 31, w, s, c [nnz] (f32). */
 mpap_status mpap_roadmap_export(const mpap_roadmap *rm, int32_t env, int32_t *row_ptr,
                                 uint32_t *dst_coll, float *w, float *s, float *c);
+
+/* Copy env's per-edge peaks (S, C) to host [nnz] f32 each (NULL skips one):
+ * S_e = max over prefixes of the increment sum (>= 0), C_e = max over steps of
+ * the clamped fold from 0 (>= 0); zero for colliding edges.  INVALID_ARGUMENT
+ * if the roadmap carries no peaks (imported without mpap_roadmap_set_peaks). */
+mpap_status mpap_roadmap_export_peaks(const mpap_roadmap *rm, int32_t env, float *S, float *C);
+
+/* Attach peaks to a single-env imported roadmap: host S, C [nnz] f32, finite,
+ * >= 0.  Replaces any previous peaks.  Synchronises. */
+mpap_status mpap_roadmap_set_peaks(mpap_roadmap *rm, const float *S, const float *C);
 
 /* Releases the roadmap's device memory (NULL is a no-op).  Waits for the
  * device to be idle first (searches of this roadmap may be in flight). */

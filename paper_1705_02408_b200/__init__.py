@@ -38,12 +38,14 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARGUMENT", 2: "NO_GOAL_NODE", 3: "NO_FEASIB
                 5: "OUT_OF_MEMORY", 6: "CUDA"}
 MPAP_MEM_HOST = 0
 MPAP_MEM_DEVICE = 1
+MPAP_SEARCH_FORALL_T = 1
 
 EXPORTED_SYMBOLS = [
     "mpap_build_roadmap_batch", "mpap_build_roadmap", "mpap_search", "mpap_search_batch", "mpap_roadmap_import",
     "mpap_roadmap_info", "mpap_roadmap_envs", "mpap_roadmap_export", "mpap_roadmap_free", "mpap_status_str",
     "mpap_last_error", "mpap_launch_count", "mpap_prof_enable", "mpap_prof_reset", "mpap_prof_read",
-    "mpap_roadmap_work",
+    "mpap_roadmap_work", "mpap_search_ex", "mpap_search_batch_ex", "mpap_roadmap_export_peaks",
+    "mpap_roadmap_set_peaks",
 ]
 
 
@@ -99,6 +101,12 @@ _lib.mpap_search.argtypes = [_vp, C.c_int32, C.c_int32, C.POINTER(mpap_goal), C.
                              C.c_int32, C.POINTER(mpap_result), C.POINTER(mpap_wave), C.c_int32, _vp]
 _lib.mpap_search_batch.argtypes = [_vp, C.c_int32, _i32p, _i32p, C.POINTER(mpap_goal), C.POINTER(C.c_double),
                                    C.c_double, _vp, C.c_int32, _vp, C.c_int32, _vp]
+_lib.mpap_search_ex.argtypes = [_vp, C.c_int32, C.c_int32, C.POINTER(mpap_goal), C.c_double, C.c_double, C.c_uint32,
+                                _i32p, C.c_int32, C.POINTER(mpap_result), C.POINTER(mpap_wave), C.c_int32, _vp]
+_lib.mpap_search_batch_ex.argtypes = [_vp, C.c_int32, _i32p, _i32p, C.POINTER(mpap_goal), C.POINTER(C.c_double),
+                                      C.c_double, C.c_uint32, _vp, C.c_int32, _vp, C.c_int32, _vp]
+_lib.mpap_roadmap_export_peaks.argtypes = [_vp, C.c_int32, _vp, _vp]
+_lib.mpap_roadmap_set_peaks.argtypes = [_vp, _vp, _vp]
 _lib.mpap_roadmap_import.argtypes = [C.c_int32, C.c_int32, _vp, _i32p, _vp, _vp, _vp, _vp, C.c_double, _vp,
                                      C.POINTER(_vp)]
 _lib.mpap_roadmap_info.argtypes = [_vp, C.c_int32, _i32p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
@@ -119,6 +127,7 @@ _lib.mpap_prof_reset.restype = None
 _lib.mpap_prof_read.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
 _lib.mpap_prof_read.restype = C.c_int32
 for _f in ("mpap_build_roadmap_batch", "mpap_build_roadmap", "mpap_search", "mpap_search_batch",
+           "mpap_search_ex", "mpap_search_batch_ex", "mpap_roadmap_export_peaks", "mpap_roadmap_set_peaks",
            "mpap_roadmap_import", "mpap_roadmap_info", "mpap_roadmap_export"):
     getattr(_lib, _f).restype = C.c_int
 
@@ -281,18 +290,20 @@ def _goal(lo, hi) -> mpap_goal:
 
 
 def mpap_search(rm: Roadmap, env: int, start: int, goal_lo, goal_hi, perception_bound: float, lam: float,
-                path_capacity: int = 65536, trace_waves: int = 0, stream=None) -> Dict[str, Any]:
+                path_capacity: int = 65536, trace_waves: int = 0, stream=None, forall_t: bool = False
+                ) -> Dict[str, Any]:
     """Alg. 3 for one query; returns the plan, its cost and perception value
     (plus counters, and per-wave counters when ``trace_waves`` > 0).  A
-    NO_FEASIBLE_PLAN outcome is returned, not raised."""
+    NO_FEASIBLE_PLAN outcome is returned, not raised.  ``forall_t`` selects
+    MPAP_SEARCH_FORALL_T (Eq. 2 for every step along the edges)."""
     g = _goal(goal_lo, goal_hi)
     path = np.zeros(max(path_capacity, 1), dtype=np.int32)
     res = mpap_result()
     waves = (mpap_wave * trace_waves)() if trace_waves > 0 else None
     st = _stream(stream)
-    s = _lib.mpap_search(rm.handle, int(env), int(start), C.byref(g), float(perception_bound), float(lam),
-                         path.ctypes.data_as(_i32p), int(path_capacity), C.byref(res), waves, int(trace_waves),
-                         C.c_void_p(st) if st else None)
+    s = _lib.mpap_search_ex(rm.handle, int(env), int(start), C.byref(g), float(perception_bound), float(lam),
+                            MPAP_SEARCH_FORALL_T if forall_t else 0, path.ctypes.data_as(_i32p), int(path_capacity),
+                            C.byref(res), waves, int(trace_waves), C.c_void_p(st) if st else None)
     if s not in (MPAP_OK, MPAP_ERR_NO_FEASIBLE_PLAN):
         raise MpapError(s, "mpap_search")
     out = {
@@ -310,7 +321,7 @@ def mpap_search(rm: Roadmap, env: int, start: int, goal_lo, goal_hi, perception_
 
 
 def mpap_search_batch(rm: Roadmap, envs, starts, goals_lo, goals_hi, perception_bounds, lam: float,
-                      path_capacity: int, paths=None, results=None, stream=None):
+                      path_capacity: int, paths=None, results=None, stream=None, forall_t: bool = False):
     """Batch of independent queries (one CTA per query, dynamic scheduling).
     With ``paths``/``results`` CUDA tensors (int32 [Q, cap], uint8 [Q*48]) the
     call is asynchronous and writes on the device; otherwise host numpy outputs
@@ -332,9 +343,10 @@ def mpap_search_batch(rm: Roadmap, envs, starts, goals_lo, goals_hi, perception_
         host_paths = np.zeros((Q, path_capacity), dtype=np.int32)
         host_res = np.zeros(Q, dtype=RESULT_DTYPE)
         pp, rp = C.c_void_p(host_paths.ctypes.data), C.c_void_p(host_res.ctypes.data)
-    s = _lib.mpap_search_batch(rm.handle, Q, ea.ctypes.data_as(_i32p), sa.ctypes.data_as(_i32p), gs,
-                               ba.ctypes.data_as(C.POINTER(C.c_double)), float(lam), pp, int(path_capacity), rp,
-                               mem, C.c_void_p(st) if st else None)
+    s = _lib.mpap_search_batch_ex(rm.handle, Q, ea.ctypes.data_as(_i32p), sa.ctypes.data_as(_i32p), gs,
+                                  ba.ctypes.data_as(C.POINTER(C.c_double)), float(lam),
+                                  MPAP_SEARCH_FORALL_T if forall_t else 0, pp, int(path_capacity), rp, mem,
+                                  C.c_void_p(st) if st else None)
     if s != MPAP_OK:
         raise MpapError(s, "mpap_search_batch")
     return host_paths, host_res
@@ -364,6 +376,27 @@ def mpap_roadmap_export(rm: Roadmap, env: int = 0) -> Dict[str, np.ndarray]:
         raise MpapError(st, "mpap_roadmap_export")
     return {"n": n, "row_ptr": row_ptr, "dst": (dc[:nnz] & 0x7FFFFFFF).astype(np.int32),
             "coll": (dc[:nnz] >> 31).astype(np.uint8), "w": w[:nnz], "s": s[:nnz], "c": c[:nnz]}
+
+
+def mpap_roadmap_export_peaks(rm: Roadmap, env: int = 0):
+    """Per-edge prefix maxima (S, C) of env's edges (f32 arrays [nnz])."""
+    nnz = mpap_roadmap_info(rm, env)["nnz"]
+    S = np.zeros(max(nnz, 1), np.float32)
+    Cc = np.zeros(max(nnz, 1), np.float32)
+    st = _lib.mpap_roadmap_export_peaks(rm.handle, int(env), S.ctypes.data, Cc.ctypes.data)
+    if st != MPAP_OK:
+        raise MpapError(st, "mpap_roadmap_export_peaks")
+    return S[:nnz], Cc[:nnz]
+
+
+def mpap_roadmap_set_peaks(rm: Roadmap, S, Cp) -> None:
+    Sa = np.ascontiguousarray(S, dtype=np.float32)
+    Ca = np.ascontiguousarray(Cp, dtype=np.float32)
+    if Sa.size == 0:
+        Sa, Ca = np.zeros(1, np.float32), np.zeros(1, np.float32)
+    st = _lib.mpap_roadmap_set_peaks(rm.handle, Sa.ctypes.data, Ca.ctypes.data)
+    if st != MPAP_OK:
+        raise MpapError(st, "mpap_roadmap_set_peaks")
 
 
 def mpap_launch_count() -> int:

@@ -706,7 +706,8 @@ __device__ __forceinline__ void chunk_bbox(const double* su, const double* sv, c
 template <int D, int DYN, int HEUR>
 __device__ void edge_heuristic(const DevParams& P, const double* su, const double* sv, double T,
                                const double* __restrict__ feat, int F, const double* __restrict__ box, int O,
-                               WarpLists<D>& L, double* fold, int lane, double& s_out, double& c_out, Work& W) {
+                               WarpLists<D>& L, double* fold, int lane, double& s_out, double& c_out,
+                               double& S_out, double& C_out, Work& W) {
   const double kk = ceil(T / P.dt);
   const int K = (kk < 1.0) ? 1 : (int)kk;
   const double Dl = T / (double)K;
@@ -763,7 +764,7 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
       }
     }
   }
-  double s = 0.0, c = 0.0;
+  double s = 0.0, c = 0.0, Sp = 0.0, Cp = 0.0;   // summary and its prefix maxima (NEXT-3)
   for (int k0 = 0; k0 < K; k0 += 32) {
     const int nk = min(32, K - k0);
     const double ta = (double)k0 * Dl, tb = (double)(k0 + nk - 1) * Dl;
@@ -928,11 +929,15 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
       const double tt = c + ij;
       c = (tt > 0.0) ? tt : 0.0;
       s = s + ij;
+      Sp = (s > Sp) ? s : Sp;
+      Cp = (c > Cp) ? c : Cp;
     }
     __syncwarp();
   }
   s_out = s;
   c_out = c;
+  S_out = Sp;
+  C_out = Cp;
 }
 
 // Persistent: each warp pulls rows (over all environments of the batch) from
@@ -955,6 +960,7 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
                                                           const NearRec* __restrict__ scratch,
                                                           const int64_t* __restrict__ row_ptr,
                                                           EdgeRec* __restrict__ edges,
+                                                          float2* __restrict__ peak,
                                                           unsigned long long* __restrict__ nnz_free,
                                                           unsigned long long* __restrict__ work,
                                                           unsigned long long* __restrict__ next_row) {
@@ -1023,6 +1029,7 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
           er.s = 0.0f;
           er.c = 0.0f;
           edges[e0 + j] = er;
+          peak[e0 + j] = make_float2(0.0f, 0.0f);
         }
       } else {
         const uint32_t dc = edges[e0 + j].dst_coll;
@@ -1031,10 +1038,14 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
         __syncwarp();
         if (lane < NS) sv[lane] = (lane < stride) ? envs[(int64_t)rec.v * stride + lane] : 0.0;
         __syncwarp();
-        double s64, c64;
-        edge_heuristic<D, DYN, HEUR>(P, su, sv, rec.tau, efeat, F, ebox, O, L, s_fold[warp], lane, s64, c64, W);
+        double s64, c64, S64, C64;
+        edge_heuristic<D, DYN, HEUR>(P, su, sv, rec.tau, efeat, F, ebox, O, L, s_fold[warp], lane, s64, c64, S64,
+                                     C64, W);
         W.flush(lane);
-        if (lane == 0) *reinterpret_cast<float2*>(&edges[e0 + j].s) = make_float2((float)s64, (float)c64);
+        if (lane == 0) {
+          *reinterpret_cast<float2*>(&edges[e0 + j].s) = make_float2((float)s64, (float)c64);
+          peak[e0 + j] = make_float2((float)S64, (float)C64);
+        }
       }
     }
     if (PHASE == 0) {
@@ -1083,7 +1094,7 @@ cudaError_t launch_edges_phase(size_t smem, cudaStream_t st, const mpap_roadmap*
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(per_sm, 1), need));
   kern<<<grid, kWarps * 32, smem, st>>>(rm->d_samples, rm->d_node_base, rm->B, rm->d_obst, rm->d_obst_base,
                                         rm->d_feat, rm->d_feat_base, rm->prm, cap, rm->o_max, rm->f_max, d_cnt,
-                                        d_scr, rm->d_row_ptr, rm->d_edges, d_free, d_work, d_next);
+                                        d_scr, rm->d_row_ptr, rm->d_edges, rm->d_peak, d_free, d_work, d_next);
   return cudaGetLastError();
 }
 
@@ -1173,6 +1184,10 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
   if (cudaMallocAsync(&rm->d_edges, sizeof(EdgeRec) * std::max<int64_t>(rm->nnz_total, 1), st) != cudaSuccess) {
     cudaGetLastError();
     return set_error(MPAP_ERR_OUT_OF_MEMORY, "edge array allocation failed");
+  }
+  if (cudaMallocAsync(&rm->d_peak, sizeof(float2) * std::max<int64_t>(rm->nnz_total, 1), st) != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(MPAP_ERR_OUT_OF_MEMORY, "peak array allocation failed");
   }
   const size_t smem = sizeof(double) * (size_t)kWarps * ((size_t)rm->f_max * (d + 1) + (size_t)rm->o_max * 2 * d);
   unsigned long long* d_next = nullptr;

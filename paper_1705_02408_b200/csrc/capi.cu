@@ -210,7 +210,7 @@ void mpap_roadmap_free(mpap_roadmap* rm) {
   // wait for the device, then hand the memory back to the stream-ordered pool
   cudaDeviceSynchronize();
   void* ptrs[] = {rm->d_samples, rm->d_obst, rm->d_feat, rm->d_obst_base, rm->d_feat_base, rm->d_node_base,
-                  rm->d_row_ptr, rm->d_edges};
+                  rm->d_row_ptr, rm->d_edges, rm->d_peak};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, 0);
   cudaSetDevice(cur);
@@ -434,6 +434,52 @@ mpap_status mpap_roadmap_export(const mpap_roadmap* rm, int32_t env, int32_t* ro
   return MPAP_OK;
 }
 
+mpap_status mpap_roadmap_export_peaks(const mpap_roadmap* rm, int32_t env, float* S, float* C) {
+  if (!rm || env < 0 || env >= rm->B) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad roadmap/env");
+  if (!rm->d_peak) return set_error(MPAP_ERR_INVALID_ARGUMENT, "roadmap carries no peaks");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != rm->device) return set_error(MPAP_ERR_INVALID_ARGUMENT, "roadmap bound to another device");
+  const int64_t e0 = rm->edge_base[env], nnz = rm->edge_base[env + 1] - e0;
+  if (nnz == 0) return MPAP_OK;
+  std::vector<float2> pk((size_t)nnz);
+  cudaError_t e = cudaMemcpy(pk.data(), rm->d_peak + e0, sizeof(float2) * nnz, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_error(e, "export peaks");
+  for (int64_t k = 0; k < nnz; ++k) {
+    if (S) S[k] = pk[k].x;
+    if (C) C[k] = pk[k].y;
+  }
+  return MPAP_OK;
+}
+
+mpap_status mpap_roadmap_set_peaks(mpap_roadmap* rm, const float* S, const float* C) {
+  if (!rm || rm->B != 1) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad roadmap (single env only)");
+  const int64_t nnz = rm->nnz_total;
+  if (nnz > 0 && (!S || !C)) return set_error(MPAP_ERR_INVALID_ARGUMENT, "NULL peak arrays");
+  std::vector<float2> pk((size_t)std::max<int64_t>(nnz, 1));
+  for (int64_t k = 0; k < nnz; ++k) {
+    if (!(S[k] >= 0.0f) || !(C[k] >= 0.0f) || !std::isfinite(S[k]) || !std::isfinite(C[k]))
+      return set_error(MPAP_ERR_INVALID_ARGUMENT, "peaks must be finite and >= 0");
+    pk[k] = make_float2(S[k], C[k]);
+  }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != rm->device) return set_error(MPAP_ERR_INVALID_ARGUMENT, "roadmap bound to another device");
+  float2* d = nullptr;
+  cudaDeviceSynchronize();   // searches of this roadmap may be in flight
+  cudaError_t e = cudaMallocAsync(&d, sizeof(float2) * pk.size(), 0);
+  if (e != cudaSuccess) return cuda_error(e, "peak allocation");
+  e = cudaMemcpyAsync(d, pk.data(), sizeof(float2) * pk.size(), cudaMemcpyHostToDevice, 0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(d, 0);
+    return cuda_error(e, "peak upload");
+  }
+  if (rm->d_peak) cudaFreeAsync(rm->d_peak, 0);
+  rm->d_peak = d;
+  return MPAP_OK;
+}
+
 static mpap_status check_query(const mpap_roadmap* rm, int32_t env, int32_t start, const mpap_goal* goal,
                                double beta) {
   if (env < 0 || env >= rm->B) return set_error(MPAP_ERR_INVALID_ARGUMENT, "env out of range");
@@ -443,7 +489,9 @@ static mpap_status check_query(const mpap_roadmap* rm, int32_t env, int32_t star
   return MPAP_OK;
 }
 
-static void to_desc(QueryDesc& q, int32_t env, int32_t start, const mpap_goal* g, double beta) {
+static void to_desc(QueryDesc& q, int32_t env, int32_t start, const mpap_goal* g, double beta, uint32_t flags) {
+  q.flags = flags;
+  q.pad = 0;
   q.env = env;
   q.start = start;
   q.beta = beta;
@@ -453,19 +501,36 @@ static void to_desc(QueryDesc& q, int32_t env, int32_t start, const mpap_goal* g
   }
 }
 
+static mpap_status check_flags(const mpap_roadmap* rm, uint32_t flags) {
+  if (flags & ~MPAP_SEARCH_FORALL_T) return set_error(MPAP_ERR_INVALID_ARGUMENT, "unknown search flag");
+  if ((flags & MPAP_SEARCH_FORALL_T) && !rm->d_peak)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "MPAP_SEARCH_FORALL_T needs edge peaks (mpap_roadmap_set_peaks)");
+  return MPAP_OK;
+}
+
 mpap_status mpap_search(const mpap_roadmap* rm, int32_t env, int32_t start, const mpap_goal* goal,
                         double perception_bound, double lambda, int32_t* path, int32_t path_capacity,
                         mpap_result* result, mpap_wave* waves, int32_t waves_capacity, void* cuda_stream) {
+  return mpap_search_ex(rm, env, start, goal, perception_bound, lambda, 0u, path, path_capacity, result, waves,
+                        waves_capacity, cuda_stream);
+}
+
+mpap_status mpap_search_ex(const mpap_roadmap* rm, int32_t env, int32_t start, const mpap_goal* goal,
+                           double perception_bound, double lambda, uint32_t flags, int32_t* path,
+                           int32_t path_capacity, mpap_result* result, mpap_wave* waves, int32_t waves_capacity,
+                           void* cuda_stream) {
   if (!rm || !result || (!path && path_capacity > 0) || path_capacity < 0)
     return set_error(MPAP_ERR_INVALID_ARGUMENT, "NULL roadmap/result/path");
   if (!(lambda > 0.0) || lambda > 1.0) return set_error(MPAP_ERR_INVALID_ARGUMENT, "lambda must be in (0, 1]");
   mpap_status s = check_query(rm, env, start, goal, perception_bound);
   if (s != MPAP_OK) return s;
+  s = check_flags(rm, flags);
+  if (s != MPAP_OK) return s;
   int cur = 0;
   cudaGetDevice(&cur);
   if (cur != rm->device) return set_error(MPAP_ERR_INVALID_ARGUMENT, "roadmap bound to another device");
   QueryDesc q;
-  to_desc(q, env, start, goal, perception_bound);
+  to_desc(q, env, start, goal, perception_bound, flags);
   std::vector<int32_t> pbuf((size_t)std::max(path_capacity, 1));
   mpap_result r{};
   s = search_batch_device(rm, 1, &q, lambda, pbuf.data(), std::max(path_capacity, 1), &r, waves, waves_capacity,
@@ -489,11 +554,21 @@ mpap_status mpap_search(const mpap_roadmap* rm, int32_t env, int32_t start, cons
 mpap_status mpap_search_batch(const mpap_roadmap* rm, int32_t n_queries, const int32_t* envs, const int32_t* starts,
                               const mpap_goal* goals, const double* perception_bounds, double lambda, int32_t* paths,
                               int32_t path_capacity, mpap_result* results, int32_t mem, void* cuda_stream) {
+  return mpap_search_batch_ex(rm, n_queries, envs, starts, goals, perception_bounds, lambda, 0u, paths,
+                              path_capacity, results, mem, cuda_stream);
+}
+
+mpap_status mpap_search_batch_ex(const mpap_roadmap* rm, int32_t n_queries, const int32_t* envs,
+                                 const int32_t* starts, const mpap_goal* goals, const double* perception_bounds,
+                                 double lambda, uint32_t flags, int32_t* paths, int32_t path_capacity,
+                                 mpap_result* results, int32_t mem, void* cuda_stream) {
   if (!rm || n_queries < 0 || (n_queries > 0 && (!envs || !starts || !goals || !perception_bounds || !paths ||
                                                   !results)) || path_capacity < 1)
     return set_error(MPAP_ERR_INVALID_ARGUMENT, "NULL argument or path_capacity < 1");
   if (mem != MPAP_MEM_HOST && mem != MPAP_MEM_DEVICE) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad mem space");
   if (!(lambda > 0.0) || lambda > 1.0) return set_error(MPAP_ERR_INVALID_ARGUMENT, "lambda must be in (0, 1]");
+  mpap_status sf = check_flags(rm, flags);
+  if (sf != MPAP_OK) return sf;
   int cur = 0;
   cudaGetDevice(&cur);
   if (cur != rm->device) return set_error(MPAP_ERR_INVALID_ARGUMENT, "roadmap bound to another device");
@@ -501,7 +576,7 @@ mpap_status mpap_search_batch(const mpap_roadmap* rm, int32_t n_queries, const i
   for (int k = 0; k < n_queries; ++k) {
     mpap_status s = check_query(rm, envs[k], starts[k], &goals[k], perception_bounds[k]);
     if (s != MPAP_OK) return s;
-    to_desc(qs[k], envs[k], starts[k], &goals[k], perception_bounds[k]);
+    to_desc(qs[k], envs[k], starts[k], &goals[k], perception_bounds[k], flags);
   }
   return search_batch_device(rm, n_queries, qs.data(), lambda, paths, path_capacity, results, nullptr, 0, mem,
                              static_cast<cudaStream_t>(cuda_stream));

@@ -65,6 +65,7 @@ struct mpap_roadmap {
   int64_t* d_node_base = nullptr;  // [B+1]
   int64_t* d_row_ptr = nullptr;    // [sum n + 1] global edge offsets
   mpap::EdgeRec* d_edges = nullptr;
+  float2* d_peak = nullptr;        // [nnz_total] (S, C) prefix maxima per edge (NEXT-3); may be null (import)
   int64_t nnz_total = 0;
   unsigned long long work[mpap::kWorkCounters] = {};  // build work counters (mpap_roadmap_work)
   cudaStream_t alloc_stream = nullptr;                 // stream the device arrays were allocated on
@@ -121,6 +122,7 @@ struct QueryDesc {
   int32_t env, start;
   double beta;
   double goal_lo[3], goal_hi[3];
+  uint32_t flags, pad;   // MPAP_SEARCH_* flags
 };
 mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryDesc* h_queries,
                                 double lambda, int32_t* paths, int32_t path_cap, mpap_result* results,

@@ -65,6 +65,7 @@ struct SearchArgs {
   const int32_t* n_env;
   const int64_t* row_ptr;
   const EdgeRec* edges;
+  const float2* peak;   // per-edge (S, C) prefix maxima (NEXT-3); null if the roadmap has none
   int stride, pos_dim;
   double T;           // lambda * r_n (f64)
   // queries
@@ -243,6 +244,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
   int32_t* stamp = A.stamp + (size_t)slot * C.n;
   uint8_t* goal = A.goal + (size_t)slot * C.n;
   const double beta = Q.beta;
+  const bool forall_t = (Q.flags & MPAP_SEARCH_FORALL_T) != 0u;   // Eq. 2 for every step (NEXT-3)
   const int d = A.pos_dim;
   mpap_result* R = A.results + q;
 
@@ -321,7 +323,13 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
               const float t = ph + __uint_as_float(raw.z);
               const float cc = __uint_as_float(raw.w);
               qh = (t > cc) ? t : cc;
-              if ((double)qh <= beta) {
+              bool ok = (double)qh <= beta;                      // A3.9 cutoff
+              if (forall_t && ok) {                              // every step of the edge
+                const float2 pk = __ldg(A.peak + e);
+                const float t2 = ph + pk.x;
+                ok = (double)((t2 > pk.y) ? t2 : pk.y) <= beta;
+              }
+              if (ok) {
                 ++my_bpass;
                 const int snx = sn[x];
                 const int m = snx & kStairCountMask;
@@ -825,6 +833,7 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     A.n_env = nullptr;
     A.row_ptr = rm->d_row_ptr;
     A.edges = rm->d_edges;
+    A.peak = rm->d_peak;
     A.stride = rm->prm.stride;
     A.pos_dim = rm->prm.pos_dim;
     A.T = lambda * rm->prm.r;

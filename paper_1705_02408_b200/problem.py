@@ -24,9 +24,9 @@ def build_problem(prob, stream=None) -> Roadmap:
 
 
 def search_problem(rm: Roadmap, prob, beta: float, env: int = 0, lam=None, trace_waves: int = 0,
-                   path_capacity: int = 65536, stream=None) -> Dict[str, Any]:
+                   path_capacity: int = 65536, stream=None, forall_t: bool = False) -> Dict[str, Any]:
     return mpap_search(rm, env, prob.start, prob.goal_lo, prob.goal_hi, beta, prob.lam if lam is None else lam,
-                       path_capacity=path_capacity, trace_waves=trace_waves, stream=stream)
+                       path_capacity=path_capacity, trace_waves=trace_waves, stream=stream, forall_t=forall_t)
 
 
 class Batch:
@@ -74,14 +74,15 @@ class Batch:
 # ---------------------------------------------------------------------------
 
 def beta_sweep(rm: Roadmap, prob, betas: Sequence[float], env: int = 0, path_capacity: int = 1024,
-               stream=None):
+               stream=None, forall_t: bool = False):
     """Explore (Alg. 3) for every beta in one batched launch on one roadmap;
     returns (paths [len(betas), cap], result records)."""
     nb = len(betas)
     envs = np.full(nb, env, dtype=np.int32)
     starts = np.full(nb, prob.start, dtype=np.int32)
     return mpap_search_batch(rm, envs, starts, [prob.goal_lo] * nb, [prob.goal_hi] * nb,
-                             np.asarray(betas, dtype=np.float64), prob.lam, path_capacity, stream=stream)
+                             np.asarray(betas, dtype=np.float64), prob.lam, path_capacity, stream=stream,
+                             forall_t=forall_t)
 
 
 def refine_beta_min(rm: Roadmap, prob, hi: float, rel_tol: float = 1e-3, per_round: int = 32, env: int = 0,
