@@ -72,6 +72,8 @@ class ClockSampler:
         self.path = None
 
     def start(self):
+        if self.idx < 0:       # disabled (diagnostic runs only)
+            return
         try:
             fd, self.path = tempfile.mkstemp(suffix=".csv")
             os.close(fd)
@@ -242,7 +244,7 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed region: device-resident inputs ----
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local) if os.environ.get("MPAP_BENCH_CLOCKS", "1") != "0" else ClockSampler(-1)
     mp.mpap_prof_reset()
     mp.mpap_prof_enable(True)
     launches0 = mp.mpap_launch_count()
@@ -252,10 +254,13 @@ def main():
     sampler.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     wall0 = time.perf_counter()
+    host_ms = []
     for k in range(args.steps):
         flush.zero_()                      # L2 flush (512 MiB > 126 MB L2), outside the step's events
         ev[k][0].record(stream)
+        h0 = time.perf_counter()
         step_device()
+        host_ms.append((time.perf_counter() - h0) * 1e3)
         ev[k][1].record(stream)
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
@@ -347,6 +352,7 @@ def main():
         "feasible_fraction": feasible_all / (world * Q), "all_status_ok": ok,
         "roofline": roof, "gpu_launches": int(launches), "clocks": clocks, "wall_s": wall,
         "step_ms": [round(x, 3) for x in step_ms],
+        "step_host_ms": [round(x, 3) for x in host_ms],
     }
     if e2e:
         line["e2e"] = e2e

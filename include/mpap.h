@@ -77,6 +77,10 @@ typedef struct {
                              W3[2x8] b3[2] (host memory); else may be NULL          */
   double mlp_gain;        /* gamma of R12                                           */
   double v_ref, w_ref;    /* > 0; MLP input scales (R12)                            */
+  int32_t edge_peaks;     /* 0 or 1: also compute the per-edge peaks (S, C) that
+                             MPAP_SEARCH_FORALL_T needs (NEXT-3; costs ~2.5% of the
+                             build: two more running maxima per heuristic step)    */
+  int32_t reserved;       /* must be 0                                              */
 } mpap_params;
 
 /* Opaque, device-resident, immutable after build: B >= 1 environments, each

@@ -63,7 +63,7 @@ class mpap_params(C.Structure):
         ("control_weight", C.c_double), ("nominal_speed", C.c_double), ("dt", C.c_double),
         ("collision_dt", C.c_double), ("n_f", C.c_double), ("fov_cos_half", C.c_double),
         ("max_range", C.c_double), ("mlp", C.POINTER(C.c_double)), ("mlp_gain", C.c_double),
-        ("v_ref", C.c_double), ("w_ref", C.c_double),
+        ("v_ref", C.c_double), ("w_ref", C.c_double), ("edge_peaks", C.c_int32), ("reserved", C.c_int32),
     ]
 
 
@@ -189,9 +189,11 @@ class Roadmap:
 
 
 def make_params(pos_dim: int, dynamics: int, has_heading: int, heuristic: int, ws_lo, ws_hi,
-                mlp: Optional[np.ndarray], **p) -> mpap_params:
-    """Pack an mpap_params struct (the MLP array must outlive the call that uses it)."""
+                mlp: Optional[np.ndarray], edge_peaks: bool = False, **p) -> mpap_params:
+    """Pack an mpap_params struct (the MLP array must outlive the call that uses it).
+    ``edge_peaks`` also computes the per-edge peaks MPAP_SEARCH_FORALL_T needs."""
     prm = mpap_params()
+    prm.edge_peaks = 1 if edge_peaks else 0
     prm.pos_dim, prm.dynamics, prm.has_heading, prm.heuristic = pos_dim, dynamics, has_heading, heuristic
     for k in range(3):
         prm.ws_lo[k] = float(ws_lo[k]) if k < len(ws_lo) else 0.0
@@ -204,11 +206,11 @@ def make_params(pos_dim: int, dynamics: int, has_heading: int, heuristic: int, w
     return prm
 
 
-def params_from_problem(prob) -> tuple:
+def params_from_problem(prob, edge_peaks: bool = False) -> tuple:
     """(mpap_params, keepalive) from a synth.Problem (marshalling only)."""
     mlp = np.ascontiguousarray(prob.mlp, dtype=np.float64)
     prm = make_params(prob.pos_dim, prob.dynamics, prob.has_heading, prob.heuristic, prob.ws_lo, prob.ws_hi,
-                      mlp, **prob.params)
+                      mlp, edge_peaks=edge_peaks, **prob.params)
     return prm, mlp
 
 

@@ -924,13 +924,22 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
     }
     fold[lane] = inc;
     __syncwarp();
-    for (int j = 0; j < nk; ++j) {   // fold in time order (every lane, same values)
-      const double ij = fold[j];
-      const double tt = c + ij;
-      c = (tt > 0.0) ? tt : 0.0;
-      s = s + ij;
-      Sp = (s > Sp) ? s : Sp;
-      Cp = (c > Cp) ? c : Cp;
+    if (P.edge_peaks) {
+      for (int j = 0; j < nk; ++j) {   // fold in time order (every lane, same values)
+        const double ij = fold[j];
+        const double tt = c + ij;
+        c = (tt > 0.0) ? tt : 0.0;
+        s = s + ij;
+        Sp = (s > Sp) ? s : Sp;        // running maxima of the prefix values (NEXT-3)
+        Cp = (c > Cp) ? c : Cp;
+      }
+    } else {
+      for (int j = 0; j < nk; ++j) {
+        const double ij = fold[j];
+        const double tt = c + ij;
+        c = (tt > 0.0) ? tt : 0.0;
+        s = s + ij;
+      }
     }
     __syncwarp();
   }
@@ -1029,7 +1038,7 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
           er.s = 0.0f;
           er.c = 0.0f;
           edges[e0 + j] = er;
-          peak[e0 + j] = make_float2(0.0f, 0.0f);
+          if (peak) peak[e0 + j] = make_float2(0.0f, 0.0f);
         }
       } else {
         const uint32_t dc = edges[e0 + j].dst_coll;
@@ -1044,7 +1053,7 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
         W.flush(lane);
         if (lane == 0) {
           *reinterpret_cast<float2*>(&edges[e0 + j].s) = make_float2((float)s64, (float)c64);
-          peak[e0 + j] = make_float2((float)S64, (float)C64);
+          if (peak) peak[e0 + j] = make_float2((float)S64, (float)C64);
         }
       }
     }
@@ -1135,7 +1144,8 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
   CK(cudaMemsetAsync(d_free, 0, sizeof(unsigned long long) * B, st));
   CK(cudaMallocAsync(&d_work, sizeof(unsigned long long) * W_NUM, st));
   CK(cudaMemsetAsync(d_work, 0, sizeof(unsigned long long) * W_NUM, st));
-  CK(cudaMallocAsync(&rm->d_row_ptr, sizeof(int64_t) * (N + 1), st));
+  rm->d_row_ptr = static_cast<int64_t*>(rm_alloc(sizeof(int64_t) * (N + 1), st));
+  if (!rm->d_row_ptr) return MPAP_ERR_OUT_OF_MEMORY;
   const dim3 grid((rm->n_max + kWarps - 1) / kWarps, B);
   for (int attempt = 0; attempt < 8; ++attempt) {
     const size_t bytes = sizeof(NearRec) * (size_t)N * (size_t)cap;
@@ -1181,13 +1191,11 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
   rm->edge_base = bounds;
   rm->nnz_total = bounds[B];
   HostTimer te("edges alloc");
-  if (cudaMallocAsync(&rm->d_edges, sizeof(EdgeRec) * std::max<int64_t>(rm->nnz_total, 1), st) != cudaSuccess) {
-    cudaGetLastError();
-    return set_error(MPAP_ERR_OUT_OF_MEMORY, "edge array allocation failed");
-  }
-  if (cudaMallocAsync(&rm->d_peak, sizeof(float2) * std::max<int64_t>(rm->nnz_total, 1), st) != cudaSuccess) {
-    cudaGetLastError();
-    return set_error(MPAP_ERR_OUT_OF_MEMORY, "peak array allocation failed");
+  rm->d_edges = static_cast<EdgeRec*>(rm_alloc(sizeof(EdgeRec) * std::max<int64_t>(rm->nnz_total, 1), st));
+  if (!rm->d_edges) return set_error(MPAP_ERR_OUT_OF_MEMORY, "edge array allocation failed");
+  if (rm->prm.edge_peaks) {
+    rm->d_peak = static_cast<float2*>(rm_alloc(sizeof(float2) * std::max<int64_t>(rm->nnz_total, 1), st));
+    if (!rm->d_peak) return set_error(MPAP_ERR_OUT_OF_MEMORY, "peak array allocation failed");
   }
   const size_t smem = sizeof(double) * (size_t)kWarps * ((size_t)rm->f_max * (d + 1) + (size_t)rm->o_max * 2 * d);
   unsigned long long* d_next = nullptr;

@@ -52,6 +52,98 @@ void* workspace(cudaStream_t st, int tag, size_t bytes) {
   return p;
 }
 
+namespace {
+struct BufCache {
+  std::mutex mu;
+  std::map<int, std::multimap<size_t, void*>> free_by_dev;   // size -> buffer
+  std::map<void*, std::pair<size_t, int>> owned;              // buffer -> (size, device)
+  std::map<int, size_t> cached_bytes, cap_bytes;
+};
+BufCache& bufcache() {
+  static BufCache* c = new BufCache();   // never destroyed: release may run at exit
+  return *c;
+}
+size_t round_size(size_t b) {
+  const size_t g = (b >= (size_t(2) << 20)) ? (size_t(2) << 20) : 256;
+  return ((std::max<size_t>(b, 1) + g - 1) / g) * g;
+}
+}  // namespace
+
+void* rm_alloc(size_t bytes, cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const size_t want = round_size(bytes);
+  BufCache& c = bufcache();
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto& fl = c.free_by_dev[dev];
+    auto it = fl.lower_bound(want);
+    if (it != fl.end() && it->first <= want + want / 8) {
+      void* p = it->second;
+      c.cached_bytes[dev] -= it->first;
+      fl.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, want, st) != cudaSuccess) {
+    cudaGetLastError();
+    // drop this device's cache and retry once
+    std::vector<void*> drop;
+    {
+      std::lock_guard<std::mutex> lk(c.mu);
+      for (auto& kv : c.free_by_dev[dev]) drop.push_back(kv.second);
+      c.free_by_dev[dev].clear();
+      c.cached_bytes[dev] = 0;
+      for (void* q : drop) c.owned.erase(q);
+    }
+    if (drop.empty()) {
+      set_error(MPAP_ERR_OUT_OF_MEMORY, "device allocation failed");
+      return nullptr;
+    }
+    cudaStreamSynchronize(st);
+    for (void* q : drop) cudaFreeAsync(q, st);
+    cudaStreamSynchronize(st);
+    if (cudaMallocAsync(&p, want, st) != cudaSuccess) {
+      cudaGetLastError();
+      set_error(MPAP_ERR_OUT_OF_MEMORY, "device allocation failed");
+      return nullptr;
+    }
+  }
+  std::lock_guard<std::mutex> lk(c.mu);
+  c.owned[p] = {want, dev};
+  return p;
+}
+
+void rm_release(void* p) {
+  if (!p) return;
+  BufCache& c = bufcache();
+  std::unique_lock<std::mutex> lk(c.mu);
+  auto it = c.owned.find(p);
+  if (it == c.owned.end()) {   // not ours (cannot happen for roadmap arrays)
+    lk.unlock();
+    cudaFreeAsync(p, 0);
+    return;
+  }
+  const size_t sz = it->second.first;
+  const int dev = it->second.second;
+  if (!c.cap_bytes.count(dev)) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    size_t cap = tot / 4;
+    if (const char* e = getenv("MPAP_CACHE_MB")) cap = (size_t)atoll(e) << 20;
+    c.cap_bytes[dev] = cap;
+  }
+  if (c.cached_bytes[dev] + sz > c.cap_bytes[dev]) {
+    c.owned.erase(it);
+    lk.unlock();
+    cudaFreeAsync(p, 0);
+    return;
+  }
+  c.free_by_dev[dev].emplace(sz, p);
+  c.cached_bytes[dev] += sz;
+}
+
 void retain_pool_memory(int device) {
   static std::mutex mu;
   static std::vector<int> done;
@@ -136,6 +228,12 @@ using namespace mpap;
 
 static bool is_fin(double x) { return std::isfinite(x); }
 
+template <typename T>
+static cudaError_t rm_alloc_into(T** out, size_t bytes, cudaStream_t st) {
+  *out = static_cast<T*>(rm_alloc(bytes, st));
+  return *out ? cudaSuccess : cudaErrorMemoryAllocation;
+}
+
 static mpap_status validate_params(const mpap_params* p, double r) {
   if (!p) return set_error(MPAP_ERR_INVALID_ARGUMENT, "params is NULL");
   if (p->pos_dim != 2 && p->pos_dim != 3) return set_error(MPAP_ERR_INVALID_ARGUMENT, "pos_dim must be 2 or 3");
@@ -155,6 +253,8 @@ static mpap_status validate_params(const mpap_params* p, double r) {
   if (!(p->fov_cos_half > 0.0) || p->fov_cos_half > 1.0)
     return set_error(MPAP_ERR_INVALID_ARGUMENT, "fov_cos_half must be in (0, 1]");
   if (!is_fin(p->mlp_gain)) return set_error(MPAP_ERR_INVALID_ARGUMENT, "mlp_gain not finite");
+  if ((p->edge_peaks != 0 && p->edge_peaks != 1) || p->reserved != 0)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "edge_peaks must be 0 or 1 and reserved 0");
   for (int k = 0; k < p->pos_dim; ++k)
     if (!(p->ws_lo[k] < p->ws_hi[k])) return set_error(MPAP_ERR_INVALID_ARGUMENT, "workspace lo >= hi");
   return MPAP_OK;
@@ -211,8 +311,7 @@ void mpap_roadmap_free(mpap_roadmap* rm) {
   cudaDeviceSynchronize();
   void* ptrs[] = {rm->d_samples, rm->d_obst, rm->d_feat, rm->d_obst_base, rm->d_feat_base, rm->d_node_base,
                   rm->d_row_ptr, rm->d_edges, rm->d_peak};
-  for (void* p : ptrs)
-    if (p) cudaFreeAsync(p, 0);
+  for (void* p : ptrs) rm_release(p);   // device is idle: safe to reuse from any stream
   cudaSetDevice(cur);
   delete rm;
 }
@@ -267,6 +366,7 @@ mpap_status mpap_build_roadmap_batch(int32_t n_envs, const double* samples, cons
   P.has_heading = params->has_heading;
   P.heuristic = params->heuristic;
   P.stride = row_stride;
+  P.edge_peaks = params->edge_peaks;
   P.hoff = d * (params->dynamics == MPAP_DOUBLE_INTEGRATOR ? 2 : 1);
   for (int k = 0; k < 3; ++k) {
     P.ws_lo[k] = params->ws_lo[k];
@@ -298,17 +398,17 @@ mpap_status mpap_build_roadmap_batch(int32_t n_envs, const double* samples, cons
     rm->f_max = std::max(rm->f_max, n_features[b]);
   }
   const cudaMemcpyKind kind = (mem == MPAP_MEM_HOST) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-  CKC(cudaMallocAsync(&rm->d_samples, sizeof(double) * N * row_stride, st));
+  CKC(rm_alloc_into(&rm->d_samples, sizeof(double) * N * row_stride, st));
   CKC(cudaMemcpyAsync(rm->d_samples, samples, sizeof(double) * N * row_stride, kind, st));
-  CKC(cudaMallocAsync(&rm->d_obst, sizeof(double) * std::max<int64_t>(O * 2 * d, 1), st));
+  CKC(rm_alloc_into(&rm->d_obst, sizeof(double) * std::max<int64_t>(O * 2 * d, 1), st));
   if (O) CKC(cudaMemcpyAsync(rm->d_obst, obstacles, sizeof(double) * O * 2 * d, kind, st));
-  CKC(cudaMallocAsync(&rm->d_feat, sizeof(double) * std::max<int64_t>(F * d, 1), st));
+  CKC(rm_alloc_into(&rm->d_feat, sizeof(double) * std::max<int64_t>(F * d, 1), st));
   if (F) CKC(cudaMemcpyAsync(rm->d_feat, features, sizeof(double) * F * d, kind, st));
-  CKC(cudaMallocAsync(&rm->d_obst_base, sizeof(int32_t) * (n_envs + 1), st));
+  CKC(rm_alloc_into(&rm->d_obst_base, sizeof(int32_t) * (n_envs + 1), st));
   CKC(cudaMemcpyAsync(rm->d_obst_base, ob.data(), sizeof(int32_t) * (n_envs + 1), cudaMemcpyHostToDevice, st));
-  CKC(cudaMallocAsync(&rm->d_feat_base, sizeof(int32_t) * (n_envs + 1), st));
+  CKC(rm_alloc_into(&rm->d_feat_base, sizeof(int32_t) * (n_envs + 1), st));
   CKC(cudaMemcpyAsync(rm->d_feat_base, fb.data(), sizeof(int32_t) * (n_envs + 1), cudaMemcpyHostToDevice, st));
-  CKC(cudaMallocAsync(&rm->d_node_base, sizeof(int64_t) * (n_envs + 1), st));
+  CKC(rm_alloc_into(&rm->d_node_base, sizeof(int64_t) * (n_envs + 1), st));
   CKC(cudaMemcpyAsync(rm->d_node_base, rm->node_base.data(), sizeof(int64_t) * (n_envs + 1),
                       cudaMemcpyHostToDevice, st));
   s = build_roadmap_device(rm, st);
@@ -377,13 +477,13 @@ mpap_status mpap_roadmap_import(int32_t n, int32_t pos_dim, const double* positi
   rm->nnz_total = nnz;
   std::vector<int64_t> rp64(n + 1);
   for (int32_t u = 0; u <= n; ++u) rp64[u] = row_ptr[u];
-  CKC(cudaMallocAsync(&rm->d_samples, sizeof(double) * n * pos_dim, st));
+  CKC(rm_alloc_into(&rm->d_samples, sizeof(double) * n * pos_dim, st));
   CKC(cudaMemcpyAsync(rm->d_samples, positions, sizeof(double) * n * pos_dim, cudaMemcpyHostToDevice, st));
-  CKC(cudaMallocAsync(&rm->d_node_base, sizeof(int64_t) * 2, st));
+  CKC(rm_alloc_into(&rm->d_node_base, sizeof(int64_t) * 2, st));
   CKC(cudaMemcpyAsync(rm->d_node_base, rm->node_base.data(), sizeof(int64_t) * 2, cudaMemcpyHostToDevice, st));
-  CKC(cudaMallocAsync(&rm->d_row_ptr, sizeof(int64_t) * (n + 1), st));
+  CKC(rm_alloc_into(&rm->d_row_ptr, sizeof(int64_t) * (n + 1), st));
   CKC(cudaMemcpyAsync(rm->d_row_ptr, rp64.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
-  CKC(cudaMallocAsync(&rm->d_edges, sizeof(EdgeRec) * er.size(), st));
+  CKC(rm_alloc_into(&rm->d_edges, sizeof(EdgeRec) * er.size(), st));
   CKC(cudaMemcpyAsync(rm->d_edges, er.data(), sizeof(EdgeRec) * er.size(), cudaMemcpyHostToDevice, st));
   CKC(cudaStreamSynchronize(st));
   *out = rm;
@@ -467,15 +567,15 @@ mpap_status mpap_roadmap_set_peaks(mpap_roadmap* rm, const float* S, const float
   if (cur != rm->device) return set_error(MPAP_ERR_INVALID_ARGUMENT, "roadmap bound to another device");
   float2* d = nullptr;
   cudaDeviceSynchronize();   // searches of this roadmap may be in flight
-  cudaError_t e = cudaMallocAsync(&d, sizeof(float2) * pk.size(), 0);
-  if (e != cudaSuccess) return cuda_error(e, "peak allocation");
-  e = cudaMemcpyAsync(d, pk.data(), sizeof(float2) * pk.size(), cudaMemcpyHostToDevice, 0);
+  d = static_cast<float2*>(rm_alloc(sizeof(float2) * pk.size(), 0));
+  if (!d) return MPAP_ERR_OUT_OF_MEMORY;
+  cudaError_t e = cudaMemcpyAsync(d, pk.data(), sizeof(float2) * pk.size(), cudaMemcpyHostToDevice, 0);
   if (e == cudaSuccess) e = cudaStreamSynchronize(0);
   if (e != cudaSuccess) {
-    cudaFreeAsync(d, 0);
+    rm_release(d);
     return cuda_error(e, "peak upload");
   }
-  if (rm->d_peak) cudaFreeAsync(rm->d_peak, 0);
+  rm_release(rm->d_peak);
   rm->d_peak = d;
   return MPAP_OK;
 }

@@ -23,6 +23,7 @@ constexpr int kWorkCounters = 16;
 struct DevParams {
   int pos_dim, dynamics, has_heading, heuristic;
   int stride;  // doubles per sample row
+  int edge_peaks;  // compute per-edge (S, C) peaks (NEXT-3)
   int hoff;    // offset of (cos yaw, sin yaw) in a row
   double ws_lo[3], ws_hi[3];
   double control_weight, nominal_speed, dt, collision_dt, n_f, fov_cos_half, max_range;
@@ -112,6 +113,16 @@ void retain_pool_memory(int device);
 // their own.  Returns nullptr on allocation failure.
 void* workspace(cudaStream_t st, int tag, size_t bytes);
 enum { WS_NEAR = 0, WS_SEARCH = 1 };
+// Device buffer cache for roadmap arrays (capi.cu).  Roadmaps are built and
+// freed every step of a batched pipeline with the same sizes; growing the
+// stream-ordered pool for them stalled the host for up to 0.5 s per call
+// (measured), so released buffers are kept per device and reused
+// best-fit (slack <= 1/8).  rm_alloc returns nullptr on failure (error set).
+// rm_release requires that no device work still uses the buffer (callers
+// synchronise first); beyond a cap (1/4 of device memory, MPAP_CACHE_MB) the
+// buffer is returned to the driver.
+void* rm_alloc(size_t bytes, cudaStream_t st);
+void rm_release(void* p);
 mpap_status cuda_error(cudaError_t e, const char* what);
 
 // roadmap build (build_kernels.cu)

@@ -13,8 +13,8 @@ from . import (MPAP_MEM_DEVICE, Roadmap, mpap_build_roadmap, mpap_build_roadmap_
                mpap_search_batch, params_from_problem)
 
 
-def build_problem(prob, stream=None) -> Roadmap:
-    prm, keep = params_from_problem(prob)
+def build_problem(prob, stream=None, edge_peaks: bool = False) -> Roadmap:
+    prm, keep = params_from_problem(prob, edge_peaks)
     obst = prob.obstacles if prob.obstacles.size else None
     feat = prob.features if prob.features.size else None
     rm = mpap_build_roadmap(prob.samples, obst if obst is not None else np.zeros((0, 2 * prob.pos_dim)),
@@ -32,7 +32,7 @@ def search_problem(rm: Roadmap, prob, beta: float, env: int = 0, lam=None, trace
 class Batch:
     """Concatenated host arrays of a list of problems sharing params and r."""
 
-    def __init__(self, probs: Sequence[Any]):
+    def __init__(self, probs: Sequence[Any], edge_peaks: bool = False):
         p0 = probs[0]
         self.probs = list(probs)
         self.stride = p0.stride
@@ -42,7 +42,7 @@ class Batch:
         self.samples = np.ascontiguousarray(np.concatenate([p.samples for p in probs]), np.float64)
         self.obstacles = np.ascontiguousarray(np.concatenate([p.obstacles.reshape(-1) for p in probs]), np.float64)
         self.features = np.ascontiguousarray(np.concatenate([p.features.reshape(-1) for p in probs]), np.float64)
-        self.prm, self._keep = params_from_problem(p0)
+        self.prm, self._keep = params_from_problem(p0, edge_peaks)
         self.r = p0.r
         self.lam = p0.lam
         self.starts = np.array([p.start for p in probs], np.int32)

@@ -109,3 +109,28 @@ def test_product_path_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_struct_layouts_match_header(mp, tmp_path):
+    """The ctypes mirrors of mpap_params / mpap_goal / mpap_result / mpap_wave
+    have the C header's sizes and field offsets (compiled here with gcc)."""
+    structs = {"mpap_params": mp.mpap_params, "mpap_goal": mp.mpap_goal, "mpap_result": mp.mpap_result,
+               "mpap_wave": mp.mpap_wave}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "mpap.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'  printf("{name} size %zu\\n", sizeof({name}));')
+        for f in cls._fields_:
+            lines.append(f'  printf("{name} {f[0]} %zu\\n", offsetof({name}, {f[0]}));')
+    lines.append("  return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+    for ln in out:
+        if not ln:
+            continue
+        name, field, val = ln.split()
+        cls = structs[name]
+        want = C.sizeof(cls) if field == "size" else getattr(cls, field).offset
+        assert int(val) == want, (name, field, val, want)

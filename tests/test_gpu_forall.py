@@ -14,7 +14,7 @@ INF = float("inf")
 @pytest.mark.parametrize("name,n", [("c1", None), ("c2", None), ("c3", 400), ("c3", 2)])
 def test_peaks_bit_exact(mp, orc, name, n):
     prob = small(name, n)
-    rm = mp.pb.build_problem(prob)
+    rm = mp.pb.build_problem(prob, edge_peaks=True)
     orm = orc.build_roadmap(prob)
     S, Cp = mp.mpap_roadmap_export_peaks(rm)
     oS, oC = orc.build_peaks(prob, orm)
@@ -29,7 +29,7 @@ def test_peaks_bit_exact(mp, orc, name, n):
 @pytest.mark.parametrize("name", ["c1", "c2"])
 def test_forall_search_parity(mp, orc, name):
     prob = make_problem(load_config(name))
-    rm = mp.pb.build_problem(prob)
+    rm = mp.pb.build_problem(prob, edge_peaks=True)
     orm = orc.build_roadmap(prob)
     for beta in prob.betas:
         g = mp.pb.search_problem(rm, prob, beta, trace_waves=4096, forall_t=True)
@@ -39,7 +39,7 @@ def test_forall_search_parity(mp, orc, name):
 
 def test_forall_search_parity_c3_reduced(mp, orc):
     prob = small("c3", 700)
-    rm = mp.pb.build_problem(prob)
+    rm = mp.pb.build_problem(prob, edge_peaks=True)
     orm = orc.build_roadmap(prob)
     for beta in [INF, 6.0, 3.0, 2.0]:
         g = mp.pb.search_problem(rm, prob, beta, trace_waves=4096, forall_t=True)
@@ -48,7 +48,7 @@ def test_forall_search_parity_c3_reduced(mp, orc):
 
 def test_forall_batch_equals_single(mp, orc):
     prob = small("c3", 700)
-    rm = mp.pb.build_problem(prob)
+    rm = mp.pb.build_problem(prob, edge_peaks=True)
     betas = [INF, 6.0, 3.0, 2.0, 1.0]
     paths, res = mp.pb.beta_sweep(rm, prob, betas, forall_t=True)
     for k, beta in enumerate(betas):
@@ -112,3 +112,17 @@ def test_forall_random_imported_graphs(mp, orc, seed):
             o = orc.search_csr(n, g["row_ptr"], g["dst"], g["coll"], g["w"], g["s"], g["c"], goal, 0, beta, lam, 1.0,
                                S=g["S"], Cp=g["C"], forall_t=True)
             assert_search_equal(gr, o)
+
+
+def test_forall_needs_peaks(mp):
+    """A roadmap built without edge_peaks carries no peaks: the all-t search
+    and the peak export are INVALID_ARGUMENT, the node-only search runs."""
+    prob = small("c2", 60)
+    rm = mp.pb.build_problem(prob)
+    for call in (lambda: mp.pb.search_problem(rm, prob, INF, forall_t=True),
+                 lambda: mp.mpap_roadmap_export_peaks(rm),
+                 lambda: mp.pb.beta_sweep(rm, prob, [INF], forall_t=True)):
+        with pytest.raises(mp.MpapError) as ei:
+            call()
+        assert ei.value.status == mp.MPAP_ERR_INVALID_ARGUMENT
+    assert mp.pb.search_problem(rm, prob, INF)["status"] in (0, 3)
