@@ -242,6 +242,25 @@ mpap_status mpap_roadmap_work(const mpap_roadmap *rm, uint64_t *counters, int32_
 mpap_status mpap_roadmap_export(const mpap_roadmap *rm, int32_t env, int32_t *row_ptr,
                                 uint32_t *dst_coll, float *w, float *s, float *c);
 
+/*
+ * mpap_roadmap_update -- online replanning:
+ * replace environment `env`'s obstacle and feature sets and re-evaluate only
+ * the edges whose collision bit or heuristic summary (and peaks) can change:
+ * those whose trajectory bounding box, grown by max_range + 1e-3, overlaps a
+ * changed box or feature (the multiset symmetric differences of the old and
+ * new sets; exact value comparison).  Afterwards `rm` equals
+ * mpap_build_roadmap* of the new environment bit for bit (the neighbour
+ * structure and costs depend on the samples only).
+ *   obstacles [n_obstacles][2d], features [n_features][d]: in `mem` space
+ *                   (validated as in the build).
+ *   n_reevaluated   out (may be NULL): number of edges re-evaluated.
+ * Synchronises the device.  Errors: INVALID_ARGUMENT (bad env, arrays, an
+ * imported roadmap), OUT_OF_MEMORY, CUDA.
+ */
+mpap_status mpap_roadmap_update(mpap_roadmap *rm, int32_t env, const double *obstacles, int32_t n_obstacles,
+                                const double *features, int32_t n_features, int32_t mem, void *cuda_stream,
+                                int64_t *n_reevaluated);
+
 /* Copy env's per-edge peaks (S, C) to host [nnz] f32 each (NULL skips one):
  * S_e = max over prefixes of the increment sum (>= 0), C_e = max over steps of
  * the clamped fold from 0 (>= 0); zero for colliding edges.  INVALID_ARGUMENT

@@ -45,7 +45,7 @@ EXPORTED_SYMBOLS = [
     "mpap_roadmap_info", "mpap_roadmap_envs", "mpap_roadmap_export", "mpap_roadmap_free", "mpap_status_str",
     "mpap_last_error", "mpap_launch_count", "mpap_prof_enable", "mpap_prof_reset", "mpap_prof_read",
     "mpap_roadmap_work", "mpap_search_ex", "mpap_search_batch_ex", "mpap_roadmap_export_peaks",
-    "mpap_roadmap_set_peaks",
+    "mpap_roadmap_set_peaks", "mpap_roadmap_update",
 ]
 
 
@@ -107,6 +107,8 @@ _lib.mpap_search_batch_ex.argtypes = [_vp, C.c_int32, _i32p, _i32p, C.POINTER(mp
                                       C.c_double, C.c_uint32, _vp, C.c_int32, _vp, C.c_int32, _vp]
 _lib.mpap_roadmap_export_peaks.argtypes = [_vp, C.c_int32, _vp, _vp]
 _lib.mpap_roadmap_set_peaks.argtypes = [_vp, _vp, _vp]
+_lib.mpap_roadmap_update.argtypes = [_vp, C.c_int32, _vp, C.c_int32, _vp, C.c_int32, C.c_int32, _vp,
+                                     C.POINTER(C.c_int64)]
 _lib.mpap_roadmap_import.argtypes = [C.c_int32, C.c_int32, _vp, _i32p, _vp, _vp, _vp, _vp, C.c_double, _vp,
                                      C.POINTER(_vp)]
 _lib.mpap_roadmap_info.argtypes = [_vp, C.c_int32, _i32p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
@@ -128,7 +130,7 @@ _lib.mpap_prof_read.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c
 _lib.mpap_prof_read.restype = C.c_int32
 for _f in ("mpap_build_roadmap_batch", "mpap_build_roadmap", "mpap_search", "mpap_search_batch",
            "mpap_search_ex", "mpap_search_batch_ex", "mpap_roadmap_export_peaks", "mpap_roadmap_set_peaks",
-           "mpap_roadmap_import", "mpap_roadmap_info", "mpap_roadmap_export"):
+           "mpap_roadmap_update", "mpap_roadmap_import", "mpap_roadmap_info", "mpap_roadmap_export"):
     getattr(_lib, _f).restype = C.c_int
 
 
@@ -399,6 +401,23 @@ def mpap_roadmap_set_peaks(rm: Roadmap, S, Cp) -> None:
     st = _lib.mpap_roadmap_set_peaks(rm.handle, Sa.ctypes.data, Ca.ctypes.data)
     if st != MPAP_OK:
         raise MpapError(st, "mpap_roadmap_set_peaks")
+
+
+def mpap_roadmap_update(rm: Roadmap, env: int, obstacles, features, stream=None) -> int:
+    """NEXT-1: replace env's obstacles [O, 2d] and features [F, d] (numpy or
+    CUDA tensors) and re-evaluate only the affected edges; returns how many."""
+    dev = _is_cuda_tensor(obstacles) or _is_cuda_tensor(features)
+    mem = MPAP_MEM_DEVICE if dev else MPAP_MEM_HOST
+    op, k1 = _ptr(obstacles, np.float64)
+    fp, k2 = _ptr(features, np.float64)
+    n = C.c_int64()
+    st = _stream(stream)
+    s = _lib.mpap_roadmap_update(rm.handle, int(env), op, int(obstacles.shape[0]), fp, int(features.shape[0]), mem,
+                                 C.c_void_p(st) if st else None, C.byref(n))
+    del k1, k2
+    if s != MPAP_OK:
+        raise MpapError(s, "mpap_roadmap_update")
+    return int(n.value)
 
 
 def mpap_launch_count() -> int:

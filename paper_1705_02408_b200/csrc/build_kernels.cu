@@ -949,11 +949,15 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
   C_out = Cp;
 }
 
-// Persistent: each warp pulls rows (over all environments of the batch) from
-// an atomic counter, so no block waits on its slowest row.  PHASE 0 computes
-// the collision bit of every r-disc entry and writes the edge records; PHASE 1
-// fills the heuristic summary (s, c) of the collision-free ones.  Two kernels
-// keep each one's code and register footprint small.
+// Persistent: each warp pulls work items from an atomic counter, so no block
+// waits on its slowest item.  Build mode (items == nullptr): item = one row
+// (over all environments of the batch), its r-disc entries from the
+// neighbour scratch.  Update mode (NEXT-1, mpap_roadmap_update): item = one
+// edge {row, global edge index} of the affected list; its dst, w and tau come
+// from the roadmap itself.  PHASE 0 computes the collision bit and writes the
+// edge record; PHASE 1 fills the heuristic summary (s, c) (and peaks) of the
+// collision-free ones.  Two kernels keep each one's code and register
+// footprint small.
 template <int PHASE>
 struct EdgeBounds { static constexpr int kMin = (PHASE == 0) ? 2 : MPAP_EDGES_MIN_BLOCKS; };
 
@@ -965,14 +969,15 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
                                                           const double* __restrict__ feat,
                                                           const int32_t* __restrict__ feat_base, DevParams P,
                                                           int cap, int o_max, int f_max,
-                                                          const int32_t* __restrict__ cnt,
                                                           const NearRec* __restrict__ scratch,
                                                           const int64_t* __restrict__ row_ptr,
                                                           EdgeRec* __restrict__ edges,
+                                                          double* __restrict__ tau_arr,
                                                           float2* __restrict__ peak,
+                                                          const longlong2* __restrict__ items, int64_t n_items,
                                                           unsigned long long* __restrict__ nnz_free,
                                                           unsigned long long* __restrict__ work,
-                                                          unsigned long long* __restrict__ next_row) {
+                                                          unsigned long long* __restrict__ next_item) {
   constexpr int NS = 2 * D + 2;   // p, v (double integrator), heading
   extern __shared__ double smem[];
   __shared__ double s_state[kWarps][2][NS];
@@ -991,7 +996,7 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
     L.fmask = reinterpret_cast<unsigned long long*>(L.box + (size_t)o_max * 2 * D);
     L.mlp = s_mlp;
   }
-  const int64_t N = node_base[B];
+  const int64_t NI = items ? n_items : node_base[B];
   const int stride = P.stride;
   Work W;
   W.sm = s_work[warp];
@@ -1002,9 +1007,20 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
   __syncwarp();
   for (;;) {
     unsigned long long rr = 0;
-    if (lane == 0) rr = atomicAdd(next_row, 1ull);
-    const int64_t row = (int64_t)__shfl_sync(FULL, rr, 0);
-    if (row >= N) break;
+    if (lane == 0) rr = atomicAdd(next_item, 1ull);
+    const int64_t idx = (int64_t)__shfl_sync(FULL, rr, 0);
+    if (idx >= NI) break;
+    int64_t row, e_begin, e_end;
+    if (items) {
+      const longlong2 it = items[idx];
+      row = it.x;
+      e_begin = it.y;
+      e_end = it.y + 1;
+    } else {
+      row = idx;
+      e_begin = row_ptr[row];
+      e_end = row_ptr[row + 1];
+    }
     int lo_b = 0, hi_b = B;   // env = last b with node_base[b] <= row
     while (hi_b - lo_b > 1) {
       const int mid = (lo_b + hi_b) >> 1;
@@ -1019,52 +1035,166 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
     const double* envs = samples + node_base[b] * stride;
     __syncwarp();
     if (lane < NS) su[lane] = (lane < stride) ? envs[u * stride + lane] : 0.0;
-    const int deg = min(cnt[row], cap);
-    const int64_t e0 = row_ptr[row];
     int nfree = 0;
-    for (int j = 0; j < deg; ++j) {
+    for (int64_t e = e_begin; e < e_end; ++e) {
       if constexpr (PHASE == 0) {
-        const NearRec rec = scratch[row * (int64_t)cap + j];
+        int v;
+        float w;
+        double tau;
+        int old_coll = 0;
+        if (items) {
+          const EdgeRec old = edges[e];
+          v = (int)(old.dst_coll & 0x7fffffffu);
+          old_coll = (int)(old.dst_coll >> 31);
+          w = old.w;
+          tau = tau_arr[e];
+        } else {
+          const NearRec rec = scratch[row * (int64_t)cap + (e - e_begin)];
+          v = rec.v;
+          w = rec.w;
+          tau = rec.tau;
+        }
         __syncwarp();
-        if (lane < NS) sv[lane] = (lane < stride) ? envs[(int64_t)rec.v * stride + lane] : 0.0;
+        if (lane < NS) sv[lane] = (lane < stride) ? envs[(int64_t)v * stride + lane] : 0.0;
         __syncwarp();
-        const bool coll = edge_collision<D, DYN>(P, su, sv, rec.tau, ebox, O, L, lane, W);
-        nfree += coll ? 0 : 1;
+        const bool coll = edge_collision<D, DYN>(P, su, sv, tau, ebox, O, L, lane, W);
+        nfree += items ? (old_coll - (coll ? 1 : 0)) : (coll ? 0 : 1);
         W.flush(lane);
         if (lane == 0) {
           EdgeRec er;
-          er.dst_coll = (uint32_t)rec.v | (coll ? 0x80000000u : 0u);
-          er.w = rec.w;
+          er.dst_coll = (uint32_t)v | (coll ? 0x80000000u : 0u);
+          er.w = w;
           er.s = 0.0f;
           er.c = 0.0f;
-          edges[e0 + j] = er;
-          if (peak) peak[e0 + j] = make_float2(0.0f, 0.0f);
+          edges[e] = er;
+          if (!items) tau_arr[e] = tau;
+          if (peak) peak[e] = make_float2(0.0f, 0.0f);
         }
       } else {
-        const uint32_t dc = edges[e0 + j].dst_coll;
+        const uint32_t dc = edges[e].dst_coll;
         if (dc >> 31) continue;   // colliding edges keep s = c = 0 (never relaxed)
-        const NearRec rec = scratch[row * (int64_t)cap + j];
+        const double tau = tau_arr[e];
         __syncwarp();
-        if (lane < NS) sv[lane] = (lane < stride) ? envs[(int64_t)rec.v * stride + lane] : 0.0;
+        if (lane < NS) sv[lane] = (lane < stride) ? envs[(int64_t)(dc & 0x7fffffffu) * stride + lane] : 0.0;
         __syncwarp();
         double s64, c64, S64, C64;
-        edge_heuristic<D, DYN, HEUR>(P, su, sv, rec.tau, efeat, F, ebox, O, L, s_fold[warp], lane, s64, c64, S64,
+        edge_heuristic<D, DYN, HEUR>(P, su, sv, tau, efeat, F, ebox, O, L, s_fold[warp], lane, s64, c64, S64,
                                      C64, W);
         W.flush(lane);
         if (lane == 0) {
-          *reinterpret_cast<float2*>(&edges[e0 + j].s) = make_float2((float)s64, (float)c64);
-          if (peak) peak[e0 + j] = make_float2((float)S64, (float)C64);
+          *reinterpret_cast<float2*>(&edges[e].s) = make_float2((float)s64, (float)c64);
+          if (peak) peak[e] = make_float2((float)S64, (float)C64);
         }
       }
     }
     if (PHASE == 0) {
-      W.add(lane, W_EDGES, deg);
-      W.add(lane, W_FREE_EDGES, nfree);
-      if (lane == 0 && nfree) atomicAdd(&nnz_free[b], (unsigned long long)nfree);
+      W.add(lane, W_EDGES, (unsigned)(e_end - e_begin));
+      if (!items) W.add(lane, W_FREE_EDGES, nfree);
+      if (lane == 0 && nfree) atomicAdd(&nnz_free[b], (unsigned long long)(long long)nfree);
     }
   }
   __syncwarp();
   if (lane >= W_EDGES && lane < W_NUM && W.sm[lane]) atomicAdd(&work[lane], (unsigned long long)W.sm[lane]);
+}
+
+// NEXT-1: edges of one environment whose collision bit or
+// heuristic summary can change when the boxes `cbox` [nb][2D] and features
+// `cfeat` [nf][D] (the symmetric differences of the old and new sets) change.
+// Warp per row, lane per edge.  With E = the edge trajectory's bounding box
+// over [0, tau] (every step point and collision-polyline vertex lies in it,
+// up to rounding far below the margins):
+//  * a changed feature matters only if it is within R + 1e-3 of E per axis
+//    (else it is out of range of every step point);
+//  * a changed box matters only if it overlaps, grown by 1e-3, the bounding
+//    box V of E and of every feature (current or changed) within R + 1e-3 of
+//    E: every polyline segment lies in E and every sight line from a step
+//    point to an in-range feature lies in V.
+// So an unlisted edge's collision bit and heuristic summary are provably
+// unchanged.
+template <int D, int DYN>
+__global__ void __launch_bounds__(kWarps * 32) k_affected(const double* __restrict__ env_samples, int stride,
+                                                            int64_t row0, int64_t n_rows,
+                                                            const int64_t* __restrict__ row_ptr,
+                                                            const EdgeRec* __restrict__ edges,
+                                                            const double* __restrict__ tau_arr, double R,
+                                                            const double* __restrict__ efeat, int F,
+                                                            const double* __restrict__ cbox, int nb,
+                                                            const double* __restrict__ cfeat, int nf,
+                                                            longlong2* __restrict__ items,
+                                                            unsigned long long* __restrict__ n_items) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (r >= n_rows) return;
+  const int64_t row = row0 + r;   // global row (row_ptr); r and dst are env-local node ids
+  const unsigned lt = lanemask_lt();
+  const double m = R + 1e-3;
+  double su[2 * D];
+#pragma unroll
+  for (int j = 0; j < 2 * D; ++j) su[j] = (DYN == 1 || j < D) ? env_samples[r * stride + j] : 0.0;
+  const int64_t e0 = row_ptr[row], e1 = row_ptr[row + 1];
+  for (int64_t eb = e0; eb < e1; eb += 32) {
+    const int64_t e = eb + lane;
+    bool hit = false;
+    if (e < e1) {
+      const int v = (int)(edges[e].dst_coll & 0x7fffffffu);
+      const double tau = tau_arr[e];
+      double sv[2 * D];
+      const double* vrow = env_samples + (int64_t)v * stride;
+#pragma unroll
+      for (int j = 0; j < 2 * D; ++j) sv[j] = (DYN == 1 || j < D) ? vrow[j] : 0.0;
+      double c2[D], c3[D], r0[D], r1[D], lo[D], hi[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) { c2[j] = 0.0; c3[j] = 0.0; r0[j] = -1.0; r1[j] = -1.0; }
+      if (DYN == 1) {
+        di_traj<D>(su, sv, tau, c2, c3);
+        cubic_stationary<D>(su, c2, c3, r0, r1);
+      }
+      chunk_bbox<D, DYN>(su, sv, c2, c3, r0, r1, tau, 0.0, tau, lo, hi);
+      for (int i = 0; i < nf && !hit; ++i) {
+        bool sep = false;
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+          if (cfeat[i * D + k] > hi[k] + m || cfeat[i * D + k] < lo[k] - m) sep = true;
+        hit = !sep;
+      }
+      if (!hit && nb > 0) {
+        double vlo[D], vhi[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) { vlo[k] = lo[k]; vhi[k] = hi[k]; }
+        for (int pass = 0; pass < 2; ++pass) {
+          const double* fl = pass ? cfeat : efeat;
+          const int nfl = pass ? nf : F;
+          for (int i = 0; i < nfl; ++i) {
+            double fc[D];
+            bool near = true;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+              fc[k] = fl[(size_t)i * D + k];
+              if (fc[k] > hi[k] + m || fc[k] < lo[k] - m) near = false;
+            }
+            if (near) {
+#pragma unroll
+              for (int k = 0; k < D; ++k) { vlo[k] = fmin(vlo[k], fc[k]); vhi[k] = fmax(vhi[k], fc[k]); }
+            }
+          }
+        }
+        for (int i = 0; i < nb && !hit; ++i) {
+          bool sep = false;
+#pragma unroll
+          for (int k = 0; k < D; ++k)
+            if (cbox[i * 2 * D + k] > vhi[k] + 1e-3 || cbox[i * 2 * D + D + k] < vlo[k] - 1e-3) sep = true;
+          hit = !sep;
+        }
+      }
+    }
+    const unsigned msk = __ballot_sync(FULL, hit);
+    if (msk) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(n_items, (unsigned long long)__popc(msk));
+      base = __shfl_sync(FULL, base, 0);
+      if (hit) items[base + __popc(msk & lt)] = make_longlong2(row, e);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1085,10 +1215,18 @@ cudaError_t launch_near(dim3 grid, cudaStream_t st, const mpap_roadmap* rm, cons
   return cudaGetLastError();
 }
 
+struct EdgeWork {            // what one k_edges launch processes
+  const NearRec* scratch;    // build mode: neighbour scratch (cap entries per row)
+  int cap;
+  const longlong2* items;    // update mode: affected edges (else nullptr)
+  int64_t n_items;
+  unsigned long long* nnz_free;
+  unsigned long long* work;
+  unsigned long long* next;  // item counter (zeroed)
+};
+
 template <int D, int DYN, int PHASE, int HEUR>
-cudaError_t launch_edges_phase(size_t smem, cudaStream_t st, const mpap_roadmap* rm, int cap, const int32_t* d_cnt,
-                               const NearRec* d_scr, unsigned long long* d_free, unsigned long long* d_work,
-                               unsigned long long* d_next) {
+cudaError_t launch_edges_phase(size_t smem, cudaStream_t st, const mpap_roadmap* rm, const EdgeWork& ew) {
   auto kern = k_edges<D, DYN, PHASE, HEUR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)std::max<size_t>(smem, 1));
@@ -1098,27 +1236,37 @@ cudaError_t launch_edges_phase(size_t smem, cudaStream_t st, const mpap_roadmap*
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
   if (e != cudaSuccess) return e;
-  const int64_t N = rm->node_base[rm->B];
-  const int64_t need = (N + kWarps - 1) / kWarps;
+  const int64_t NI = ew.items ? ew.n_items : rm->node_base[rm->B];
+  const int64_t need = (NI + kWarps - 1) / kWarps;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(per_sm, 1), need));
   kern<<<grid, kWarps * 32, smem, st>>>(rm->d_samples, rm->d_node_base, rm->B, rm->d_obst, rm->d_obst_base,
-                                        rm->d_feat, rm->d_feat_base, rm->prm, cap, rm->o_max, rm->f_max, d_cnt,
-                                        d_scr, rm->d_row_ptr, rm->d_edges, rm->d_peak, d_free, d_work, d_next);
+                                        rm->d_feat, rm->d_feat_base, rm->prm, ew.cap, rm->o_max, rm->f_max,
+                                        ew.scratch, rm->d_row_ptr, rm->d_edges, rm->d_tau, rm->d_peak, ew.items,
+                                        ew.n_items, ew.nnz_free, ew.work, ew.next);
   return cudaGetLastError();
 }
 
 template <int D, int DYN>
-cudaError_t launch_edges(int phase, size_t smem, cudaStream_t st, const mpap_roadmap* rm, int cap,
-                         const int32_t* d_cnt, const NearRec* d_scr, unsigned long long* d_free,
-                         unsigned long long* d_work, unsigned long long* d_next) {
-  if (phase == 0)
-    return launch_edges_phase<D, DYN, 0, 0>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next);
+cudaError_t launch_edges(int phase, size_t smem, cudaStream_t st, const mpap_roadmap* rm, EdgeWork ew) {
+  if (phase == 0) return launch_edges_phase<D, DYN, 0, 0>(smem, st, rm, ew);
+  ew.next += 1;
   switch (rm->prm.heuristic) {
-    case 0: return launch_edges_phase<D, DYN, 1, 0>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next + 1);
-    case 1: return launch_edges_phase<D, DYN, 1, 1>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next + 1);
-    case 2: return launch_edges_phase<D, DYN, 1, 2>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next + 1);
-    default: return launch_edges_phase<D, DYN, 1, 3>(smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next + 1);
+    case 0: return launch_edges_phase<D, DYN, 1, 0>(smem, st, rm, ew);
+    case 1: return launch_edges_phase<D, DYN, 1, 1>(smem, st, rm, ew);
+    case 2: return launch_edges_phase<D, DYN, 1, 2>(smem, st, rm, ew);
+    default: return launch_edges_phase<D, DYN, 1, 3>(smem, st, rm, ew);
   }
+}
+
+cudaError_t launch_edges_any(int phase, size_t smem, cudaStream_t st, const mpap_roadmap* rm, const EdgeWork& ew) {
+  const int d = rm->prm.pos_dim, dyn = rm->prm.dynamics;
+  if (d == 2) return dyn ? launch_edges<2, 1>(phase, smem, st, rm, ew) : launch_edges<2, 0>(phase, smem, st, rm, ew);
+  return dyn ? launch_edges<3, 1>(phase, smem, st, rm, ew) : launch_edges<3, 0>(phase, smem, st, rm, ew);
+}
+
+size_t edges_smem(const mpap_roadmap* rm) {
+  const int d = rm->prm.pos_dim;
+  return sizeof(double) * (size_t)kWarps * ((size_t)rm->f_max * (d + 1) + (size_t)rm->o_max * 2 * d);
 }
 }  // namespace
 
@@ -1197,19 +1345,17 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
     rm->d_peak = static_cast<float2*>(rm_alloc(sizeof(float2) * std::max<int64_t>(rm->nnz_total, 1), st));
     if (!rm->d_peak) return set_error(MPAP_ERR_OUT_OF_MEMORY, "peak array allocation failed");
   }
-  const size_t smem = sizeof(double) * (size_t)kWarps * ((size_t)rm->f_max * (d + 1) + (size_t)rm->o_max * 2 * d);
+  rm->d_tau = static_cast<double*>(rm_alloc(sizeof(double) * std::max<int64_t>(rm->nnz_total, 1), st));
+  if (!rm->d_tau) return set_error(MPAP_ERR_OUT_OF_MEMORY, "tau array allocation failed");
+  const size_t smem = edges_smem(rm);
   unsigned long long* d_next = nullptr;
   CK(cudaMallocAsync(&d_next, 2 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(d_next, 0, 2 * sizeof(unsigned long long), st));
   if (rm->nnz_total > 0) {
     for (int phase = 0; phase < 2; ++phase) {
       ProfScope ps(phase == 0 ? "k_collide" : "k_heuristic", st);
-      cudaError_t e;
-      if (d == 2) e = dyn ? launch_edges<2, 1>(phase, smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next)
-                          : launch_edges<2, 0>(phase, smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next);
-      else e = dyn ? launch_edges<3, 1>(phase, smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next)
-                   : launch_edges<3, 0>(phase, smem, st, rm, cap, d_cnt, d_scr, d_free, d_work, d_next);
-      CK(e);
+      const EdgeWork ew{d_scr, cap, nullptr, 0, d_free, d_work, d_next};
+      CK(launch_edges_any(phase, smem, st, rm, ew));
       note_launch();
     }
   }
@@ -1227,6 +1373,88 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
     CK(cudaStreamSynchronize(st));
   }
   rm->nnz_free.assign(fr.begin(), fr.end());
+  return MPAP_OK;
+}
+
+// NEXT-1: online update of one environment.  The obstacle and
+// feature arrays of rm already hold the new sets; cbox / cfeat are the
+// changed boxes and features (symmetric differences, host).  Lists the
+// affected edges (k_affected) and re-runs collision and heuristic on exactly
+// those (k_edges in item mode), so the roadmap equals a full build of the new
+// environment bit for bit.
+mpap_status update_roadmap_device(mpap_roadmap* rm, int env, const std::vector<double>& cbox,
+                                  const std::vector<double>& cfeat, int64_t* n_reeval, cudaStream_t st) {
+  const int d = rm->prm.pos_dim, dyn = rm->prm.dynamics;
+  const int nb = (int)(cbox.size() / (2 * d)), nf = (int)(cfeat.size() / d);
+  const int64_t row0 = rm->node_base[env], n_rows = rm->n[env];
+  const int64_t nnz_env = rm->edge_base[env + 1] - rm->edge_base[env];
+  if (n_reeval) *n_reeval = 0;
+  if ((nb == 0 && nf == 0) || nnz_env == 0) return MPAP_OK;
+  double* d_cb = nullptr;
+  double* d_cf = nullptr;
+  longlong2* d_items = nullptr;
+  unsigned long long* d_ctr = nullptr;   // [0] n_items, [1..2] item counters, [3] free delta, [4..] work
+  CK(cudaMallocAsync(&d_cb, sizeof(double) * std::max<size_t>(cbox.size(), 1), st));
+  CK(cudaMallocAsync(&d_cf, sizeof(double) * std::max<size_t>(cfeat.size(), 1), st));
+  if (nb) CK(cudaMemcpyAsync(d_cb, cbox.data(), sizeof(double) * cbox.size(), cudaMemcpyHostToDevice, st));
+  if (nf) CK(cudaMemcpyAsync(d_cf, cfeat.data(), sizeof(double) * cfeat.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaMallocAsync(&d_items, sizeof(longlong2) * nnz_env, st));
+  CK(cudaMallocAsync(&d_ctr, sizeof(unsigned long long) * (4 + W_NUM), st));
+  CK(cudaMemsetAsync(d_ctr, 0, sizeof(unsigned long long) * (4 + W_NUM), st));
+  {
+    ProfScope ps("k_affected", st);
+    const dim3 grid((unsigned)((n_rows + kWarps - 1) / kWarps));
+    const double* es = rm->d_samples + row0 * rm->prm.stride;
+    const double R = rm->prm.max_range;
+    int64_t fb = 0;
+    for (int b = 0; b < env; ++b) fb += rm->n_feat[b];
+    const double* ef = rm->d_feat + fb * d;
+    const int F = rm->n_feat[env];
+    if (d == 2) {
+      if (dyn) k_affected<2, 1><<<grid, kWarps * 32, 0, st>>>(es, rm->prm.stride, row0, n_rows, rm->d_row_ptr,
+                                                              rm->d_edges, rm->d_tau, R, ef, F, d_cb, nb, d_cf, nf,
+                                                              d_items, d_ctr);
+      else k_affected<2, 0><<<grid, kWarps * 32, 0, st>>>(es, rm->prm.stride, row0, n_rows, rm->d_row_ptr,
+                                                          rm->d_edges, rm->d_tau, R, ef, F, d_cb, nb, d_cf, nf, d_items,
+                                                          d_ctr);
+    } else {
+      if (dyn) k_affected<3, 1><<<grid, kWarps * 32, 0, st>>>(es, rm->prm.stride, row0, n_rows, rm->d_row_ptr,
+                                                              rm->d_edges, rm->d_tau, R, ef, F, d_cb, nb, d_cf, nf,
+                                                              d_items, d_ctr);
+      else k_affected<3, 0><<<grid, kWarps * 32, 0, st>>>(es, rm->prm.stride, row0, n_rows, rm->d_row_ptr,
+                                                          rm->d_edges, rm->d_tau, R, ef, F, d_cb, nb, d_cf, nf, d_items,
+                                                          d_ctr);
+    }
+    CK(cudaGetLastError());
+  }
+  note_launch();
+  unsigned long long n_items = 0;
+  CK(cudaMemcpyAsync(&n_items, d_ctr, sizeof(n_items), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (n_items > 0) {
+    // the free-edge delta is accumulated in a per-env array indexed by env
+    unsigned long long* d_free = nullptr;
+    CK(cudaMallocAsync(&d_free, sizeof(unsigned long long) * rm->B, st));
+    CK(cudaMemsetAsync(d_free, 0, sizeof(unsigned long long) * rm->B, st));
+    const size_t smem = edges_smem(rm);
+    for (int phase = 0; phase < 2; ++phase) {
+      ProfScope ps(phase == 0 ? "k_collide" : "k_heuristic", st);
+      const EdgeWork ew{nullptr, 0, d_items, (int64_t)n_items, d_free, d_ctr + 4 - W_EDGES, d_ctr + 1};
+      CK(launch_edges_any(phase, smem, st, rm, ew));
+      note_launch();
+    }
+    unsigned long long delta = 0;
+    CK(cudaMemcpyAsync(&delta, d_free + env, sizeof(delta), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaFreeAsync(d_free, st));
+    rm->nnz_free[env] += (int64_t)(long long)delta;
+  }
+  CK(cudaFreeAsync(d_cb, st));
+  CK(cudaFreeAsync(d_cf, st));
+  CK(cudaFreeAsync(d_items, st));
+  CK(cudaFreeAsync(d_ctr, st));
+  CK(cudaStreamSynchronize(st));
+  if (n_reeval) *n_reeval = (int64_t)n_items;
   return MPAP_OK;
 }
 

@@ -3,6 +3,7 @@
 // memory ownership.  All compute happens in build_kernels.cu / search_kernels.cu.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -310,7 +311,7 @@ void mpap_roadmap_free(mpap_roadmap* rm) {
   // wait for the device, then hand the memory back to the stream-ordered pool
   cudaDeviceSynchronize();
   void* ptrs[] = {rm->d_samples, rm->d_obst, rm->d_feat, rm->d_obst_base, rm->d_feat_base, rm->d_node_base,
-                  rm->d_row_ptr, rm->d_edges, rm->d_peak};
+                  rm->d_row_ptr, rm->d_edges, rm->d_peak, rm->d_tau};
   for (void* p : ptrs) rm_release(p);   // device is idle: safe to reuse from any stream
   cudaSetDevice(cur);
   delete rm;
@@ -532,6 +533,123 @@ mpap_status mpap_roadmap_export(const mpap_roadmap* rm, int32_t env, int32_t* ro
     if (c) c[k] = er[k].c;
   }
   return MPAP_OK;
+}
+
+// Multiset symmetric difference of two lists of k-double rows (exact compare).
+static void sym_diff(const std::vector<double>& a, const std::vector<double>& b, int k, std::vector<double>& out) {
+  auto rows = [k](const std::vector<double>& v) {
+    std::vector<std::vector<double>> r(v.size() / k);
+    for (size_t i = 0; i < r.size(); ++i) r[i].assign(v.begin() + i * k, v.begin() + (i + 1) * k);
+    std::sort(r.begin(), r.end());
+    return r;
+  };
+  const auto ra = rows(a), rb = rows(b);
+  size_t i = 0, j = 0;
+  while (i < ra.size() || j < rb.size()) {
+    if (j == rb.size() || (i < ra.size() && ra[i] < rb[j])) {
+      out.insert(out.end(), ra[i].begin(), ra[i].end());
+      ++i;
+    } else if (i == ra.size() || rb[j] < ra[i]) {
+      out.insert(out.end(), rb[j].begin(), rb[j].end());
+      ++j;
+    } else {
+      ++i;
+      ++j;
+    }
+  }
+}
+
+// Replace env's segment of a concatenated per-env array (rows of k doubles).
+static mpap_status splice_env(double** arr, int32_t** d_base, std::vector<int32_t>& counts, int env,
+                              const std::vector<double>& seg, int k, cudaStream_t st) {
+  const int B = (int)counts.size();
+  std::vector<int32_t> base(B + 1, 0);
+  for (int b = 0; b < B; ++b) base[b + 1] = base[b] + counts[b];
+  const int32_t n_new = (int32_t)(seg.size() / k);
+  const int64_t tot = (int64_t)base[B] - counts[env] + n_new;
+  double* na = static_cast<double*>(rm_alloc(sizeof(double) * std::max<int64_t>(tot * k, 1), st));
+  if (!na) return MPAP_ERR_OUT_OF_MEMORY;
+  const int64_t head = (int64_t)base[env] * k, tail = ((int64_t)base[B] - base[env + 1]) * k;
+  cudaError_t e = cudaSuccess;
+  if (head) e = cudaMemcpyAsync(na, *arr, sizeof(double) * head, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && n_new)
+    e = cudaMemcpyAsync(na + head, seg.data(), sizeof(double) * seg.size(), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && tail)
+    e = cudaMemcpyAsync(na + head + (int64_t)n_new * k, *arr + (int64_t)base[env + 1] * k, sizeof(double) * tail,
+                        cudaMemcpyDeviceToDevice, st);
+  counts[env] = n_new;
+  for (int b = 0; b < B; ++b) base[b + 1] = base[b] + counts[b];
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(*d_base, base.data(), sizeof(int32_t) * (B + 1), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    rm_release(na);
+    return cuda_error(e, "splice env arrays");
+  }
+  rm_release(*arr);
+  *arr = na;
+  return MPAP_OK;
+}
+
+mpap_status mpap_roadmap_update(mpap_roadmap* rm, int32_t env, const double* obstacles, int32_t n_obstacles,
+                                const double* features, int32_t n_features, int32_t mem, void* cuda_stream,
+                                int64_t* n_reevaluated) {
+  if (n_reevaluated) *n_reevaluated = 0;
+  if (!rm || env < 0 || env >= rm->B) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad roadmap/env");
+  if (!rm->d_tau) return set_error(MPAP_ERR_INVALID_ARGUMENT, "imported roadmaps cannot be updated");
+  if (mem != MPAP_MEM_HOST && mem != MPAP_MEM_DEVICE) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad mem space");
+  if (n_obstacles < 0 || n_features < 0 || (n_obstacles > 0 && !obstacles) || (n_features > 0 && !features))
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad obstacle/feature arrays");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != rm->device) return set_error(MPAP_ERR_INVALID_ARGUMENT, "roadmap bound to another device");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  const int d = rm->prm.pos_dim;
+  std::vector<double> nbx((size_t)n_obstacles * 2 * d), nft((size_t)n_features * d);
+  const cudaMemcpyKind kind = (mem == MPAP_MEM_HOST) ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost;
+  cudaError_t e = cudaSuccess;
+  if (n_obstacles) e = cudaMemcpy(nbx.data(), obstacles, sizeof(double) * nbx.size(), kind);
+  if (e == cudaSuccess && n_features) e = cudaMemcpy(nft.data(), features, sizeof(double) * nft.size(), kind);
+  if (e != cudaSuccess) return cuda_error(e, "update inputs");
+  for (double x : nbx)
+    if (!is_fin(x)) return set_error(MPAP_ERR_INVALID_ARGUMENT, "non-finite obstacle");
+  for (double x : nft)
+    if (!is_fin(x)) return set_error(MPAP_ERR_INVALID_ARGUMENT, "non-finite feature");
+  for (int32_t o = 0; o < n_obstacles; ++o)
+    for (int k = 0; k < d; ++k)
+      if (!(nbx[(size_t)o * 2 * d + k] < nbx[(size_t)o * 2 * d + d + k]))
+        return set_error(MPAP_ERR_INVALID_ARGUMENT, "obstacle with lo >= hi");
+  // the old sets of this env
+  cudaDeviceSynchronize();   // searches / builds reading the old arrays may be in flight
+  int64_t ob = 0, fb = 0;
+  for (int b = 0; b < env; ++b) {
+    ob += rm->n_obst[b];
+    fb += rm->n_feat[b];
+  }
+  std::vector<double> obx((size_t)rm->n_obst[env] * 2 * d), oft((size_t)rm->n_feat[env] * d);
+  if (!obx.empty()) e = cudaMemcpy(obx.data(), rm->d_obst + ob * 2 * d, sizeof(double) * obx.size(),
+                                   cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && !oft.empty())
+    e = cudaMemcpy(oft.data(), rm->d_feat + fb * d, sizeof(double) * oft.size(), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_error(e, "update old sets");
+  std::vector<double> cbox, cfeat;
+  sym_diff(obx, nbx, 2 * d, cbox);
+  sym_diff(oft, nft, d, cfeat);
+  mpap_status s = MPAP_OK;
+  if (!cbox.empty()) {
+    s = splice_env(&rm->d_obst, &rm->d_obst_base, rm->n_obst, env, nbx, 2 * d, st);
+    if (s != MPAP_OK) return s;
+  }
+  if (!cfeat.empty()) {
+    s = splice_env(&rm->d_feat, &rm->d_feat_base, rm->n_feat, env, nft, d, st);
+    if (s != MPAP_OK) return s;
+  }
+  rm->o_max = rm->f_max = 0;
+  for (int b = 0; b < rm->B; ++b) {
+    rm->o_max = std::max(rm->o_max, rm->n_obst[b]);
+    rm->f_max = std::max(rm->f_max, rm->n_feat[b]);
+  }
+  return update_roadmap_device(rm, env, cbox, cfeat, n_reevaluated, st);
 }
 
 mpap_status mpap_roadmap_export_peaks(const mpap_roadmap* rm, int32_t env, float* S, float* C) {

@@ -66,6 +66,7 @@ struct mpap_roadmap {
   int64_t* d_node_base = nullptr;  // [B+1]
   int64_t* d_row_ptr = nullptr;    // [sum n + 1] global edge offsets
   mpap::EdgeRec* d_edges = nullptr;
+  double* d_tau = nullptr;         // [nnz_total] edge durations (NEXT-1 updates re-evaluate edges from it)
   float2* d_peak = nullptr;        // [nnz_total] (S, C) prefix maxima per edge (NEXT-3); may be null (import)
   int64_t nnz_total = 0;
   unsigned long long work[mpap::kWorkCounters] = {};  // build work counters (mpap_roadmap_work)
@@ -127,6 +128,10 @@ mpap_status cuda_error(cudaError_t e, const char* what);
 
 // roadmap build (build_kernels.cu)
 mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st);
+// NEXT-1: re-evaluate the edges of env affected by the changed boxes/features
+// (host arrays); rm's obstacle/feature arrays already hold the new sets.
+mpap_status update_roadmap_device(mpap_roadmap* rm, int env, const std::vector<double>& cbox,
+                                  const std::vector<double>& cfeat, int64_t* n_reeval, cudaStream_t st);
 
 // search (search_kernels.cu)
 struct QueryDesc {
