@@ -35,13 +35,27 @@
 namespace mpap {
 
 #define FULL 0xffffffffu
+#ifndef MPAP_EDGE_SMEM
+#define MPAP_EDGE_SMEM 1
+#endif
+#ifndef MPAP_FEAT_TWO_PASS
+#define MPAP_FEAT_TWO_PASS 0
+#endif
+#ifndef MPAP_FEAT_UNROLL
+#define MPAP_FEAT_UNROLL 1
+#endif
+constexpr int kFeatUnroll = MPAP_FEAT_UNROLL;
 #ifndef MPAP_LAZY_INV
 #define MPAP_LAZY_INV 0
 #endif
 #ifndef MPAP_EDGES_MIN_BLOCKS
-#define MPAP_EDGES_MIN_BLOCKS 1
+#define MPAP_EDGES_MIN_BLOCKS 4
 #endif
-constexpr int kWarps = 8;                 // warps per block in the build kernels
+#ifndef MPAP_KWARPS
+#define MPAP_KWARPS 4
+#endif
+constexpr int kWarps = MPAP_KWARPS;       // warps per block of the edge kernels
+constexpr int kNearWarps = 8;             // warps per block of k_near
 constexpr double kCullMargin = 1e-6;      // absolute; >> rounding of O(100) coordinates
 constexpr int kNearIntervals = 16;        // level-2 neighbour filter resolution
 
@@ -64,7 +78,7 @@ __device__ __forceinline__ bool seg_box(const double* A, const double* B, const 
     if (dk == 0.0) {
       if (A[k] < lo || A[k] > hi) return false;
     } else {
-      const double inv = 1.0 / dk;
+      const double inv = __drcp_rn(dk);   // == 1.0 / dk (both correctly rounded)
       double ta = (lo - A[k]) * inv;
       double tb = (hi - A[k]) * inv;
       if (ta > tb) { const double tmp = ta; ta = tb; tb = tmp; }
@@ -212,18 +226,18 @@ enum {
 // k_near
 // ---------------------------------------------------------------------------
 template <int D, int DYN>
-__global__ void __launch_bounds__(kWarps * 32) k_near(const double* __restrict__ samples,
+__global__ void __launch_bounds__(kNearWarps * 32) k_near(const double* __restrict__ samples,
                                                       const int64_t* __restrict__ node_base,
                                                       const int32_t* __restrict__ n_env, DevParams P, int cap,
                                                       int32_t* __restrict__ cnt, NearRec* __restrict__ scratch,
                                                       int* __restrict__ overflow,
                                                       unsigned long long* __restrict__ work) {
   constexpr int NS = DYN ? 2 * D : D;   // state doubles used by the cost
-  __shared__ int queue[kWarps][64];
+  __shared__ int queue[kNearWarps][64];
   const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = n_env[b];
-  const int u = blockIdx.x * kWarps + warp;
+  const int u = blockIdx.x * kNearWarps + warp;
   if (u >= nb) return;  // warp-uniform
   const int64_t row = node_base[b] + u;
   const int stride = P.stride;
@@ -489,7 +503,7 @@ __device__ __forceinline__ unsigned seg_hits_boxes(const double* A, const double
   double inv[D], slo[D], shi[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    inv[k] = (!MPAP_LAZY_INV && Dv[k] != 0.0) ? 1.0 / Dv[k] : 0.0;
+    inv[k] = (!MPAP_LAZY_INV && Dv[k] != 0.0) ? __drcp_rn(Dv[k]) : 0.0;   // == 1.0 / Dv[k]
     slo[k] = fmin(A[k], B[k]) - kCullMargin;
     shi[k] = fmax(A[k], B[k]) + kCullMargin;
   }
@@ -512,7 +526,7 @@ __device__ __forceinline__ unsigned seg_hits_boxes(const double* A, const double
     if (sep) continue;
     if (!have_inv) {
 #pragma unroll
-      for (int k = 0; k < D; ++k) inv[k] = (Dv[k] != 0.0) ? 1.0 / Dv[k] : 0.0;
+      for (int k = 0; k < D; ++k) inv[k] = (Dv[k] != 0.0) ? __drcp_rn(Dv[k]) : 0.0;
       have_inv = true;
     }
     ++tests;
@@ -706,11 +720,34 @@ __device__ __forceinline__ void chunk_bbox(const double* su, const double* sv, c
 template <int D, int DYN, int HEUR>
 __device__ void edge_heuristic(const DevParams& P, const double* su, const double* sv, double T,
                                const double* __restrict__ feat, int F, const double* __restrict__ box, int O,
-                               WarpLists<D>& L, double* fold, int lane, double& s_out, double& c_out,
-                               double& S_out, double& C_out, Work& W) {
+                               WarpLists<D>& L, double* fold, double* ec, int lane, double& s_out,
+                               double& c_out, double& S_out, double& C_out, Work& W) {
   const double kk = ceil(T / P.dt);
   const int K = (kk < 1.0) ? 1 : (int)kk;
   const double Dl = T / (double)K;
+#if MPAP_EDGE_SMEM
+  // per-edge trajectory constants live in the warp's shared scratch `ec`
+  // (read per chunk / per step) instead of 4*D registers
+  {
+    double t2[D], t3[D], q0[D], q1[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) { t2[j] = 0.0; t3[j] = 0.0; q0[j] = -1.0; q1[j] = -1.0; }
+    if (DYN == 1) {
+      di_traj<D>(su, sv, T, t2, t3);
+      cubic_stationary<D>(su, t2, t3, q0, q1);
+    }
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) { ec[j] = t2[j]; ec[D + j] = t3[j]; ec[2 * D + j] = q0[j]; ec[3 * D + j] = q1[j]; }
+    }
+    __syncwarp();
+  }
+  const double* c2 = ec;
+  const double* c3 = ec + D;
+  const double* r0 = ec + 2 * D;
+  const double* r1 = ec + 3 * D;
+#else
   double c2[D], c3[D], r0[D], r1[D];
 #pragma unroll
   for (int j = 0; j < D; ++j) { c2[j] = 0.0; c3[j] = 0.0; r0[j] = -1.0; r1[j] = -1.0; }
@@ -718,11 +755,20 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
     di_traj<D>(su, sv, T, c2, c3);
     cubic_stationary<D>(su, c2, c3, r0, r1);
   }
+#endif
   const int hoff = P.hoff;
   double omega = 0.0;
+#if MPAP_EDGE_SMEM
+#define hu0 su[hoff]
+#define hu1 su[hoff + 1]
+#define hv0 sv[hoff]
+#define hv1 sv[hoff + 1]
+  if (P.has_heading) {
+#else
   double hu0 = 0.0, hu1 = 0.0, hv0 = 0.0, hv1 = 0.0;
   if (P.has_heading) {
     hu0 = su[hoff]; hu1 = su[hoff + 1]; hv0 = sv[hoff]; hv1 = sv[hoff + 1];
+#endif
     const double ex = hv0 - hu0, ey = hv1 - hu1;
     omega = sqrt(ex * ex + ey * ey) / T;
   }
@@ -890,6 +936,41 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
 #pragma unroll
       for (int j = 0; j < D; ++j) hh = fma(hv[j], hv[j], hh);
       int kv = 0;
+#if MPAP_FEAT_TWO_PASS
+      // Two passes per 32 features: range + FOV for each (independent
+      // chains), then the occlusion test for the candidates.
+      for (int i0 = 0; i0 < nf; i0 += 32) {
+        const int ie = min(nf, i0 + 32);
+        unsigned cand = 0u;
+#pragma unroll kFeatUnroll
+        for (int i = i0; i < ie; ++i) {
+          double dl[D];
+          double dd = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) { dl[j] = L.f[j][i] - x[j]; dd = fma(dl[j], dl[j], dd); }
+          bool ok = !(dd > R2);
+          if (heur != 0) {
+            double dot = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) dot = fma(hv[j], dl[j], dot);
+            ok = ok && (hh > 0.0) && !(dot < 0.0) && !(dot * dot < cos2 * (hh * dd));
+          }
+          cand |= (ok ? 1u : 0u) << (i - i0);
+        }
+        while (cand) {
+          const int i = i0 + __ffs(cand) - 1;
+          cand &= cand - 1u;
+          double fp[D], dl[D];
+#pragma unroll
+          for (int j = 0; j < D; ++j) { fp[j] = L.f[j][i]; dl[j] = fp[j] - x[j]; }
+          ++W.occl_segs;
+          const unsigned rr = use_mask ? seg_hits_boxes<D, true>(x, fp, dl, L.box, nb, L.fmask[i])
+                                       : seg_hits_boxes<D, false>(x, fp, dl, L.box, nb, 0ull);
+          W.occl_tests += rr >> 1;
+          if (!(rr & 1u)) ++kv;
+        }
+      }
+#else
       for (int i = 0; i < nf; ++i) {
         double dl[D];
         double dd = 0.0;
@@ -913,6 +994,7 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
         W.occl_tests += rr >> 1;
         if (!(rr & 1u)) ++kv;
       }
+#endif
       inc = Dl - (double)kv * (Dl / P.n_f);
       if (heur == 3) {
         const double z0 = speed / P.v_ref;
@@ -947,6 +1029,12 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
   c_out = c;
   S_out = Sp;
   C_out = Cp;
+#if MPAP_EDGE_SMEM
+#undef hu0
+#undef hu1
+#undef hv0
+#undef hv1
+#endif
 }
 
 // Persistent: each warp pulls work items from an atomic counter, so no block
@@ -984,6 +1072,7 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
   __shared__ unsigned s_work[kWarps][W_NUM];
   __shared__ double s_mlp[kMlpSize];
   __shared__ double s_fold[kWarps][32];
+  __shared__ double s_ec[kWarps][12];
   for (int i = threadIdx.x; i < kMlpSize; i += blockDim.x) s_mlp[i] = P.mlp[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1078,8 +1167,8 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
         if (lane < NS) sv[lane] = (lane < stride) ? envs[(int64_t)(dc & 0x7fffffffu) * stride + lane] : 0.0;
         __syncwarp();
         double s64, c64, S64, C64;
-        edge_heuristic<D, DYN, HEUR>(P, su, sv, tau, efeat, F, ebox, O, L, s_fold[warp], lane, s64, c64, S64,
-                                     C64, W);
+        edge_heuristic<D, DYN, HEUR>(P, su, sv, tau, efeat, F, ebox, O, L, s_fold[warp], s_ec[warp], lane, s64,
+                                     c64, S64, C64, W);
         W.flush(lane);
         if (lane == 0) {
           *reinterpret_cast<float2*>(&edges[e].s) = make_float2((float)s64, (float)c64);
@@ -1210,7 +1299,7 @@ namespace {
 template <int D, int DYN>
 cudaError_t launch_near(dim3 grid, cudaStream_t st, const mpap_roadmap* rm, const int32_t* d_n, int cap,
                         int32_t* d_cnt, NearRec* d_scr, int* d_over, unsigned long long* d_work) {
-  k_near<D, DYN><<<grid, kWarps * 32, 0, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->prm, cap, d_cnt, d_scr,
+  k_near<D, DYN><<<grid, kNearWarps * 32, 0, st>>>(rm->d_samples, rm->d_node_base, d_n, rm->prm, cap, d_cnt, d_scr,
                                                d_over, d_work);
   return cudaGetLastError();
 }
@@ -1294,7 +1383,7 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
   CK(cudaMemsetAsync(d_work, 0, sizeof(unsigned long long) * W_NUM, st));
   rm->d_row_ptr = static_cast<int64_t*>(rm_alloc(sizeof(int64_t) * (N + 1), st));
   if (!rm->d_row_ptr) return MPAP_ERR_OUT_OF_MEMORY;
-  const dim3 grid((rm->n_max + kWarps - 1) / kWarps, B);
+  const dim3 grid((rm->n_max + kNearWarps - 1) / kNearWarps, B);
   for (int attempt = 0; attempt < 8; ++attempt) {
     const size_t bytes = sizeof(NearRec) * (size_t)N * (size_t)cap;
     d_scr = static_cast<NearRec*>(workspace(st, WS_NEAR, bytes));
