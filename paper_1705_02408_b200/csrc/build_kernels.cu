@@ -38,6 +38,15 @@ namespace mpap {
 #ifndef MPAP_EDGE_SMEM
 #define MPAP_EDGE_SMEM 1
 #endif
+#ifndef MPAP_NEAR_HIER
+#define MPAP_NEAR_HIER 1
+#endif
+#ifndef MPAP_SEG_INLINE_BB
+#define MPAP_SEG_INLINE_BB 0
+#endif
+#ifndef MPAP_EDGE_SMEM2
+#define MPAP_EDGE_SMEM2 0
+#endif
 #ifndef MPAP_FEAT_TWO_PASS
 #define MPAP_FEAT_TWO_PASS 0
 #endif
@@ -234,6 +243,24 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_near(const double* __restri
                                                       unsigned long long* __restrict__ work) {
   constexpr int NS = DYN ? 2 * D : D;   // state doubles used by the cost
   __shared__ int queue[kNearWarps][64];
+#if MPAP_NEAR_HIER
+  // interval tables of the level-2 filter: [level][interval] = {ta, tb, 1/tb, 1/tb^3}
+  // for the whole range (level 0), quarters (1) and sixteenths (2) of (0, r]
+  __shared__ double s_near[3][16][4];
+  if (DYN == 1 && threadIdx.x < 21) {
+    const int t = threadIdx.x;
+    const int lvl = (t == 0) ? 0 : (t < 5) ? 1 : 2;
+    const int jj = (t == 0) ? 0 : (t < 5) ? t - 1 : t - 5;
+    const int nseg = (lvl == 0) ? 1 : (lvl == 1) ? 4 : 16;
+    const double ta = P.r * (double)jj / (double)nseg;
+    const double tb = P.r * (double)(jj + 1) / (double)nseg;
+    s_near[lvl][jj][0] = ta;
+    s_near[lvl][jj][1] = tb;
+    s_near[lvl][jj][2] = 1.0 / tb;
+    s_near[lvl][jj][3] = 1.0 / (tb * tb * tb);
+  }
+  __syncthreads();
+#endif
   const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = n_env[b];
@@ -334,6 +361,25 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_near(const double* __restri
             as += a * e;
           }
           const double tv = (ss > 0.0) ? 2.0 * as / ss : 0.0;   // vertex of the quadratic
+#if MPAP_NEAR_HIER
+          // Lower bound of c on [ta, tb] (reciprocals of tb from the block's
+          // table): tested on [0, r], then on its 4 quarters, then on the 4
+          // sixteenths of each quarter that is still possible.
+          auto possible_on = [&](int lvl, int jj) -> bool {
+            const double ta = s_near[lvl][jj][0], tb = s_near[lvl][jj][1];
+            const double tq = fmin(fmax(tv, ta), tb);
+            const double g2 = fmax(dp2 - tq * as + tq * tq * ss * 0.25, 0.0);
+            const double L = ta + ru * (12.0 * g2 * s_near[lvl][jj][3] + dv2 * s_near[lvl][jj][2]);
+            return L * (1.0 - 1e-9) < r;
+          };
+          bool possible = false;
+          if (possible_on(0, 0)) {
+            for (int q = 0; q < 4 && !possible; ++q) {
+              if (!possible_on(1, q)) continue;
+              for (int jj = 4 * q; jj < 4 * q + 4 && !possible; ++jj) possible = possible_on(2, jj);
+            }
+          }
+#else
           bool possible = false;
           for (int jj = 0; jj < kNearIntervals && !possible; ++jj) {
             const double ta = r * (double)jj / (double)kNearIntervals;
@@ -343,6 +389,7 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_near(const double* __restri
             const double L = ta + ru * (12.0 * g2 / (tb * tb * tb) + dv2 / tb);
             possible = L * (1.0 - 1e-9) < r;
           }
+#endif
           pf = possible;
         }
       }
@@ -500,6 +547,11 @@ __device__ int cull_boxes(const double* __restrict__ box, int O, const double* l
 template <int D, bool USE_MASK>
 __device__ __forceinline__ unsigned seg_hits_boxes(const double* A, const double* B, const double* Dv,
                                                    const double* bl, int nl, unsigned long long mask) {
+#if MPAP_SEG_INLINE_BB
+  double inv[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) inv[k] = (!MPAP_LAZY_INV && Dv[k] != 0.0) ? __drcp_rn(Dv[k]) : 0.0;   // == 1.0 / Dv[k]
+#else
   double inv[D], slo[D], shi[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
@@ -507,6 +559,7 @@ __device__ __forceinline__ unsigned seg_hits_boxes(const double* A, const double
     slo[k] = fmin(A[k], B[k]) - kCullMargin;
     shi[k] = fmax(A[k], B[k]) + kCullMargin;
   }
+#endif
   bool have_inv = !MPAP_LAZY_INV;   // reciprocals formed only if some box survives the prefilter
   unsigned tests = 0;
   int i = -1;
@@ -521,8 +574,13 @@ __device__ __forceinline__ unsigned seg_hits_boxes(const double* A, const double
     const double* bx = bl + (size_t)i * 2 * D;
     bool sep = false;
 #pragma unroll
-    for (int k = 0; k < D; ++k)
+    for (int k = 0; k < D; ++k) {
+#if MPAP_SEG_INLINE_BB
+      if (bx[k] > fmax(A[k], B[k]) + kCullMargin || bx[D + k] < fmin(A[k], B[k]) - kCullMargin) sep = true;
+#else
       if (bx[k] > shi[k] || bx[D + k] < slo[k]) sep = true;
+#endif
+    }
     if (sep) continue;
     if (!have_inv) {
 #pragma unroll
@@ -810,7 +868,20 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
       }
     }
   }
+#if MPAP_EDGE_SMEM2
+  // the bearing-cull constants are only read per chunk: keep them in the
+  // warp's scratch, not in registers across the step loop
+  __syncwarp();
+  if (lane == 0) {
+    float* ef = reinterpret_cast<float*>(ec + 16);
+    ef[0] = ux; ef[1] = uy; ef[2] = c1; ef[3] = s1; ef[4] = smax; ef[5] = ang ? 1.0f : 0.0f;
+    ec[12] = 0.0; ec[13] = 0.0; ec[14] = 0.0; ec[15] = 0.0;
+  }
+  __syncwarp();
+#endif
+#if !MPAP_EDGE_SMEM2
   double s = 0.0, c = 0.0, Sp = 0.0, Cp = 0.0;   // summary and its prefix maxima (NEXT-3)
+#endif
   for (int k0 = 0; k0 < K; k0 += 32) {
     const int nk = min(32, K - k0);
     const double ta = (double)k0 * Dl, tb = (double)(k0 + nk - 1) * Dl;
@@ -841,6 +912,11 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
         const float ey = fmaxf(fmaxf(fly - fy, fy - fhy), 0.0f);
         const float ez = (D == 3) ? fmaxf(fmaxf(flz - fz, fz - fhz), 0.0f) : 0.0f;
         keep = ex * ex + ey * ey + ez * ez <= mf2;
+#if MPAP_EDGE_SMEM2
+        const float* ef = reinterpret_cast<const float*>(ec + 16);
+        const float ux = ef[0], uy = ef[1], c1 = ef[2], s1 = ef[3], smax = ef[4];
+        const bool ang = ef[5] != 0.0f;
+#endif
         if (keep && ang) {
           const float dx = fx - ccx, dy = fy - ccy;
           const float dc2 = dx * dx + dy * dy;
@@ -1006,6 +1082,9 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
     }
     fold[lane] = inc;
     __syncwarp();
+#if MPAP_EDGE_SMEM2
+    double s = ec[12], c = ec[13], Sp = ec[14], Cp = ec[15];
+#endif
     if (P.edge_peaks) {
       for (int j = 0; j < nk; ++j) {   // fold in time order (every lane, same values)
         const double ij = fold[j];
@@ -1023,12 +1102,24 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
         s = s + ij;
       }
     }
+#if MPAP_EDGE_SMEM2
+    __syncwarp();
+    if (lane == 0) { ec[12] = s; ec[13] = c; ec[14] = Sp; ec[15] = Cp; }
+#endif
     __syncwarp();
   }
+#if MPAP_EDGE_SMEM2
+  __syncwarp();
+  s_out = ec[12];
+  c_out = ec[13];
+  S_out = ec[14];
+  C_out = ec[15];
+#else
   s_out = s;
   c_out = c;
   S_out = Sp;
   C_out = Cp;
+#endif
 #if MPAP_EDGE_SMEM
 #undef hu0
 #undef hu1
@@ -1072,7 +1163,7 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
   __shared__ unsigned s_work[kWarps][W_NUM];
   __shared__ double s_mlp[kMlpSize];
   __shared__ double s_fold[kWarps][32];
-  __shared__ double s_ec[kWarps][12];
+  __shared__ double s_ec[kWarps][20];
   for (int i = threadIdx.x; i < kMlpSize; i += blockDim.x) s_mlp[i] = P.mlp[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
