@@ -444,7 +444,7 @@ def mpap_prof_read(kernel: str) -> tuple:
     return float(ms.value), int(n.value)
 
 
-KERNELS = ("k_near", "k_scan", "k_collide", "k_heuristic", "k_search")
+KERNELS = ("k_near", "k_scan", "k_collide", "k_heuristic", "k_fold", "k_search")
 
 
 WORK_FIELDS = ["pairs", "prefilter_pass", "bisect_iters", "edges", "coll_segs", "coll_box_tests", "steps",

@@ -768,22 +768,21 @@ __device__ __forceinline__ void chunk_bbox(const double* su, const double* sv, c
   }
 }
 
-// Heuristic summary (s, c) of reading R10 for a collision-free edge.  Steps
-// are processed 32 at a time (one per lane).  Per chunk every lane computes
-// the chunk's bounding box and heading arc analytically; the warp culls the
-// features that can be visible from the chunk and the boxes that can occlude
-// a sight line into shared memory (ballot compaction); each lane then counts
-// the visible features of its step, and the per-step increments are folded in
-// time order from shared memory (every lane folds the same sequence).
+// Visible-feature counts of a collision-free edge (the k_v of P:324-328, per
+// step of reading R9).  Steps are processed 32 at a time (one per lane).  Per
+// chunk every lane computes the chunk's bounding box and heading arc
+// analytically; the warp culls the features that can be visible from the
+// chunk and the boxes that can occlude a sight line into shared memory
+// (ballot compaction); each lane then counts the visible features of its
+// step and stores the count in `kv_out[k]`.  The increments, the learned
+// heuristic and the ordered fold run in k_fold (one thread per edge).
 template <int D, int DYN, int HEUR>
-__device__ void edge_heuristic(const DevParams& P, const double* su, const double* sv, double T,
-                               const double* __restrict__ feat, int F, const double* __restrict__ box, int O,
-                               WarpLists<D>& L, double* fold, double* ec, int lane, double& s_out,
-                               double& c_out, double& S_out, double& C_out, Work& W) {
+__device__ void edge_visible(const DevParams& P, const double* su, const double* sv, double T,
+                             const double* __restrict__ feat, int F, const double* __restrict__ box, int O,
+                             WarpLists<D>& L, double* ec, int lane, uint16_t* __restrict__ kv_out, Work& W) {
   const double kk = ceil(T / P.dt);
   const int K = (kk < 1.0) ? 1 : (int)kk;
   const double Dl = T / (double)K;
-#if MPAP_EDGE_SMEM
   // per-edge trajectory constants live in the warp's shared scratch `ec`
   // (read per chunk / per step) instead of 4*D registers
   {
@@ -805,31 +804,11 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
   const double* c3 = ec + D;
   const double* r0 = ec + 2 * D;
   const double* r1 = ec + 3 * D;
-#else
-  double c2[D], c3[D], r0[D], r1[D];
-#pragma unroll
-  for (int j = 0; j < D; ++j) { c2[j] = 0.0; c3[j] = 0.0; r0[j] = -1.0; r1[j] = -1.0; }
-  if (DYN == 1) {
-    di_traj<D>(su, sv, T, c2, c3);
-    cubic_stationary<D>(su, c2, c3, r0, r1);
-  }
-#endif
   const int hoff = P.hoff;
-  double omega = 0.0;
-#if MPAP_EDGE_SMEM
 #define hu0 su[hoff]
 #define hu1 su[hoff + 1]
 #define hv0 sv[hoff]
 #define hv1 sv[hoff + 1]
-  if (P.has_heading) {
-#else
-  double hu0 = 0.0, hu1 = 0.0, hv0 = 0.0, hv1 = 0.0;
-  if (P.has_heading) {
-    hu0 = su[hoff]; hu1 = su[hoff + 1]; hv0 = sv[hoff]; hv1 = sv[hoff + 1];
-#endif
-    const double ex = hv0 - hu0, ey = hv1 - hu1;
-    omega = sqrt(ex * ex + ey * ey) / T;
-  }
   const double R = P.max_range;
   const double m = R + kCullMargin;
   const double R2 = R * R;
@@ -868,20 +847,6 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
       }
     }
   }
-#if MPAP_EDGE_SMEM2
-  // the bearing-cull constants are only read per chunk: keep them in the
-  // warp's scratch, not in registers across the step loop
-  __syncwarp();
-  if (lane == 0) {
-    float* ef = reinterpret_cast<float*>(ec + 16);
-    ef[0] = ux; ef[1] = uy; ef[2] = c1; ef[3] = s1; ef[4] = smax; ef[5] = ang ? 1.0f : 0.0f;
-    ec[12] = 0.0; ec[13] = 0.0; ec[14] = 0.0; ec[15] = 0.0;
-  }
-  __syncwarp();
-#endif
-#if !MPAP_EDGE_SMEM2
-  double s = 0.0, c = 0.0, Sp = 0.0, Cp = 0.0;   // summary and its prefix maxima (NEXT-3)
-#endif
   for (int k0 = 0; k0 < K; k0 += 32) {
     const int nk = min(32, K - k0);
     const double ta = (double)k0 * Dl, tb = (double)(k0 + nk - 1) * Dl;
@@ -912,11 +877,6 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
         const float ey = fmaxf(fmaxf(fly - fy, fy - fhy), 0.0f);
         const float ez = (D == 3) ? fmaxf(fmaxf(flz - fz, fz - fhz), 0.0f) : 0.0f;
         keep = ex * ex + ey * ey + ez * ez <= mf2;
-#if MPAP_EDGE_SMEM2
-        const float* ef = reinterpret_cast<const float*>(ec + 16);
-        const float ux = ef[0], uy = ef[1], c1 = ef[2], s1 = ef[3], smax = ef[4];
-        const bool ang = ef[5] != 0.0f;
-#endif
         if (keep && ang) {
           const float dx = fx - ccx, dy = fy - ccy;
           const float dc2 = dx * dx + dy * dy;
@@ -973,11 +933,9 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
     if (heur != 0) W.add(lane, W_FOV_TESTS, nk * nf);
     if (heur == 3) W.add(lane, W_MLP, nk);
     const int k = k0 + lane;
-    double inc = 0.0;
     if (k < K) {
       const double t = (double)k * Dl;
       double x[D], hv[D];
-      double speed = P.nominal_speed;   // |v(t)| for the MLP (kinematic: nominal)
 #pragma unroll
       for (int j = 0; j < D; ++j) hv[j] = 0.0;
       if (DYN == 0) {
@@ -989,19 +947,8 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
           for (int j = 0; j < D; ++j) hv[j] = sv[j] - su[j];
         }
       } else {
-        double vel[D];
         di_pos<D>(su, c2, c3, t, x);
-        di_vel<D>(su, c2, c3, t, vel);
-        if (heur == 3) {
-          double ss = 0.0;
-#pragma unroll
-          for (int j = 0; j < D; ++j) ss = fma(vel[j], vel[j], ss);
-          speed = sqrt(ss);
-        }
-        if (heur == 1) {
-#pragma unroll
-          for (int j = 0; j < D; ++j) hv[j] = vel[j];
-        }
+        if (heur == 1) di_vel<D>(su, c2, c3, t, hv);
       }
       if (heur >= 2) {
         const double sp = t / T;
@@ -1012,41 +959,6 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
 #pragma unroll
       for (int j = 0; j < D; ++j) hh = fma(hv[j], hv[j], hh);
       int kv = 0;
-#if MPAP_FEAT_TWO_PASS
-      // Two passes per 32 features: range + FOV for each (independent
-      // chains), then the occlusion test for the candidates.
-      for (int i0 = 0; i0 < nf; i0 += 32) {
-        const int ie = min(nf, i0 + 32);
-        unsigned cand = 0u;
-#pragma unroll kFeatUnroll
-        for (int i = i0; i < ie; ++i) {
-          double dl[D];
-          double dd = 0.0;
-#pragma unroll
-          for (int j = 0; j < D; ++j) { dl[j] = L.f[j][i] - x[j]; dd = fma(dl[j], dl[j], dd); }
-          bool ok = !(dd > R2);
-          if (heur != 0) {
-            double dot = 0.0;
-#pragma unroll
-            for (int j = 0; j < D; ++j) dot = fma(hv[j], dl[j], dot);
-            ok = ok && (hh > 0.0) && !(dot < 0.0) && !(dot * dot < cos2 * (hh * dd));
-          }
-          cand |= (ok ? 1u : 0u) << (i - i0);
-        }
-        while (cand) {
-          const int i = i0 + __ffs(cand) - 1;
-          cand &= cand - 1u;
-          double fp[D], dl[D];
-#pragma unroll
-          for (int j = 0; j < D; ++j) { fp[j] = L.f[j][i]; dl[j] = fp[j] - x[j]; }
-          ++W.occl_segs;
-          const unsigned rr = use_mask ? seg_hits_boxes<D, true>(x, fp, dl, L.box, nb, L.fmask[i])
-                                       : seg_hits_boxes<D, false>(x, fp, dl, L.box, nb, 0ull);
-          W.occl_tests += rr >> 1;
-          if (!(rr & 1u)) ++kv;
-        }
-      }
-#else
       for (int i = 0; i < nf; ++i) {
         double dl[D];
         double dd = 0.0;
@@ -1070,62 +982,14 @@ __device__ void edge_heuristic(const DevParams& P, const double* su, const doubl
         W.occl_tests += rr >> 1;
         if (!(rr & 1u)) ++kv;
       }
-#endif
-      inc = Dl - (double)kv * (Dl / P.n_f);
-      if (heur == 3) {
-        const double z0 = speed / P.v_ref;
-        const double z1 = omega / P.w_ref;
-        const double z2 = (double)kv / P.n_f;
-        const double o = mlp_out0(L.mlp, z0, z1, z2);
-        inc = inc + Dl * (P.mlp_gain * o);
-      }
+      kv_out[k] = (uint16_t)kv;
     }
-    fold[lane] = inc;
-    __syncwarp();
-#if MPAP_EDGE_SMEM2
-    double s = ec[12], c = ec[13], Sp = ec[14], Cp = ec[15];
-#endif
-    if (P.edge_peaks) {
-      for (int j = 0; j < nk; ++j) {   // fold in time order (every lane, same values)
-        const double ij = fold[j];
-        const double tt = c + ij;
-        c = (tt > 0.0) ? tt : 0.0;
-        s = s + ij;
-        Sp = (s > Sp) ? s : Sp;        // running maxima of the prefix values (NEXT-3)
-        Cp = (c > Cp) ? c : Cp;
-      }
-    } else {
-      for (int j = 0; j < nk; ++j) {
-        const double ij = fold[j];
-        const double tt = c + ij;
-        c = (tt > 0.0) ? tt : 0.0;
-        s = s + ij;
-      }
-    }
-#if MPAP_EDGE_SMEM2
-    __syncwarp();
-    if (lane == 0) { ec[12] = s; ec[13] = c; ec[14] = Sp; ec[15] = Cp; }
-#endif
     __syncwarp();
   }
-#if MPAP_EDGE_SMEM2
-  __syncwarp();
-  s_out = ec[12];
-  c_out = ec[13];
-  S_out = ec[14];
-  C_out = ec[15];
-#else
-  s_out = s;
-  c_out = c;
-  S_out = Sp;
-  C_out = Cp;
-#endif
-#if MPAP_EDGE_SMEM
 #undef hu0
 #undef hu1
 #undef hv0
 #undef hv1
-#endif
 }
 
 // Persistent: each warp pulls work items from an atomic counter, so no block
@@ -1152,6 +1016,10 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
                                                           const int64_t* __restrict__ row_ptr,
                                                           EdgeRec* __restrict__ edges,
                                                           double* __restrict__ tau_arr,
+                                                          int32_t* __restrict__ esrc,
+                                                          long long* __restrict__ koff,
+                                                          uint16_t* __restrict__ kvbuf,
+                                                          unsigned long long* __restrict__ kv_total,
                                                           float2* __restrict__ peak,
                                                           const longlong2* __restrict__ items, int64_t n_items,
                                                           unsigned long long* __restrict__ nnz_free,
@@ -1162,8 +1030,7 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
   __shared__ double s_state[kWarps][2][NS];
   __shared__ unsigned s_work[kWarps][W_NUM];
   __shared__ double s_mlp[kMlpSize];
-  __shared__ double s_fold[kWarps][32];
-  __shared__ double s_ec[kWarps][20];
+  __shared__ double s_ec[kWarps][12];
   for (int i = threadIdx.x; i < kMlpSize; i += blockDim.x) s_mlp[i] = P.mlp[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1216,6 +1083,7 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
     __syncwarp();
     if (lane < NS) su[lane] = (lane < stride) ? envs[u * stride + lane] : 0.0;
     int nfree = 0;
+    long long kv_local = 0;   // PHASE 0: kv slots of the row's free edges (multiples of 8)
     for (int64_t e = e_begin; e < e_end; ++e) {
       if constexpr (PHASE == 0) {
         int v;
@@ -1247,8 +1115,21 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
           er.s = 0.0f;
           er.c = 0.0f;
           edges[e] = er;
-          if (!items) tau_arr[e] = tau;
+          if (!items) {
+            tau_arr[e] = tau;
+            esrc[e] = (int32_t)row;
+          }
           if (peak) peak[e] = make_float2(0.0f, 0.0f);
+          if (!coll) {   // kv slots for k_heuristic / k_fold: K steps rounded up to 8
+            const double kk = ceil(tau / P.dt);
+            const long long K8 = (((kk < 1.0) ? 1 : (long long)kk) + 7) & ~7ll;
+            if (items) {
+              koff[e] = (long long)atomicAdd(kv_total, (unsigned long long)K8);
+            } else {
+              koff[e] = kv_local;
+              kv_local += K8;
+            }
+          }
         }
       } else {
         const uint32_t dc = edges[e].dst_coll;
@@ -1257,17 +1138,21 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
         __syncwarp();
         if (lane < NS) sv[lane] = (lane < stride) ? envs[(int64_t)(dc & 0x7fffffffu) * stride + lane] : 0.0;
         __syncwarp();
-        double s64, c64, S64, C64;
-        edge_heuristic<D, DYN, HEUR>(P, su, sv, tau, efeat, F, ebox, O, L, s_fold[warp], s_ec[warp], lane, s64,
-                                     c64, S64, C64, W);
+        edge_visible<D, DYN, HEUR>(P, su, sv, tau, efeat, F, ebox, O, L, s_ec[warp], lane, kvbuf + koff[e], W);
         W.flush(lane);
-        if (lane == 0) {
-          *reinterpret_cast<float2*>(&edges[e].s) = make_float2((float)s64, (float)c64);
-          if (peak) peak[e] = make_float2((float)S64, (float)C64);
-        }
       }
     }
     if (PHASE == 0) {
+      if (!items) {   // one atomic per row, then rebase the row's offsets
+        long long base = 0;
+        if (lane == 0 && kv_local) base = (long long)atomicAdd(kv_total, (unsigned long long)kv_local);
+        base = __shfl_sync(FULL, base, 0);
+        kv_local = __shfl_sync(FULL, kv_local, 0);
+        __syncwarp();   // lane 0's koff / edge stores are visible to the warp
+        if (kv_local)
+          for (int64_t e = e_begin + lane; e < e_end; e += 32)
+            if (!(edges[e].dst_coll >> 31)) koff[e] += base;
+      }
       W.add(lane, W_EDGES, (unsigned)(e_end - e_begin));
       if (!items) W.add(lane, W_FREE_EDGES, nfree);
       if (lane == 0 && nfree) atomicAdd(&nnz_free[b], (unsigned long long)(long long)nfree);
@@ -1275,6 +1160,96 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
   }
   __syncwarp();
   if (lane >= W_EDGES && lane < W_NUM && W.sm[lane]) atomicAdd(&work[lane], (unsigned long long)W.sm[lane]);
+}
+
+
+// Increments and ordered fold (reading R10) of every collision-free edge, one
+// thread per edge, from the per-step visible counts k_v written by
+// k_heuristic: inc_k = Dl - k_v (Dl / n_f), plus Dl * gamma * o_k
+// for the learned heuristic (o_k = MLP(|v(t_k)| / v_ref, omega / w_ref,
+// k_v / n_f), reading R12); then c <- max(0, c + inc_k), s <- s + inc_k in
+// step order (and the running maxima S, C of NEXT-3).  The same operations in
+// the same order as the per-step definition.
+constexpr int kFoldThreads = 256;
+
+template <int D, int DYN, int HEUR>
+__global__ void __launch_bounds__(kFoldThreads) k_fold(const double* __restrict__ samples,
+                                                      const int64_t* __restrict__ node_base, int B, DevParams P,
+                                                      const int32_t* __restrict__ esrc,
+                                                      const double* __restrict__ tau_arr,
+                                                      const long long* __restrict__ koff,
+                                                      const uint16_t* __restrict__ kvbuf,
+                                                      EdgeRec* __restrict__ edges, float2* __restrict__ peak,
+                                                      const longlong2* __restrict__ items, int64_t n) {
+  __shared__ double s_mlp[kMlpSize];
+  if (HEUR == 3)
+    for (int i = threadIdx.x; i < kMlpSize; i += blockDim.x) s_mlp[i] = P.mlp[i];
+  __syncthreads();
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  const int64_t e = items ? items[idx].y : idx;
+  const uint32_t dc = edges[e].dst_coll;
+  if (dc >> 31) return;   // colliding: s = c = 0
+  const int64_t row = esrc[e];
+  int lo_b = 0, hi_b = B;   // env = last b with node_base[b] <= row
+  while (hi_b - lo_b > 1) {
+    const int mid = (lo_b + hi_b) >> 1;
+    if (node_base[mid] <= row) lo_b = mid; else hi_b = mid;
+  }
+  const int stride = P.stride;
+  const double* envs = samples + node_base[lo_b] * stride;
+  const double* su = envs + (row - node_base[lo_b]) * stride;
+  const double* sv = envs + (int64_t)(dc & 0x7fffffffu) * stride;
+  const double T = tau_arr[e];
+  const double kk = ceil(T / P.dt);
+  const int K = (kk < 1.0) ? 1 : (int)kk;
+  const double Dl = T / (double)K;
+  double omega = 0.0;
+  double su_l[2 * D], sv_l[2 * D];
+#pragma unroll
+  for (int j = 0; j < 2 * D; ++j) {
+    su_l[j] = (DYN == 1 || j < D) ? su[j] : 0.0;
+    sv_l[j] = (DYN == 1 || j < D) ? sv[j] : 0.0;
+  }
+  if (HEUR == 3 && P.has_heading) {
+    const double ex = sv[P.hoff] - su[P.hoff], ey = sv[P.hoff + 1] - su[P.hoff + 1];
+    omega = sqrt(ex * ex + ey * ey) / T;
+  }
+  double c2[D], c3[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) { c2[j] = 0.0; c3[j] = 0.0; }
+  if (HEUR == 3 && DYN == 1) di_traj<D>(su_l, sv_l, T, c2, c3);
+  const uint16_t* kvp = kvbuf + koff[e];
+  const double q = Dl / P.n_f;
+  double s = 0.0, c = 0.0, Sp = 0.0, Cp = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const int kv = kvp[k];
+    double inc = Dl - (double)kv * q;
+    if (HEUR == 3) {
+      double speed = P.nominal_speed;   // |v(t)| for the MLP (kinematic: nominal)
+      if (DYN == 1) {
+        const double t = (double)k * Dl;
+        double vel[D];
+        di_vel<D>(su_l, c2, c3, t, vel);
+        double ss = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) ss = fma(vel[j], vel[j], ss);
+        speed = sqrt(ss);
+      }
+      const double z0 = speed / P.v_ref;
+      const double z1 = omega / P.w_ref;
+      const double z2 = (double)kv / P.n_f;
+      const double o = mlp_out0(s_mlp, z0, z1, z2);
+      inc = inc + Dl * (P.mlp_gain * o);
+    }
+    const double tt = c + inc;
+    c = (tt > 0.0) ? tt : 0.0;
+    s = s + inc;
+    Sp = (s > Sp) ? s : Sp;   // running maxima of the prefix values (NEXT-3)
+    Cp = (c > Cp) ? c : Cp;
+  }
+  *reinterpret_cast<float2*>(&edges[e].s) = make_float2((float)s, (float)c);
+  if (peak) peak[e] = make_float2((float)Sp, (float)Cp);
 }
 
 // NEXT-1: edges of one environment whose collision bit or
@@ -1402,7 +1377,10 @@ struct EdgeWork {            // what one k_edges launch processes
   int64_t n_items;
   unsigned long long* nnz_free;
   unsigned long long* work;
-  unsigned long long* next;  // item counter (zeroed)
+  unsigned long long* next;  // item counters (zeroed), one per phase
+  long long* koff;           // per-edge offsets into kvbuf
+  uint16_t* kvbuf;           // per-step visible counts (phase 1 output)
+  unsigned long long* kv_total;
 };
 
 template <int D, int DYN, int PHASE, int HEUR>
@@ -1421,8 +1399,9 @@ cudaError_t launch_edges_phase(size_t smem, cudaStream_t st, const mpap_roadmap*
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(per_sm, 1), need));
   kern<<<grid, kWarps * 32, smem, st>>>(rm->d_samples, rm->d_node_base, rm->B, rm->d_obst, rm->d_obst_base,
                                         rm->d_feat, rm->d_feat_base, rm->prm, ew.cap, rm->o_max, rm->f_max,
-                                        ew.scratch, rm->d_row_ptr, rm->d_edges, rm->d_tau, rm->d_peak, ew.items,
-                                        ew.n_items, ew.nnz_free, ew.work, ew.next);
+                                        ew.scratch, rm->d_row_ptr, rm->d_edges, rm->d_tau, rm->d_esrc, ew.koff,
+                                        ew.kvbuf, ew.kv_total, rm->d_peak, ew.items, ew.n_items, ew.nnz_free,
+                                        ew.work, ew.next);
   return cudaGetLastError();
 }
 
@@ -1442,6 +1421,58 @@ cudaError_t launch_edges_any(int phase, size_t smem, cudaStream_t st, const mpap
   const int d = rm->prm.pos_dim, dyn = rm->prm.dynamics;
   if (d == 2) return dyn ? launch_edges<2, 1>(phase, smem, st, rm, ew) : launch_edges<2, 0>(phase, smem, st, rm, ew);
   return dyn ? launch_edges<3, 1>(phase, smem, st, rm, ew) : launch_edges<3, 0>(phase, smem, st, rm, ew);
+}
+
+template <int D, int DYN>
+cudaError_t launch_fold_dd(cudaStream_t st, const mpap_roadmap* rm, const EdgeWork& ew) {
+  const int64_t n = ew.items ? ew.n_items : rm->nnz_total;
+  if (n == 0) return cudaSuccess;
+  const dim3 grid((unsigned)((n + kFoldThreads - 1) / kFoldThreads));
+#define MPAP_FOLD_ARGS rm->d_samples, rm->d_node_base, rm->B, rm->prm, rm->d_esrc, rm->d_tau, ew.koff, ew.kvbuf, \
+    rm->d_edges, rm->d_peak, ew.items, n
+  switch (rm->prm.heuristic) {
+    case 3: k_fold<D, DYN, 3><<<grid, kFoldThreads, 0, st>>>(MPAP_FOLD_ARGS); break;
+    default: k_fold<D, DYN, 0><<<grid, kFoldThreads, 0, st>>>(MPAP_FOLD_ARGS); break;
+  }
+#undef MPAP_FOLD_ARGS
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fold(cudaStream_t st, const mpap_roadmap* rm, const EdgeWork& ew) {
+  const int d = rm->prm.pos_dim, dyn = rm->prm.dynamics;
+  if (d == 2) return dyn ? launch_fold_dd<2, 1>(st, rm, ew) : launch_fold_dd<2, 0>(st, rm, ew);
+  return dyn ? launch_fold_dd<3, 1>(st, rm, ew) : launch_fold_dd<3, 0>(st, rm, ew);
+}
+
+size_t edges_smem(const mpap_roadmap* rm);
+
+// collide (+ kv slot offsets) -> size the kv buffer -> visible counts -> fold
+cudaError_t edge_phases(size_t smem, cudaStream_t st, const mpap_roadmap* rm, EdgeWork ew) {
+  {
+    ProfScope ps("k_collide", st);
+    cudaError_t e = launch_edges_any(0, smem, st, rm, ew);
+    if (e != cudaSuccess) return e;
+  }
+  note_launch();
+  unsigned long long total = 0;
+  cudaError_t e = cudaMemcpyAsync(&total, ew.kv_total, sizeof(total), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return e;
+  ew.kvbuf = static_cast<uint16_t*>(workspace(st, WS_KV, sizeof(uint16_t) * std::max<unsigned long long>(total, 8)));
+  if (!ew.kvbuf) return cudaErrorMemoryAllocation;
+  {
+    ProfScope ps("k_heuristic", st);
+    e = launch_edges_any(1, smem, st, rm, ew);
+    if (e != cudaSuccess) return e;
+  }
+  note_launch();
+  {
+    ProfScope ps("k_fold", st);
+    e = launch_fold(st, rm, ew);
+    if (e != cudaSuccess) return e;
+  }
+  note_launch();
+  return cudaSuccess;
 }
 
 size_t edges_smem(const mpap_roadmap* rm) {
@@ -1527,17 +1558,17 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
   }
   rm->d_tau = static_cast<double*>(rm_alloc(sizeof(double) * std::max<int64_t>(rm->nnz_total, 1), st));
   if (!rm->d_tau) return set_error(MPAP_ERR_OUT_OF_MEMORY, "tau array allocation failed");
+  rm->d_esrc = static_cast<int32_t*>(rm_alloc(sizeof(int32_t) * std::max<int64_t>(rm->nnz_total, 1), st));
+  if (!rm->d_esrc) return set_error(MPAP_ERR_OUT_OF_MEMORY, "edge source array allocation failed");
   const size_t smem = edges_smem(rm);
-  unsigned long long* d_next = nullptr;
-  CK(cudaMallocAsync(&d_next, 2 * sizeof(unsigned long long), st));
-  CK(cudaMemsetAsync(d_next, 0, 2 * sizeof(unsigned long long), st));
+  unsigned long long* d_next = nullptr;   // [0..1] item counters of the two edge phases, [2] kv slots
+  CK(cudaMallocAsync(&d_next, 3 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(d_next, 0, 3 * sizeof(unsigned long long), st));
   if (rm->nnz_total > 0) {
-    for (int phase = 0; phase < 2; ++phase) {
-      ProfScope ps(phase == 0 ? "k_collide" : "k_heuristic", st);
-      const EdgeWork ew{d_scr, cap, nullptr, 0, d_free, d_work, d_next};
-      CK(launch_edges_any(phase, smem, st, rm, ew));
-      note_launch();
-    }
+    EdgeWork ew{d_scr, cap, nullptr, 0, d_free, d_work, d_next, nullptr, nullptr, d_next + 2};
+    ew.koff = static_cast<long long*>(workspace(st, WS_KOFF, sizeof(long long) * rm->nnz_total));
+    if (!ew.koff) return set_error(MPAP_ERR_OUT_OF_MEMORY, "kv offset workspace allocation failed");
+    CK(edge_phases(smem, st, rm, ew));
   }
   std::vector<unsigned long long> fr(B);
   CK(cudaMemcpyAsync(fr.data(), d_free, sizeof(unsigned long long) * B, cudaMemcpyDeviceToHost, st));
@@ -1573,7 +1604,7 @@ mpap_status update_roadmap_device(mpap_roadmap* rm, int env, const std::vector<d
   double* d_cb = nullptr;
   double* d_cf = nullptr;
   longlong2* d_items = nullptr;
-  unsigned long long* d_ctr = nullptr;   // [0] n_items, [1..2] item counters, [3] free delta, [4..] work
+  unsigned long long* d_ctr = nullptr;   // [0] n_items, [1..2] item counters, [3] kv slots, [4..] work
   CK(cudaMallocAsync(&d_cb, sizeof(double) * std::max<size_t>(cbox.size(), 1), st));
   CK(cudaMallocAsync(&d_cf, sizeof(double) * std::max<size_t>(cfeat.size(), 1), st));
   if (nb) CK(cudaMemcpyAsync(d_cb, cbox.data(), sizeof(double) * cbox.size(), cudaMemcpyHostToDevice, st));
@@ -1617,12 +1648,11 @@ mpap_status update_roadmap_device(mpap_roadmap* rm, int env, const std::vector<d
     CK(cudaMallocAsync(&d_free, sizeof(unsigned long long) * rm->B, st));
     CK(cudaMemsetAsync(d_free, 0, sizeof(unsigned long long) * rm->B, st));
     const size_t smem = edges_smem(rm);
-    for (int phase = 0; phase < 2; ++phase) {
-      ProfScope ps(phase == 0 ? "k_collide" : "k_heuristic", st);
-      const EdgeWork ew{nullptr, 0, d_items, (int64_t)n_items, d_free, d_ctr + 4 - W_EDGES, d_ctr + 1};
-      CK(launch_edges_any(phase, smem, st, rm, ew));
-      note_launch();
-    }
+    EdgeWork ew{nullptr, 0, d_items, (int64_t)n_items, d_free, d_ctr + 4 - W_EDGES, d_ctr + 1, nullptr, nullptr,
+                d_ctr + 3};
+    ew.koff = static_cast<long long*>(workspace(st, WS_KOFF, sizeof(long long) * rm->nnz_total));
+    if (!ew.koff) return set_error(MPAP_ERR_OUT_OF_MEMORY, "kv offset workspace allocation failed");
+    CK(edge_phases(smem, st, rm, ew));
     unsigned long long delta = 0;
     CK(cudaMemcpyAsync(&delta, d_free + env, sizeof(delta), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

@@ -311,7 +311,7 @@ void mpap_roadmap_free(mpap_roadmap* rm) {
   // wait for the device, then hand the memory back to the stream-ordered pool
   cudaDeviceSynchronize();
   void* ptrs[] = {rm->d_samples, rm->d_obst, rm->d_feat, rm->d_obst_base, rm->d_feat_base, rm->d_node_base,
-                  rm->d_row_ptr, rm->d_edges, rm->d_peak, rm->d_tau};
+                  rm->d_row_ptr, rm->d_edges, rm->d_peak, rm->d_tau, rm->d_esrc};
   for (void* p : ptrs) rm_release(p);   // device is idle: safe to reuse from any stream
   cudaSetDevice(cur);
   delete rm;

@@ -67,6 +67,7 @@ struct mpap_roadmap {
   int64_t* d_row_ptr = nullptr;    // [sum n + 1] global edge offsets
   mpap::EdgeRec* d_edges = nullptr;
   double* d_tau = nullptr;         // [nnz_total] edge durations (NEXT-1 updates re-evaluate edges from it)
+  int32_t* d_esrc = nullptr;       // [nnz_total] global source row of each edge (k_fold)
   float2* d_peak = nullptr;        // [nnz_total] (S, C) prefix maxima per edge (NEXT-3); may be null (import)
   int64_t nnz_total = 0;
   unsigned long long work[mpap::kWorkCounters] = {};  // build work counters (mpap_roadmap_work)
@@ -113,7 +114,7 @@ void retain_pool_memory(int device);
 // on one stream reuse it (stream order serialises them); other streams get
 // their own.  Returns nullptr on allocation failure.
 void* workspace(cudaStream_t st, int tag, size_t bytes);
-enum { WS_NEAR = 0, WS_SEARCH = 1 };
+enum { WS_NEAR = 0, WS_SEARCH = 1, WS_KOFF = 2, WS_KV = 3 };
 // Device buffer cache for roadmap arrays (capi.cu).  Roadmaps are built and
 // freed every step of a batched pipeline with the same sizes; growing the
 // stream-ordered pool for them stalled the host for up to 0.5 s per call
