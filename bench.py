@@ -365,18 +365,25 @@ def main():
     return 0
 
 
-# Algorithmic FP64 operations per counted unit (+, -, *, /, sqrt each = 1),
-# read off the kernels' source.  D = 3, double integrator,
-# heading + MLP heuristic (the C5 workload).
+# Algorithmic FP64 operations per counted unit (+, -, *, /, sqrt, min/max,
+# compare and FMA each = 1), read off the kernels' source.
+# D = 3, double integrator, heading + MLP heuristic (the C5 workload).
 def fp64_ops(kernel: str, w: dict, D: int = 3) -> float:
     if kernel == "k_near":
         return 18 * w["pairs"] + 101 * w["prefilter_pass"] + 9 * w["bisect_iters"]
     if kernel == "k_collide":
         return (12 * D + 2 * D + 4) * w["coll_segs"] + 4 * D * w["coll_box_tests"] + 27 * w["edges"]
     if kernel == "k_heuristic":
-        per_step = 1 + 12 * D + 8 + 2 * D + 6
-        return (per_step * w["steps"] + 205 * w["mlp"] + 3 * D * w["range_tests"] + (2 * D + 3) * w["fov_tests"]
-                + D * w["occl_segs"] + 4 * D * w["occl_box_tests"] + 40 * w["free_edges"])
+        # per step: t, position (3 per axis), heading interpolation (2 x 3 + 1), |h|^2 (D);
+        # range test 2D + 1, FOV test 2D + 3, occlusion segment 6D (dl, 1/dl, segment box),
+        # slab box test 4D; per free edge 40 (trajectory, stationary points, arc)
+        per_step = 1 + 3 * D + 7 + D
+        return (per_step * w["steps"] + (2 * D + 1) * w["range_tests"] + (2 * D + 3) * w["fov_tests"]
+                + 6 * D * w["occl_segs"] + 4 * D * w["occl_box_tests"] + 40 * w["free_edges"])
+    if kernel == "k_fold":
+        # per step: increment 2, MLP 3-8-8-1 with ReLUs 128, speed (t, velocity 3D, |v|^2 D, sqrt) 14,
+        # inputs 3 divisions, learned term 2, fold with running maxima 5; per free edge 36
+        return (2 + 128 + 14 + 3 + 2 + 5) * w["steps"] + 36 * w["free_edges"]
     return 0.0
 
 

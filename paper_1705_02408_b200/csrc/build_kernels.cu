@@ -35,27 +35,8 @@
 namespace mpap {
 
 #define FULL 0xffffffffu
-#ifndef MPAP_EDGE_SMEM
-#define MPAP_EDGE_SMEM 1
-#endif
-#ifndef MPAP_NEAR_HIER
-#define MPAP_NEAR_HIER 1
-#endif
-#ifndef MPAP_SEG_INLINE_BB
-#define MPAP_SEG_INLINE_BB 0
-#endif
-#ifndef MPAP_EDGE_SMEM2
-#define MPAP_EDGE_SMEM2 0
-#endif
-#ifndef MPAP_FEAT_TWO_PASS
-#define MPAP_FEAT_TWO_PASS 0
-#endif
-#ifndef MPAP_FEAT_UNROLL
-#define MPAP_FEAT_UNROLL 1
-#endif
-constexpr int kFeatUnroll = MPAP_FEAT_UNROLL;
-#ifndef MPAP_LAZY_INV
-#define MPAP_LAZY_INV 0
+#ifndef MPAP_FOLD_MIN_BLOCKS
+#define MPAP_FOLD_MIN_BLOCKS 4
 #endif
 #ifndef MPAP_EDGES_MIN_BLOCKS
 #define MPAP_EDGES_MIN_BLOCKS 4
@@ -66,7 +47,6 @@ constexpr int kFeatUnroll = MPAP_FEAT_UNROLL;
 constexpr int kWarps = MPAP_KWARPS;       // warps per block of the edge kernels
 constexpr int kNearWarps = 8;             // warps per block of k_near
 constexpr double kCullMargin = 1e-6;      // absolute; >> rounding of O(100) coordinates
-constexpr int kNearIntervals = 16;        // level-2 neighbour filter resolution
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -243,7 +223,6 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_near(const double* __restri
                                                       unsigned long long* __restrict__ work) {
   constexpr int NS = DYN ? 2 * D : D;   // state doubles used by the cost
   __shared__ int queue[kNearWarps][64];
-#if MPAP_NEAR_HIER
   // interval tables of the level-2 filter: [level][interval] = {ta, tb, 1/tb, 1/tb^3}
   // for the whole range (level 0), quarters (1) and sixteenths (2) of (0, r]
   __shared__ double s_near[3][16][4];
@@ -260,7 +239,6 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_near(const double* __restri
     s_near[lvl][jj][3] = 1.0 / (tb * tb * tb);
   }
   __syncthreads();
-#endif
   const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = n_env[b];
@@ -361,7 +339,6 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_near(const double* __restri
             as += a * e;
           }
           const double tv = (ss > 0.0) ? 2.0 * as / ss : 0.0;   // vertex of the quadratic
-#if MPAP_NEAR_HIER
           // Lower bound of c on [ta, tb] (reciprocals of tb from the block's
           // table): tested on [0, r], then on its 4 quarters, then on the 4
           // sixteenths of each quarter that is still possible.
@@ -379,17 +356,6 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_near(const double* __restri
               for (int jj = 4 * q; jj < 4 * q + 4 && !possible; ++jj) possible = possible_on(2, jj);
             }
           }
-#else
-          bool possible = false;
-          for (int jj = 0; jj < kNearIntervals && !possible; ++jj) {
-            const double ta = r * (double)jj / (double)kNearIntervals;
-            const double tb = r * (double)(jj + 1) / (double)kNearIntervals;
-            const double tq = fmin(fmax(tv, ta), tb);
-            const double g2 = fmax(dp2 - tq * as + tq * tq * ss * 0.25, 0.0);
-            const double L = ta + ru * (12.0 * g2 / (tb * tb * tb) + dv2 / tb);
-            possible = L * (1.0 - 1e-9) < r;
-          }
-#endif
           pf = possible;
         }
       }
@@ -547,20 +513,13 @@ __device__ int cull_boxes(const double* __restrict__ box, int O, const double* l
 template <int D, bool USE_MASK>
 __device__ __forceinline__ unsigned seg_hits_boxes(const double* A, const double* B, const double* Dv,
                                                    const double* bl, int nl, unsigned long long mask) {
-#if MPAP_SEG_INLINE_BB
-  double inv[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) inv[k] = (!MPAP_LAZY_INV && Dv[k] != 0.0) ? __drcp_rn(Dv[k]) : 0.0;   // == 1.0 / Dv[k]
-#else
   double inv[D], slo[D], shi[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    inv[k] = (!MPAP_LAZY_INV && Dv[k] != 0.0) ? __drcp_rn(Dv[k]) : 0.0;   // == 1.0 / Dv[k]
+    inv[k] = (Dv[k] != 0.0) ? __drcp_rn(Dv[k]) : 0.0;   // == 1.0 / Dv[k]
     slo[k] = fmin(A[k], B[k]) - kCullMargin;
     shi[k] = fmax(A[k], B[k]) + kCullMargin;
   }
-#endif
-  bool have_inv = !MPAP_LAZY_INV;   // reciprocals formed only if some box survives the prefilter
   unsigned tests = 0;
   int i = -1;
   for (;;) {
@@ -575,18 +534,9 @@ __device__ __forceinline__ unsigned seg_hits_boxes(const double* A, const double
     bool sep = false;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-#if MPAP_SEG_INLINE_BB
-      if (bx[k] > fmax(A[k], B[k]) + kCullMargin || bx[D + k] < fmin(A[k], B[k]) - kCullMargin) sep = true;
-#else
       if (bx[k] > shi[k] || bx[D + k] < slo[k]) sep = true;
-#endif
     }
     if (sep) continue;
-    if (!have_inv) {
-#pragma unroll
-      for (int k = 0; k < D; ++k) inv[k] = (Dv[k] != 0.0) ? __drcp_rn(Dv[k]) : 0.0;
-      have_inv = true;
-    }
     ++tests;
     double t0 = 0.0, t1 = 1.0;
     bool hit = true;
@@ -1020,6 +970,8 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
                                                           long long* __restrict__ koff,
                                                           uint16_t* __restrict__ kvbuf,
                                                           unsigned long long* __restrict__ kv_total,
+                                                          longlong2* __restrict__ flist,
+                                                          unsigned long long* __restrict__ fcount,
                                                           float2* __restrict__ peak,
                                                           const longlong2* __restrict__ items, int64_t n_items,
                                                           unsigned long long* __restrict__ nnz_free,
@@ -1149,9 +1101,19 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
         base = __shfl_sync(FULL, base, 0);
         kv_local = __shfl_sync(FULL, kv_local, 0);
         __syncwarp();   // lane 0's koff / edge stores are visible to the warp
-        if (kv_local)
-          for (int64_t e = e_begin + lane; e < e_end; e += 32)
-            if (!(edges[e].dst_coll >> 31)) koff[e] += base;
+        // the row's free edges, in order, into the free list (k_fold's work)
+        unsigned long long fbase = 0;
+        if (lane == 0 && nfree) fbase = atomicAdd(fcount, (unsigned long long)nfree);
+        fbase = __shfl_sync(FULL, fbase, 0);
+        int fr = 0;
+        for (int64_t e0 = e_begin; e0 < e_end; e0 += 32) {
+          const int64_t e = e0 + lane;
+          const bool fe = (e < e_end) && !(edges[e].dst_coll >> 31);
+          if (fe) koff[e] += base;
+          const unsigned fm = __ballot_sync(FULL, fe);
+          if (fe) flist[fbase + fr + __popc(fm & lanemask_lt())] = make_longlong2(row, e);
+          fr += __popc(fm);
+        }
       }
       W.add(lane, W_EDGES, (unsigned)(e_end - e_begin));
       if (!items) W.add(lane, W_FREE_EDGES, nfree);
@@ -1173,7 +1135,7 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
 constexpr int kFoldThreads = 256;
 
 template <int D, int DYN, int HEUR>
-__global__ void __launch_bounds__(kFoldThreads) k_fold(const double* __restrict__ samples,
+__global__ void __launch_bounds__(kFoldThreads, MPAP_FOLD_MIN_BLOCKS) k_fold(const double* __restrict__ samples,
                                                       const int64_t* __restrict__ node_base, int B, DevParams P,
                                                       const int32_t* __restrict__ esrc,
                                                       const double* __restrict__ tau_arr,
@@ -1381,6 +1343,8 @@ struct EdgeWork {            // what one k_edges launch processes
   long long* koff;           // per-edge offsets into kvbuf
   uint16_t* kvbuf;           // per-step visible counts (phase 1 output)
   unsigned long long* kv_total;
+  longlong2* flist;          // build mode: free edges {row, edge} (k_fold's items)
+  unsigned long long* fcount;
 };
 
 template <int D, int DYN, int PHASE, int HEUR>
@@ -1400,8 +1364,8 @@ cudaError_t launch_edges_phase(size_t smem, cudaStream_t st, const mpap_roadmap*
   kern<<<grid, kWarps * 32, smem, st>>>(rm->d_samples, rm->d_node_base, rm->B, rm->d_obst, rm->d_obst_base,
                                         rm->d_feat, rm->d_feat_base, rm->prm, ew.cap, rm->o_max, rm->f_max,
                                         ew.scratch, rm->d_row_ptr, rm->d_edges, rm->d_tau, rm->d_esrc, ew.koff,
-                                        ew.kvbuf, ew.kv_total, rm->d_peak, ew.items, ew.n_items, ew.nnz_free,
-                                        ew.work, ew.next);
+                                        ew.kvbuf, ew.kv_total, ew.flist, ew.fcount, rm->d_peak, ew.items,
+                                        ew.n_items, ew.nnz_free, ew.work, ew.next);
   return cudaGetLastError();
 }
 
@@ -1454,8 +1418,9 @@ cudaError_t edge_phases(size_t smem, cudaStream_t st, const mpap_roadmap* rm, Ed
     if (e != cudaSuccess) return e;
   }
   note_launch();
-  unsigned long long total = 0;
+  unsigned long long total = 0, nfree = 0;
   cudaError_t e = cudaMemcpyAsync(&total, ew.kv_total, sizeof(total), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && !ew.items) e = cudaMemcpyAsync(&nfree, ew.fcount, sizeof(nfree), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return e;
   ew.kvbuf = static_cast<uint16_t*>(workspace(st, WS_KV, sizeof(uint16_t) * std::max<unsigned long long>(total, 8)));
@@ -1468,7 +1433,12 @@ cudaError_t edge_phases(size_t smem, cudaStream_t st, const mpap_roadmap* rm, Ed
   note_launch();
   {
     ProfScope ps("k_fold", st);
-    e = launch_fold(st, rm, ew);
+    EdgeWork fw = ew;
+    if (!ew.items) {   // build: the free-edge list written by k_collide
+      fw.items = ew.flist;
+      fw.n_items = (int64_t)nfree;
+    }
+    e = launch_fold(st, rm, fw);
     if (e != cudaSuccess) return e;
   }
   note_launch();
@@ -1561,11 +1531,13 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
   rm->d_esrc = static_cast<int32_t*>(rm_alloc(sizeof(int32_t) * std::max<int64_t>(rm->nnz_total, 1), st));
   if (!rm->d_esrc) return set_error(MPAP_ERR_OUT_OF_MEMORY, "edge source array allocation failed");
   const size_t smem = edges_smem(rm);
-  unsigned long long* d_next = nullptr;   // [0..1] item counters of the two edge phases, [2] kv slots
-  CK(cudaMallocAsync(&d_next, 3 * sizeof(unsigned long long), st));
-  CK(cudaMemsetAsync(d_next, 0, 3 * sizeof(unsigned long long), st));
+  unsigned long long* d_next = nullptr;   // [0..1] item counters of the two edge phases, [2] kv slots, [3] free edges
+  CK(cudaMallocAsync(&d_next, 4 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(d_next, 0, 4 * sizeof(unsigned long long), st));
   if (rm->nnz_total > 0) {
-    EdgeWork ew{d_scr, cap, nullptr, 0, d_free, d_work, d_next, nullptr, nullptr, d_next + 2};
+    EdgeWork ew{d_scr, cap, nullptr, 0, d_free, d_work, d_next, nullptr, nullptr, d_next + 2, nullptr, d_next + 3};
+    ew.flist = static_cast<longlong2*>(workspace(st, WS_FLIST, sizeof(longlong2) * rm->nnz_total));
+    if (!ew.flist) return set_error(MPAP_ERR_OUT_OF_MEMORY, "free-edge list workspace allocation failed");
     ew.koff = static_cast<long long*>(workspace(st, WS_KOFF, sizeof(long long) * rm->nnz_total));
     if (!ew.koff) return set_error(MPAP_ERR_OUT_OF_MEMORY, "kv offset workspace allocation failed");
     CK(edge_phases(smem, st, rm, ew));
@@ -1649,7 +1621,7 @@ mpap_status update_roadmap_device(mpap_roadmap* rm, int env, const std::vector<d
     CK(cudaMemsetAsync(d_free, 0, sizeof(unsigned long long) * rm->B, st));
     const size_t smem = edges_smem(rm);
     EdgeWork ew{nullptr, 0, d_items, (int64_t)n_items, d_free, d_ctr + 4 - W_EDGES, d_ctr + 1, nullptr, nullptr,
-                d_ctr + 3};
+                d_ctr + 3, nullptr, nullptr};
     ew.koff = static_cast<long long*>(workspace(st, WS_KOFF, sizeof(long long) * rm->nnz_total));
     if (!ew.koff) return set_error(MPAP_ERR_OUT_OF_MEMORY, "kv offset workspace allocation failed");
     CK(edge_phases(smem, st, rm, ew));

@@ -114,7 +114,7 @@ void retain_pool_memory(int device);
 // on one stream reuse it (stream order serialises them); other streams get
 // their own.  Returns nullptr on allocation failure.
 void* workspace(cudaStream_t st, int tag, size_t bytes);
-enum { WS_NEAR = 0, WS_SEARCH = 1, WS_KOFF = 2, WS_KV = 3 };
+enum { WS_NEAR = 0, WS_SEARCH = 1, WS_KOFF = 2, WS_KV = 3, WS_FLIST = 4 };
 // Device buffer cache for roadmap arrays (capi.cu).  Roadmaps are built and
 // freed every step of a batched pipeline with the same sizes; growing the
 // stream-ordered pool for them stalled the host for up to 0.5 s per call
