@@ -1184,31 +1184,39 @@ __global__ void __launch_bounds__(kFoldThreads, MPAP_FOLD_MIN_BLOCKS) k_fold(con
   const uint16_t* kvp = kvbuf + koff[e];
   const double q = Dl / P.n_f;
   double s = 0.0, c = 0.0, Sp = 0.0, Cp = 0.0;
-  for (int k = 0; k < K; ++k) {
-    const int kv = kvp[k];
-    double inc = Dl - (double)kv * q;
-    if (HEUR == 3) {
-      double speed = P.nominal_speed;   // |v(t)| for the MLP (kinematic: nominal)
-      if (DYN == 1) {
-        const double t = (double)k * Dl;
-        double vel[D];
-        di_vel<D>(su_l, c2, c3, t, vel);
-        double ss = 0.0;
+  // the edge's counts are 8-aligned: one 16-byte load per 8 steps
+  for (int k0 = 0; k0 < K; k0 += 8) {
+    const uint4 q8 = __ldg(reinterpret_cast<const uint4*>(kvp + k0));
+    const unsigned wv[4] = {q8.x, q8.y, q8.z, q8.w};
 #pragma unroll
-        for (int j = 0; j < D; ++j) ss = fma(vel[j], vel[j], ss);
-        speed = sqrt(ss);
+    for (int jj = 0; jj < 8; ++jj) {
+      const int k = k0 + jj;
+      if (k >= K) break;
+      const int kv = (int)((wv[jj >> 1] >> (16 * (jj & 1))) & 0xffffu);
+      double inc = Dl - (double)kv * q;
+      if (HEUR == 3) {
+        double speed = P.nominal_speed;   // |v(t)| for the MLP (kinematic: nominal)
+        if (DYN == 1) {
+          const double t = (double)k * Dl;
+          double vel[D];
+          di_vel<D>(su_l, c2, c3, t, vel);
+          double ss = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) ss = fma(vel[j], vel[j], ss);
+          speed = sqrt(ss);
+        }
+        const double z0 = speed / P.v_ref;
+        const double z1 = omega / P.w_ref;
+        const double z2 = (double)kv / P.n_f;
+        const double o = mlp_out0(s_mlp, z0, z1, z2);
+        inc = inc + Dl * (P.mlp_gain * o);
       }
-      const double z0 = speed / P.v_ref;
-      const double z1 = omega / P.w_ref;
-      const double z2 = (double)kv / P.n_f;
-      const double o = mlp_out0(s_mlp, z0, z1, z2);
-      inc = inc + Dl * (P.mlp_gain * o);
+      const double tt = c + inc;
+      c = (tt > 0.0) ? tt : 0.0;
+      s = s + inc;
+      Sp = (s > Sp) ? s : Sp;   // running maxima of the prefix values (NEXT-3)
+      Cp = (c > Cp) ? c : Cp;
     }
-    const double tt = c + inc;
-    c = (tt > 0.0) ? tt : 0.0;
-    s = s + inc;
-    Sp = (s > Sp) ? s : Sp;   // running maxima of the prefix values (NEXT-3)
-    Cp = (c > Cp) ? c : Cp;
   }
   *reinterpret_cast<float2*>(&edges[e].s) = make_float2((float)s, (float)c);
   if (peak) peak[e] = make_float2((float)Sp, (float)Cp);
