@@ -271,6 +271,69 @@ mpap_status mpap_roadmap_export_peaks(const mpap_roadmap *rm, int32_t env, float
  * >= 0.  Replaces any previous peaks.  Synchronises. */
 mpap_status mpap_roadmap_set_peaks(mpap_roadmap *rm, const float *S, const float *C);
 
+/*
+ * Monte Carlo verification (Alg. 1 step 4; §3: "an
+ * asymptotically exact probability of motion plan p satisfying a
+ * localization error bound through MC sampling").
+ * One trial simulates the double-integrator vehicle tracking the
+ * plan's nominal trajectory (the edges' cubic trajectories, reading R7) with
+ * feedback on its ESTIMATED state, an inertial estimate from a noisy
+ * accelerometer and a translation-only 3D-to-3D position fix from
+ * the features in view from the TRUE state, fused by a per-axis
+ * Kalman filter.  Exact model, operation order and the counter-based
+ * noise generator: DESIGN.md §4 readings R31-R36.
+ */
+typedef struct {
+  int32_t trials;     /* trials per plan, >= 1                                  */
+  int32_t pad;
+  uint64_t seed;      /* noise stream key; trial t of every plan uses stream (seed, trial0 + t) */
+  double sigma_imu;   /* accelerometer noise per axis (m/s^2), >= 0             */
+  double sigma_vis;   /* feature relative-position noise per axis (m), >= 0     */
+  double u_max;       /* per-axis control limit, > 0                            */
+  double k_p, k_d;    /* tracking gains per axis (e.g. LQR), finite             */
+  double p0_pos, p0_vel;  /* initial filter covariance diagonal, >= 0           */
+  double delta;       /* localisation error bound delta_x_hat of Eq. 1   */
+} mpap_mc_params;
+
+typedef struct {
+  int32_t status;     /* OK, or INVALID_ARGUMENT if a plan edge is not a
+                         collision-free edge of the roadmap                      */
+  int32_t trials;
+  int64_t exceed;     /* trials with max_t |x_hat - x| >= delta                  */
+  int64_t steps;      /* simulation steps per trial                             */
+  int64_t fixes;      /* steps with >= 1 feature in view, summed over trials    */
+  double p_hat;       /* exceed / trials                                */
+} mpap_mc_result;
+
+/*
+ * mpap_mc_verify_batch -- MC verification of n_plans plans, all trials of
+ * all plans in one launch (warp per trial).
+ *   rm              a double-integrator roadmap built by mpap_build_roadmap*
+ *                   (imported roadmaps carry no geometry: INVALID_ARGUMENT).
+ *   envs            host, [n_plans] environment of each plan.
+ *   paths           host, [n_plans][path_stride] node sequences (start first),
+ *                   as returned by mpap_search_batch.
+ *   path_lens       host, [n_plans], 1 <= len <= path_stride (len 1 = start in
+ *                   goal: zero steps, zero errors).
+ *   mc              host; trials, noise, gains, delta (validated).
+ *   trial0          first trial id (trials are independent streams).
+ *   max_err, max_dev  host, [n_plans][mc->trials] f64 each (NULL skips):
+ *                   max over steps of |x_hat - x| and |x_nom - x|.
+ *   results         host, [n_plans].
+ * Returns OK if the batch executed (each plan's outcome in results[p].status),
+ * INVALID_ARGUMENT for bad arguments, OUT_OF_MEMORY, CUDA.  Synchronises.
+ */
+mpap_status mpap_mc_verify_batch(const mpap_roadmap *rm, int32_t n_plans, const int32_t *envs,
+                                 const int32_t *paths, int32_t path_stride, const int32_t *path_lens,
+                                 const mpap_mc_params *mc, uint64_t trial0, double *max_err,
+                                 double *max_dev, mpap_mc_result *results, void *cuda_stream);
+
+/* Single-plan form: returns results->status (OK or INVALID_ARGUMENT for an
+ * invalid plan) unless the call itself failed. */
+mpap_status mpap_mc_verify(const mpap_roadmap *rm, int32_t env, const int32_t *path, int32_t path_len,
+                           const mpap_mc_params *mc, uint64_t trial0, double *max_err, double *max_dev,
+                           mpap_mc_result *result, void *cuda_stream);
+
 /* Releases the roadmap's device memory (NULL is a no-op).  Waits for the
  * device to be idle first (searches of this roadmap may be in flight). */
 void mpap_roadmap_free(mpap_roadmap *rm);
@@ -286,7 +349,8 @@ int64_t mpap_launch_count(void);
  * every kernel launch of this library is bracketed by an event pair recorded
  * on its launching stream.  mpap_prof_read synchronises those events and
  * returns the accumulated milliseconds and launch count of `kernel`
- * ("k_near", "k_scan", "k_edges", "k_search"); returns 1 if it was seen. */
+ * ("k_near", "k_scan", "k_collide", "k_heuristic", "k_fold",
+ * "k_search", "k_mc"); returns 1 if it was seen. */
 void mpap_prof_enable(int32_t on);
 void mpap_prof_reset(void);
 int32_t mpap_prof_read(const char *kernel, double *total_ms, int64_t *launches);

@@ -63,6 +63,26 @@ class OrcResult(C.Structure):
     ]
 
 
+class OrcMc(C.Structure):
+    _fields_ = [("trials", C.c_int32), ("pad", C.c_int32), ("seed", C.c_uint64),
+                ("sigma_imu", C.c_double), ("sigma_vis", C.c_double), ("u_max", C.c_double),
+                ("k_p", C.c_double), ("k_d", C.c_double), ("p0_pos", C.c_double), ("p0_vel", C.c_double),
+                ("delta", C.c_double)]
+
+
+class OrcMcTrace(C.Structure):
+    _fields_ = [("err_final", C.c_double * 3), ("p11", C.c_double), ("p12", C.c_double), ("p22", C.c_double),
+                ("steps", C.c_int64), ("draws", C.c_int64), ("fixes", C.c_int64)]
+
+
+MC_FIELDS = ["trials", "seed", "sigma_imu", "sigma_vis", "u_max", "k_p", "k_d", "p0_pos", "p0_vel", "delta"]
+
+
+def _mc_struct(mc: Dict[str, Any]) -> "OrcMc":
+    return OrcMc(trials=int(mc.get("trials", 0)), pad=0, seed=int(mc["seed"]) & (2 ** 64 - 1),
+                 **{k: float(mc[k]) for k in MC_FIELDS[2:]})
+
+
 WAVE_FIELDS = ["i", "group", "relax", "beta_pass", "inserted", "killed", "touched", "stair_sum"]
 
 
@@ -123,6 +143,14 @@ def lib():
         L.orc_build_peaks.restype = None
         L.orc_goal_mask.argtypes = [dp, C.c_int32, C.c_int32, C.c_int32, dp, dp, u8p]
         L.orc_goal_mask.restype = None
+        L.orc_mc_normal.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
+        L.orc_mc_normal.restype = C.c_double
+        L.orc_mc_trial.argtypes = [C.POINTER(OrcEnv), C.POINTER(OrcParams), i32p, C.c_int32, C.POINTER(OrcMc),
+                                   C.c_uint64, dp, dp, C.POINTER(OrcMcTrace)]
+        L.orc_mc_trial.restype = C.c_int
+        L.orc_mc_verify.argtypes = [C.POINTER(OrcEnv), C.POINTER(OrcParams), i32p, C.c_int32, C.POINTER(OrcMc),
+                                    C.c_uint64, C.c_int32, dp, dp]
+        L.orc_mc_verify.restype = C.c_int64
         _lib = L
     return _lib
 
@@ -400,3 +428,46 @@ def build_roadmap_parallel(prob, procs: int = 0, use_prefilter: bool = True) -> 
     cat = lambda k, dt: np.concatenate([r[k] for r in rows]).astype(dt) if rows else np.zeros(0, dt)
     return {"n": n, "row_ptr": row_ptr, "dst": cat("dst", np.int32), "coll": cat("coll", np.uint8),
             "w": cat("w", np.float32), "s": cat("s", np.float32), "c": cat("c", np.float32)}
+
+
+# ---------------------------------------------------------------------------
+# Monte Carlo verification (NEXT-4; Alg. 1 step 4, model P:310-321)
+# ---------------------------------------------------------------------------
+
+def mc_normal(seed: int, trial: int, idx: int) -> float:
+    """Normal number `idx` of trial `trial` (counter-based, reading R33)."""
+    return float(lib().orc_mc_normal(int(seed) & (2 ** 64 - 1), int(trial), int(idx)))
+
+
+def mc_trial(prob, path, mc: Dict[str, Any], trial: int) -> Dict[str, Any]:
+    """One closed-loop trial along `path`: max localisation error, max
+    deviation from the nominal, and the pins' trace (final error, filter
+    covariance, step/draw/fix counts)."""
+    ctx = _Ctx(prob)
+    p = np.ascontiguousarray(path, dtype=np.int32)
+    m = _mc_struct(mc)
+    e, dv = C.c_double(), C.c_double()
+    tr = OrcMcTrace()
+    s = lib().orc_mc_trial(C.byref(ctx.env), C.byref(ctx.prm), _ptr(p, C.c_int32), len(p), C.byref(m),
+                           int(trial), C.byref(e), C.byref(dv), C.byref(tr))
+    if s != 0:
+        raise ValueError("invalid plan for Monte Carlo (not a double-integrator r-disc path)")
+    return {"max_err": e.value, "max_dev": dv.value, "err_final": np.array(tr.err_final[:]),
+            "p11": tr.p11, "p12": tr.p12, "p22": tr.p22, "steps": tr.steps, "draws": tr.draws,
+            "fixes": tr.fixes}
+
+
+def mc_verify(prob, path, mc: Dict[str, Any], trial0: int = 0, ntrials: Optional[int] = None) -> Dict[str, Any]:
+    """Trials trial0 .. trial0+ntrials-1: per-trial max errors / deviations and
+    the exceedance count (p_hat = exceed / trials)."""
+    ctx = _Ctx(prob)
+    p = np.ascontiguousarray(path, dtype=np.int32)
+    m = _mc_struct(mc)
+    nt = int(mc["trials"] if ntrials is None else ntrials)
+    me = np.zeros(max(nt, 1))
+    md = np.zeros(max(nt, 1))
+    ex = lib().orc_mc_verify(C.byref(ctx.env), C.byref(ctx.prm), _ptr(p, C.c_int32), len(p), C.byref(m),
+                             int(trial0), nt, _ptr(me, C.c_double), _ptr(md, C.c_double))
+    if ex < 0:
+        raise ValueError("invalid plan for Monte Carlo")
+    return {"max_err": me[:nt], "max_dev": md[:nt], "exceed": int(ex), "p_hat": ex / nt if nt else 0.0}

@@ -16,6 +16,9 @@
  *                  RemoveDominated, PH, cutoff (A3.9),
  *                  termination (A3.5), argmin (A3.20-21)
  *                  under readings R3-R5, R13-R16, R24-R27.
+ *   orc_mc_*    -- Alg. 1 step 4 Monte Carlo verification
+ *                  with the §4.1 simulation model, readings
+ *                  R31-R36 (NEXT-4).
  *
  * Pins: tests/test_oracle_*.py (closed forms, brute force, Dijkstra in the
  * exact regime, dense-sampling collision, SPEC worked examples).  Functions
@@ -852,4 +855,216 @@ void orc_goal_mask(const double *samples, int32_t n, int32_t stride, int32_t d,
     for (int k = 0; k < d; ++k) if (p[k] < lo[k] || p[k] > hi[k]) in = 0;
     out[x] = (uint8_t)in;
   }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Monte Carlo verification (Alg. 1 step 4; §3; simulation */
+/* model §4.1) -- NEXT-4, readings R31-R36 of DESIGN.md §4.       */
+/* One trial = closed-loop simulation of the 6D double integrator tracking  */
+/* the plan's nominal trajectory with an LQR-type feedback on the ESTIMATED */
+/* state, an inertial estimate from a noisy accelerometer,  */
+/* a translation-only 3D-to-3D position fix from the features in view from  */
+/* the TRUE state, fused by a Kalman filter.  Output:   */
+/* max_t |x_hat - x| and max_t |x_nom - x|; p_hat = P(max err >= delta)     */
+/* (Eq. 1; "asymptotically exact probability").                 */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t trials;
+  int32_t pad;
+  uint64_t seed;
+  double sigma_imu;   /* accelerometer white noise per axis (m/s^2) */
+  double sigma_vis;   /* feature relative-position noise per axis (m) */
+  double u_max;       /* per-axis control limit                              */
+  double k_p, k_d;    /* tracking gains per axis (LQR)                */
+  double p0_pos, p0_vel;  /* initial filter covariance diag                  */
+  double delta;       /* localisation error bound delta_x_hat (Eq. 1)        */
+} orc_mc;
+
+typedef struct {     /* extra per-trial outputs used by the oracle's pins    */
+  double err_final[3];     /* x_hat - x at the last step                     */
+  double p11, p12, p22;    /* filter covariance at the last step             */
+  int64_t steps;           /* simulation steps                               */
+  int64_t draws;           /* normals consumed                               */
+  int64_t fixes;           /* steps with >= 1 feature in view                */
+} orc_mc_trace;
+
+/* counter-based generator (R33): SplitMix64's finaliser over a Weyl sequence. */
+static uint64_t mc_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+/* normal number `idx` of trial `trial`: Irwin-Hall sum of 12 uniform 32-bit
+ * words (the two halves of 6 consecutive 64-bit draws) minus 6 (R33). */
+double orc_mc_normal(uint64_t seed, uint64_t trial, uint64_t idx) {
+  const uint64_t G = 0x9E3779B97F4A7C15ULL;
+  uint64_t key = mc_mix(seed + G * (trial + 1ULL));
+  uint64_t S = 0;
+  for (int i = 0; i < 6; ++i) {
+    uint64_t w = mc_mix(key + G * (idx * 6ULL + (uint64_t)i + 1ULL));
+    S += (w & 0xffffffffULL) + (w >> 32);
+  }
+  return (double)S * (1.0 / 4294967296.0) - 6.0;
+}
+
+/* features in view from x with heading hv (same predicate as the heuristic,
+ * P:319 "in the field of view and unobstructed"); writes their indices. */
+static int visible_list(const orc_env *E, const orc_params *prm, const double *x, const double *hv, int32_t *out) {
+  int d = prm->pos_dim;
+  double R2 = prm->max_range * prm->max_range;
+  double cos2 = prm->fov_cos_half * prm->fov_cos_half;
+  int count = 0;
+  for (int f = 0; f < E->n_features; ++f) {
+    const double *F = E->features + (size_t)f * d;
+    double dl[3];
+    double dd = 0.0;
+    for (int j = 0; j < d; ++j) { dl[j] = F[j] - x[j]; dd = fma(dl[j], dl[j], dd); }
+    if (dd > R2) continue;
+    if (prm->heuristic != 0) {
+      double hh = 0.0, dot = 0.0;
+      for (int j = 0; j < d; ++j) hh = fma(hv[j], hv[j], hh);
+      for (int j = 0; j < d; ++j) dot = fma(hv[j], dl[j], dot);
+      if (!(hh > 0.0)) continue;
+      if (dot < 0.0) continue;
+      if (dot * dot < cos2 * (hh * dd)) continue;
+    }
+    if (seg_hits_any(x, F, E, d)) continue;
+    out[count++] = f;
+  }
+  return count;
+}
+
+/* One trial along plan path[0..L-1] (double-integrator roadmap only).
+ * Returns 0, or -1 if a plan edge has no connection (not an r-disc edge). */
+int orc_mc_trial(const orc_env *E, const orc_params *prm, const int32_t *path, int32_t L,
+                 const orc_mc *mc, uint64_t trial, double *max_err, double *max_dev, orc_mc_trace *tr) {
+  if (prm->dynamics != 1 || L < 1) return -1;
+  int d = prm->pos_dim;
+  int hoff = 2 * d;
+  const double *s0 = E->samples + (size_t)path[0] * E->stride;
+  double x[3] = {0, 0, 0}, v[3] = {0, 0, 0}, xh[3] = {0, 0, 0}, vh[3] = {0, 0, 0};
+  for (int j = 0; j < d; ++j) { x[j] = s0[j]; v[j] = s0[d + j]; xh[j] = s0[j]; vh[j] = s0[d + j]; }
+  double p11 = mc->p0_pos, p12 = 0.0, p22 = mc->p0_vel;
+  const double q = mc->sigma_imu * mc->sigma_imu;
+  const double rv = mc->sigma_vis * mc->sigma_vis;
+  double me = 0.0, md = 0.0;
+  uint64_t ctr = 0;
+  int64_t steps = 0, fixes = 0;
+  int32_t *vis = (int32_t *)malloc(sizeof(int32_t) * (size_t)(E->n_features > 0 ? E->n_features : 1));
+  for (int32_t e = 0; e + 1 < L; ++e) {
+    const double *su = E->samples + (size_t)path[e] * E->stride;
+    const double *sv = E->samples + (size_t)path[e + 1] * E->stride;
+    double c64, T;
+    if (!orc_cost_di(su, sv, d, prm->control_weight, E->r, &c64, &T)) { free(vis); return -1; }
+    double c2[3] = {0, 0, 0}, c3[3] = {0, 0, 0};
+    di_traj(su, sv, d, T, c2, c3);
+    double kk = ceil(T / prm->dt);
+    int K = (kk < 1.0) ? 1 : (int)kk;
+    double Dl = T / (double)K;
+    double D2 = Dl * Dl;
+    for (int k = 0; k < K; ++k) {
+      double t = (double)k * Dl;
+      double xn[3], vn[3], an[3] = {0, 0, 0};
+      di_pos(su, c2, c3, d, t, xn);
+      di_vel(su, c2, c3, d, t, vn);
+      for (int j = 0; j < d; ++j) an[j] = fma(t, 6.0 * c3[j], 2.0 * c2[j]);   /* nominal acceleration */
+      /* (1) control on the estimate, saturated (R32) */
+      double u[3] = {0, 0, 0};
+      for (int j = 0; j < d; ++j) {
+        double uj = (an[j] + mc->k_p * (xn[j] - xh[j])) + mc->k_d * (vn[j] - vh[j]);
+        if (uj > mc->u_max) uj = mc->u_max;
+        if (uj < -mc->u_max) uj = -mc->u_max;
+        u[j] = uj;
+      }
+      /* (2) true dynamics x'' = u, semi-implicit Euler */
+      for (int j = 0; j < d; ++j) { v[j] = v[j] + u[j] * Dl; x[j] = x[j] + v[j] * Dl; }
+      /* (3) accelerometer = true acceleration + noise; filter prediction */
+      for (int j = 0; j < d; ++j) {
+        double am = u[j] + mc->sigma_imu * orc_mc_normal(mc->seed, trial, ctr++);
+        vh[j] = vh[j] + am * Dl;
+        xh[j] = xh[j] + vh[j] * Dl;
+      }
+      {
+        double a = Dl * p12;
+        double n11 = (((p11 + a) + a) + D2 * p22) + q * (D2 * D2);
+        double n12 = (p12 + Dl * p22) + q * (D2 * Dl);
+        double n22 = p22 + q * D2;
+        p11 = n11; p12 = n12; p22 = n22;
+      }
+      /* (4) features in view from the TRUE state at t + Dl (yaw tracked exactly) */
+      double t1 = (double)(k + 1) * Dl;
+      double hv[3] = {0, 0, 0};
+      if (prm->heuristic == 1) {
+        for (int j = 0; j < d; ++j) hv[j] = v[j];
+      } else if (prm->heuristic >= 2) {
+        double s = t1 / T;
+        hv[0] = fma(s, sv[hoff], (1.0 - s) * su[hoff]);
+        hv[1] = fma(s, sv[hoff + 1], (1.0 - s) * su[hoff + 1]);
+      }
+      int kv = visible_list(E, prm, x, hv, vis);
+      /* (5) translation-only 3D-to-3D fix: mean over features of f - z_f, with
+       * z_f = (f - x) + noise; Kalman update with R = sigma^2 / k */
+      if (kv > 0) {
+        double sum[3] = {0, 0, 0};
+        for (int i = 0; i < kv; ++i) {
+          const double *F = E->features + (size_t)vis[i] * d;
+          for (int j = 0; j < d; ++j) {
+            double z = (F[j] - x[j]) + mc->sigma_vis * orc_mc_normal(mc->seed, trial, ctr++);
+            sum[j] = sum[j] + (F[j] - z);
+          }
+        }
+        double Rm = rv / (double)kv;
+        double S = p11 + Rm;
+        double K1 = 0.0, K2 = 0.0;          /* S == 0: no uncertainty left, no gain (R34) */
+        if (S > 0.0) { K1 = p11 / S; K2 = p12 / S; }
+        for (int j = 0; j < d; ++j) {
+          double fix = sum[j] / (double)kv;
+          double y = fix - xh[j];
+          xh[j] = xh[j] + K1 * y;
+          vh[j] = vh[j] + K2 * y;
+        }
+        double n11 = p11 - K1 * p11;
+        double n12 = p12 - K1 * p12;
+        double n22 = p22 - K2 * p12;
+        p11 = n11; p12 = n12; p22 = n22;
+        ++fixes;
+      }
+      /* (6) localisation error and deviation from the nominal at t + Dl */
+      double xn1[3];
+      di_pos(su, c2, c3, d, t1, xn1);
+      double ee = 0.0, dd = 0.0;
+      for (int j = 0; j < d; ++j) {
+        double a = xh[j] - x[j];
+        double b = xn1[j] - x[j];
+        ee = ee + a * a;
+        dd = dd + b * b;
+      }
+      double err = sqrt(ee), dev = sqrt(dd);
+      if (err > me) me = err;
+      if (dev > md) md = dev;
+      ++steps;
+    }
+  }
+  free(vis);
+  *max_err = me;
+  *max_dev = md;
+  if (tr) {
+    for (int j = 0; j < 3; ++j) tr->err_final[j] = xh[j] - x[j];
+    tr->p11 = p11; tr->p12 = p12; tr->p22 = p22;
+    tr->steps = steps; tr->draws = (int64_t)ctr; tr->fixes = fixes;
+  }
+  return 0;
+}
+
+/* All trials; returns the number with max_err >= delta (p_hat = count/trials,
+ * P:290), or -1 on an invalid plan edge. */
+int64_t orc_mc_verify(const orc_env *E, const orc_params *prm, const int32_t *path, int32_t L,
+                      const orc_mc *mc, uint64_t trial0, int32_t ntrials, double *max_err, double *max_dev) {
+  int64_t exceed = 0;
+  for (int32_t i = 0; i < ntrials; ++i) {
+    if (orc_mc_trial(E, prm, path, L, mc, trial0 + (uint64_t)i, &max_err[i], &max_dev[i], NULL) != 0) return -1;
+    if (max_err[i] >= mc->delta) ++exceed;
+  }
+  return exceed;
 }

@@ -45,7 +45,7 @@ EXPORTED_SYMBOLS = [
     "mpap_roadmap_info", "mpap_roadmap_envs", "mpap_roadmap_export", "mpap_roadmap_free", "mpap_status_str",
     "mpap_last_error", "mpap_launch_count", "mpap_prof_enable", "mpap_prof_reset", "mpap_prof_read",
     "mpap_roadmap_work", "mpap_search_ex", "mpap_search_batch_ex", "mpap_roadmap_export_peaks",
-    "mpap_roadmap_set_peaks", "mpap_roadmap_update",
+    "mpap_roadmap_set_peaks", "mpap_roadmap_update", "mpap_mc_verify", "mpap_mc_verify_batch",
 ]
 
 
@@ -91,6 +91,16 @@ RESULT_DTYPE = np.dtype([("status", np.int32), ("path_len", np.int32), ("waves",
                          ("relaxations", np.int64), ("labels_inserted", np.int64)])
 assert RESULT_DTYPE.itemsize == C.sizeof(mpap_result) == 48
 
+class mpap_mc_params(C.Structure):
+    _fields_ = [("trials", C.c_int32), ("pad", C.c_int32), ("seed", C.c_uint64),
+                ("sigma_imu", C.c_double), ("sigma_vis", C.c_double), ("u_max", C.c_double),
+                ("k_p", C.c_double), ("k_d", C.c_double), ("p0_pos", C.c_double), ("p0_vel", C.c_double),
+                ("delta", C.c_double)]
+
+
+MC_RESULT_DTYPE = np.dtype([("status", np.int32), ("trials", np.int32), ("exceed", np.int64), ("steps", np.int64),
+                            ("fixes", np.int64), ("p_hat", np.float64)])
+
 _vp = C.c_void_p
 _i32p = C.POINTER(C.c_int32)
 _lib.mpap_build_roadmap_batch.argtypes = [C.c_int32, _vp, _i32p, C.c_int32, _vp, _i32p, _vp, _i32p, C.c_double,
@@ -105,6 +115,10 @@ _lib.mpap_search_ex.argtypes = [_vp, C.c_int32, C.c_int32, C.POINTER(mpap_goal),
                                 _i32p, C.c_int32, C.POINTER(mpap_result), C.POINTER(mpap_wave), C.c_int32, _vp]
 _lib.mpap_search_batch_ex.argtypes = [_vp, C.c_int32, _i32p, _i32p, C.POINTER(mpap_goal), C.POINTER(C.c_double),
                                       C.c_double, C.c_uint32, _vp, C.c_int32, _vp, C.c_int32, _vp]
+_lib.mpap_mc_verify_batch.argtypes = [_vp, C.c_int32, _vp, _vp, C.c_int32, _vp, C.POINTER(mpap_mc_params),
+                                      C.c_uint64, _vp, _vp, _vp, _vp]
+_lib.mpap_mc_verify.argtypes = [_vp, C.c_int32, _vp, C.c_int32, C.POINTER(mpap_mc_params), C.c_uint64, _vp, _vp,
+                                _vp, _vp]
 _lib.mpap_roadmap_export_peaks.argtypes = [_vp, C.c_int32, _vp, _vp]
 _lib.mpap_roadmap_set_peaks.argtypes = [_vp, _vp, _vp]
 _lib.mpap_roadmap_update.argtypes = [_vp, C.c_int32, _vp, C.c_int32, _vp, C.c_int32, C.c_int32, _vp,
@@ -445,6 +459,7 @@ def mpap_prof_read(kernel: str) -> tuple:
 
 
 KERNELS = ("k_near", "k_scan", "k_collide", "k_heuristic", "k_fold", "k_search")
+MC_KERNELS = ("k_mc_plan", "k_mc")
 
 
 WORK_FIELDS = ["pairs", "prefilter_pass", "bisect_iters", "edges", "coll_segs", "coll_box_tests", "steps",
@@ -458,3 +473,51 @@ def mpap_roadmap_work(rm: Roadmap) -> dict:
     if s != MPAP_OK:
         raise MpapError(s, "mpap_roadmap_work")
     return {k: int(a[i]) for i, k in enumerate(WORK_FIELDS)}
+
+
+def make_mc_params(mc: Dict[str, Any]) -> mpap_mc_params:
+    """mpap_mc_params from a dict with the struct's field names."""
+    return mpap_mc_params(trials=int(mc["trials"]), pad=0, seed=int(mc["seed"]) & (2 ** 64 - 1),
+                          **{k: float(mc[k]) for k in ("sigma_imu", "sigma_vis", "u_max", "k_p", "k_d", "p0_pos",
+                                                       "p0_vel", "delta")})
+
+
+def mpap_mc_verify_batch(rm: Roadmap, envs, paths, path_lens, mc: Dict[str, Any], trial0: int = 0,
+                         per_trial: bool = True, stream=None):
+    """Monte Carlo verification (Alg. 1 step 4) of n plans: returns
+    (results [n] MC_RESULT_DTYPE, max_err [n, trials], max_dev [n, trials])."""
+    P = len(envs)
+    ea = np.ascontiguousarray(envs, dtype=np.int32)
+    pa = np.ascontiguousarray(paths, dtype=np.int32).reshape(P, -1)
+    la = np.ascontiguousarray(path_lens, dtype=np.int32)
+    m = make_mc_params(mc)
+    res = np.zeros(max(P, 1), dtype=MC_RESULT_DTYPE)
+    me = np.zeros((P, m.trials)) if per_trial else None
+    md = np.zeros((P, m.trials)) if per_trial else None
+    st = _stream(stream)
+    s = _lib.mpap_mc_verify_batch(rm.handle, P, C.c_void_p(ea.ctypes.data), C.c_void_p(pa.ctypes.data),
+                                  int(pa.shape[1]) if P else 1, C.c_void_p(la.ctypes.data), C.byref(m), int(trial0),
+                                  C.c_void_p(me.ctypes.data) if per_trial else None,
+                                  C.c_void_p(md.ctypes.data) if per_trial else None, C.c_void_p(res.ctypes.data),
+                                  C.c_void_p(st) if st else None)
+    if s != MPAP_OK:
+        raise MpapError(s, "mpap_mc_verify_batch")
+    return res[:P], me, md
+
+
+def mpap_mc_verify(rm: Roadmap, env: int, path, mc: Dict[str, Any], trial0: int = 0, stream=None) -> Dict[str, Any]:
+    """Monte Carlo verification of one plan: p_hat = P(max |x_hat - x| >= delta)."""
+    pa = np.ascontiguousarray(path, dtype=np.int32)
+    m = make_mc_params(mc)
+    res = np.zeros(1, dtype=MC_RESULT_DTYPE)
+    me = np.zeros(m.trials)
+    md = np.zeros(m.trials)
+    st = _stream(stream)
+    s = _lib.mpap_mc_verify(rm.handle, int(env), C.c_void_p(pa.ctypes.data), len(pa), C.byref(m), int(trial0),
+                            C.c_void_p(me.ctypes.data), C.c_void_p(md.ctypes.data), C.c_void_p(res.ctypes.data),
+                            C.c_void_p(st) if st else None)
+    if s != MPAP_OK:
+        raise MpapError(s, "mpap_mc_verify")
+    r = res[0]
+    return {"p_hat": float(r["p_hat"]), "exceed": int(r["exceed"]), "trials": int(r["trials"]),
+            "steps": int(r["steps"]), "fixes": int(r["fixes"]), "max_err": me, "max_dev": md}

@@ -31,6 +31,7 @@
 #include <cstring>
 
 #include "mpap_internal.cuh"
+#include "traj.cuh"
 
 namespace mpap {
 
@@ -178,31 +179,6 @@ __device__ bool cost_di(const double* su, const double* sv, double ru, double r,
   c_out = best_c;
   tau_out = best_t;
   return true;
-}
-
-template <int D>
-__device__ __forceinline__ void di_traj(const double* su, const double* sv, double tau, double* c2, double* c3) {
-  const double tau2 = tau * tau;
-  const double tau3 = tau2 * tau;
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    const double dp = (sv[j] - su[j]) - su[D + j] * tau;
-    const double dl = sv[D + j] - su[D + j];
-    c2[j] = (3.0 * dp - dl * tau) / tau2;
-    c3[j] = (dl * tau - 2.0 * dp) / tau3;
-  }
-}
-
-template <int D>
-__device__ __forceinline__ void di_pos(const double* su, const double* c2, const double* c3, double t, double* x) {
-#pragma unroll
-  for (int j = 0; j < D; ++j) x[j] = fma(t, fma(t, fma(t, c3[j], c2[j]), su[D + j]), su[j]);
-}
-
-template <int D>
-__device__ __forceinline__ void di_vel(const double* su, const double* c2, const double* c3, double t, double* v) {
-#pragma unroll
-  for (int j = 0; j < D; ++j) v[j] = fma(t, fma(t, 3.0 * c3[j], 2.0 * c2[j]), su[D + j]);
 }
 
 // Work counters (always on; one atomicAdd per row per counter).

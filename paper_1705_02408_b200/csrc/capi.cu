@@ -800,4 +800,44 @@ mpap_status mpap_search_batch_ex(const mpap_roadmap* rm, int32_t n_queries, cons
                              static_cast<cudaStream_t>(cuda_stream));
 }
 
+
+mpap_status mpap_mc_verify_batch(const mpap_roadmap* rm, int32_t n_plans, const int32_t* envs, const int32_t* paths,
+                                 int32_t path_stride, const int32_t* path_lens, const mpap_mc_params* mc,
+                                 uint64_t trial0, double* max_err, double* max_dev, mpap_mc_result* results,
+                                 void* cuda_stream) {
+  if (!rm || !mc || n_plans < 0 || (n_plans > 0 && (!envs || !paths || !path_lens || !results)) || path_stride < 1)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "NULL argument, n_plans < 0 or path_stride < 1");
+  if (!rm->d_samples || !rm->d_tau || rm->prm.dynamics != MPAP_DOUBLE_INTEGRATOR)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "Monte Carlo needs a double-integrator roadmap built with geometry");
+  if (mc->trials < 1) return set_error(MPAP_ERR_INVALID_ARGUMENT, "trials must be >= 1");
+  const double nonneg[] = {mc->sigma_imu, mc->sigma_vis, mc->p0_pos, mc->p0_vel, mc->delta};
+  for (double x : nonneg)
+    if (!is_fin(x) || x < 0.0) return set_error(MPAP_ERR_INVALID_ARGUMENT, "noise/covariance/delta must be finite >= 0");
+  if (!is_fin(mc->u_max) || !(mc->u_max > 0.0) || !is_fin(mc->k_p) || !is_fin(mc->k_d))
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "u_max must be > 0 and gains finite");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != rm->device) return set_error(MPAP_ERR_INVALID_ARGUMENT, "roadmap bound to another device");
+  for (int32_t p = 0; p < n_plans; ++p) {
+    if (envs[p] < 0 || envs[p] >= rm->B) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad env");
+    if (path_lens[p] < 1 || path_lens[p] > path_stride) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad path_len");
+    const int32_t* path = paths + (size_t)p * path_stride;
+    for (int32_t j = 0; j < path_lens[p]; ++j)
+      if (path[j] < 0 || path[j] >= rm->n[envs[p]]) return set_error(MPAP_ERR_INVALID_ARGUMENT, "node out of range");
+  }
+  return mc_verify_device(rm, n_plans, envs, paths, path_stride, path_lens, mc, trial0, max_err, max_dev, results,
+                          static_cast<cudaStream_t>(cuda_stream));
+}
+
+mpap_status mpap_mc_verify(const mpap_roadmap* rm, int32_t env, const int32_t* path, int32_t path_len,
+                           const mpap_mc_params* mc, uint64_t trial0, double* max_err, double* max_dev,
+                           mpap_mc_result* result, void* cuda_stream) {
+  if (!result || !path || path_len < 1) return set_error(MPAP_ERR_INVALID_ARGUMENT, "NULL result/path or path_len < 1");
+  mpap_status s = mpap_mc_verify_batch(rm, 1, &env, path, path_len, &path_len, mc, trial0, max_err, max_dev, result,
+                                       cuda_stream);
+  if (s != MPAP_OK) return s;
+  if (result->status != MPAP_OK) return set_error((mpap_status)result->status, "plan edge is not a collision-free roadmap edge");
+  return MPAP_OK;
+}
+
 }  // extern "C"

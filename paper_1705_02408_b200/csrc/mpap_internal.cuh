@@ -144,4 +144,10 @@ struct QueryDesc {
 mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryDesc* h_queries,
                                 double lambda, int32_t* paths, int32_t path_cap, mpap_result* results,
                                 mpap_wave* h_waves, int32_t waves_cap, int32_t mem, cudaStream_t st);
+
+// Monte Carlo verification (mc_kernels.cu; NEXT-4); arguments validated by capi.cu
+mpap_status mc_verify_device(const mpap_roadmap* rm, int32_t n_plans, const int32_t* envs, const int32_t* paths,
+                             int32_t path_stride, const int32_t* path_lens, const mpap_mc_params* mc,
+                             uint64_t trial0, double* max_err, double* max_dev, mpap_mc_result* results,
+                             cudaStream_t st);
 }  // namespace mpap

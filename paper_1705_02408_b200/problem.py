@@ -9,8 +9,8 @@ from typing import Any, Dict, List, Sequence
 
 import numpy as np
 
-from . import (MPAP_MEM_DEVICE, Roadmap, mpap_build_roadmap, mpap_build_roadmap_batch, mpap_search,
-               mpap_search_batch, params_from_problem)
+from . import (MPAP_MEM_DEVICE, Roadmap, mpap_build_roadmap, mpap_build_roadmap_batch, mpap_mc_verify_batch,
+               mpap_search, mpap_search_batch, params_from_problem)
 
 
 def build_problem(prob, stream=None, edge_peaks: bool = False) -> Roadmap:
@@ -65,6 +65,18 @@ class Batch:
         envs = np.arange(len(self.probs), dtype=np.int32)
         return mpap_search_batch(rm, envs, self.starts, self.goals_lo, self.goals_hi, betas, self.lam,
                                  path_capacity, paths=paths, results=results, stream=stream)
+
+    def mc_verify(self, rm: Roadmap, paths, results, mc: Dict[str, Any], trial0: int = 0, per_trial: bool = False,
+                  stream=None):
+        """Monte Carlo verification (NEXT-4) of every feasible plan of a
+        search batch (host paths/results as returned by ``search``); returns
+        (env indices, MC results, per-trial max errors or None)."""
+        ok = np.nonzero(results["status"] == 0)[0].astype(np.int32)
+        if ok.size == 0:
+            return ok, None, None
+        res, me, _ = mpap_mc_verify_batch(rm, ok, paths[ok], results["path_len"][ok], mc, trial0=trial0,
+                                          per_trial=per_trial, stream=stream)
+        return ok, res, me
 
 
 # ---------------------------------------------------------------------------

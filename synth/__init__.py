@@ -9,3 +9,4 @@ identical float64 bytes it returns.
 """
 from .halton import halton, halton_points  # noqa: F401
 from .envs import Problem, make_problem, load_config, CONFIG_DIR  # noqa: F401
+from .mc import DEFAULT_MC, mc_params, line_problem  # noqa: F401
