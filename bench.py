@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-procs", type=int, default=0)
+    ap.add_argument("--no-mc", action="store_true", help="skip the Monte Carlo verification measurement")
+    ap.add_argument("--mc-trials", type=int, default=1000)
     return ap.parse_args()
 
 
@@ -356,6 +358,9 @@ def main():
     }
     if e2e:
         line["e2e"] = e2e
+    if not args.no_mc:
+        line["mc_verify"] = measure_mc(mp, B, betas, PATH_CAP, args.mc_trials, rank == 0 and world == 1
+                                       and not args.no_cpu_baseline)
     if (rank == 0) and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, beta, args.cpu_procs or os.cpu_count() or 1)
     if rank == 0:
@@ -363,6 +368,52 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def measure_mc(mp, B, betas, path_cap: int, trials: int, with_cpu: bool):
+    """NEXT-4: Monte Carlo verification (Alg. 1 step 4,
+    P:290) of the batch's feasible plans, `trials` trials each (Table 1 uses
+    1000), in one k_mc launch; timed with the library's CUDA events on
+    the launching stream (3 timed runs after 1 warm-up), outside the bench
+    step.  The oracle times one trial per plan of a few plans on one core."""
+    import torch
+    from synth import mc_params
+    mc = mc_params(trials=trials)
+    rm = B.build()
+    paths, res = B.search(rm, betas, path_capacity=path_cap)
+    B.mc_verify(rm, paths, res, mc)
+    torch.cuda.synchronize()
+    mp.mpap_prof_reset()
+    mp.mpap_prof_enable(True)
+    runs = 3
+    for k in range(runs):
+        ok, mres, _ = B.mc_verify(rm, paths, res, mc, trial0=k * trials)
+    mp.mpap_prof_enable(False)
+    ms, n = mp.mpap_prof_read("k_mc")
+    ms_plan, _ = mp.mpap_prof_read("k_mc_plan")
+    rm.free()
+    if mres is None:
+        return {"plans": 0}
+    t = (ms + ms_plan) / runs / 1e3
+    steps = float(mres["steps"].sum()) * trials
+    out = {"plans": int(ok.size), "trials_per_plan": trials, "ms_per_batch": (ms + ms_plan) / runs,
+           "k_mc_ms": ms / max(n, 1), "trials_per_s": ok.size * trials / t, "trial_steps_per_s": steps / t,
+           "p_hat_mean": float(mres["p_hat"].mean()), "fix_fraction": float(mres["fixes"].sum() / max(steps, 1)),
+           "params": {k: mc[k] for k in ("sigma_imu", "sigma_vis", "delta", "k_p", "k_d", "u_max")}}
+    if with_cpu:
+        import oracle
+        oracle.build()
+        t0 = time.perf_counter()
+        nt = 0
+        for e in ok[:4]:
+            path = paths[e][: res["path_len"][e]]
+            for tr in range(8):
+                oracle.mc_trial(B.probs[e], path, mc, tr)
+                nt += 1
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": nt / dt, "unit": "trials/s", "cores": 1, "kind": "oracle",
+                               "sample": f"{nt} trials of {min(4, ok.size)} plans (1 thread)"}
+    return out
 
 
 # Algorithmic FP64 operations per counted unit (+, -, *, /, sqrt, min/max,

@@ -42,6 +42,12 @@ namespace mpap {
 constexpr int kMcWarps = 4;                 // warps per k_mc block
 constexpr double kMcCullMargin = 1e-6;      // box/sight-line bounding-box gap that provably misses
 
+// per-warp shared memory: features [F][D], boxes [O][2D], contributions
+// [F][D] (doubles), candidate list and occluded flags [F] each (ints)
+__host__ __device__ constexpr size_t mc_warp_doubles(int d, int f_max, int o_max) {
+  return (size_t)f_max * d * 2 + (size_t)o_max * 2 * d + (size_t)f_max;
+}
+
 struct McSeg {
   double su[6];      // source node p0[D], v0[D]
   double hu[2], hv[2];  // source / destination heading (cos yaw, sin yaw)
@@ -162,9 +168,11 @@ __global__ void __launch_bounds__(kMcWarps * 32) k_mc(const double* __restrict__
                                                        unsigned long long* __restrict__ fixes) {
   extern __shared__ double mc_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* wf = mc_smem + (size_t)warp * ((size_t)f_max * D * 2 + (size_t)o_max * 2 * D);
+  double* wf = mc_smem + (size_t)warp * mc_warp_doubles(D, f_max, o_max);
   double* wb = wf + (size_t)f_max * D;       // boxes [O][2D]
   double* wc = wb + (size_t)o_max * 2 * D;   // fix contributions [F][D] in rank order
+  int* wl = reinterpret_cast<int*>(wc + (size_t)f_max * D);   // candidate / visible feature list [F]
+  int* wo = wl + f_max;                                        // candidate occluded flags [F]
   unsigned lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
   const double R2 = max_range * max_range;
@@ -259,51 +267,87 @@ __global__ void __launch_bounds__(kMcWarps * 32) k_mc(const double* __restrict__
         double hh = 0.0;
 #pragma unroll
         for (int j = 0; j < D; ++j) hh = fma(hvec[j], hvec[j], hh);
-        int kv = 0;
+        // (a) range and FOV, lane per feature -> candidate list (index order)
+        int nc = 0;
         for (int f0 = 0; f0 < F; f0 += 32) {
           const int f = f0 + lane;
-          bool vis = false;
-          double fc[D], dl[D];
+          bool cand = false;
           if (f < F) {
+            double dl[D];
             double dd = 0.0;
 #pragma unroll
-            for (int j = 0; j < D; ++j) { fc[j] = wf[f * D + j]; dl[j] = fc[j] - x[j]; dd = fma(dl[j], dl[j], dd); }
-            vis = !(dd > R2);
-            if (vis && HEUR != 0) {
+            for (int j = 0; j < D; ++j) { dl[j] = wf[f * D + j] - x[j]; dd = fma(dl[j], dl[j], dd); }
+            cand = !(dd > R2);
+            if (cand && HEUR != 0) {
               double dot = 0.0;
 #pragma unroll
               for (int j = 0; j < D; ++j) dot = fma(hvec[j], dl[j], dot);
-              if (!(hh > 0.0) || dot < 0.0 || dot * dot < cos2 * (hh * dd)) vis = false;
+              if (!(hh > 0.0) || dot < 0.0 || dot * dot < cos2 * (hh * dd)) cand = false;
             }
-            if (vis) {   // unobstructed: no box meets the sight line [x, f]
-              double inv[D], slo[D], shi[D];
+          }
+          const unsigned cm = __ballot_sync(FULLW, cand);
+          if (cand) {
+            const int pos = nc + __popc(cm & lt);
+            wl[pos] = f;
+            wo[pos] = 0;
+          }
+          nc += __popc(cm);
+        }
+        __syncwarp();
+        // (b) occlusion, lane per (candidate, box) pair: a candidate is in
+        // view iff no box meets its sight line [x, f] (order-free OR)
+        if (O > 0 && nc > 0) {
+          const int npair = nc * O;
+          int c = lane / O, o = lane - c * O;
+          for (int p0 = 0; p0 < npair; p0 += 32) {
+            if (p0 + lane < npair && !wo[c]) {
+              double fc[D], dl[D], inv[D];
+              bool sep = false;
+              const double* bx = wb + o * 2 * D;
 #pragma unroll
               for (int j = 0; j < D; ++j) {
-                inv[j] = (dl[j] != 0.0) ? 1.0 / dl[j] : 0.0;
-                slo[j] = fmin(x[j], fc[j]) - kMcCullMargin;
-                shi[j] = fmax(x[j], fc[j]) + kMcCullMargin;
+                fc[j] = wf[wl[c] * D + j];
+                dl[j] = fc[j] - x[j];
+                if (bx[j] > fmax(x[j], fc[j]) + kMcCullMargin || bx[D + j] < fmin(x[j], fc[j]) - kMcCullMargin)
+                  sep = true;
               }
-              for (int o = 0; o < O; ++o) {
-                const double* bx = wb + o * 2 * D;
-                bool sep = false;
+              if (!sep) {
 #pragma unroll
-                for (int j = 0; j < D; ++j)
-                  if (bx[j] > shi[j] || bx[D + j] < slo[j]) sep = true;
-                if (!sep && mc_seg_box<D>(x, dl, inv, bx)) { vis = false; break; }
+                for (int j = 0; j < D; ++j) inv[j] = (dl[j] != 0.0) ? 1.0 / dl[j] : 0.0;
+                if (mc_seg_box<D>(x, dl, inv, bx)) wo[c] = 1;
               }
             }
+            o += 32;
+            while (o >= O) { o -= O; ++c; }
           }
+          __syncwarp();
+        }
+        // (c) visible list in index order (in-place compaction, pos <= i)
+        int kv = 0;
+        for (int i0 = 0; i0 < nc; i0 += 32) {
+          const int i = i0 + lane;
+          const bool vis = (i < nc) && !wo[i];
+          const int f = vis ? wl[i] : 0;
           const unsigned vm = __ballot_sync(FULLW, vis);
-          if (vis) {   // (5) z_f = (f - x) + noise; contribution f - z_f at rank order
-            const int rank = kv + __popc(vm & lt);
-            const uint64_t base = ctr + (uint64_t)rank * D;
-#pragma unroll
-            for (int j = 0; j < D; ++j) {
-              const double z = dl[j] + M.sigma_vis * mc_normal(key, base + (uint64_t)j);
-              wc[rank * D + j] = fc[j] - z;
-            }
-          }
+          __syncwarp();
+          if (vis) wl[kv + __popc(vm & lt)] = f;
           kv += __popc(vm);
+        }
+        __syncwarp();
+        // (d) z_f = (f - x) + noise, normal index base + rank * d + axis,
+        // lane per (rank, axis); contribution f - z_f
+        for (int n0 = 0; n0 < kv * D; n0 += 32) {
+          const int n = n0 + lane;
+          if (n < kv * D) {
+            const int i = n / D, j = n - (n / D) * D;
+            double xj = x[0];
+#pragma unroll
+            for (int jj = 1; jj < D; ++jj)
+              if (j == jj) xj = x[jj];
+            const double fc = wf[wl[i] * D + j];
+            const double z = (fc - xj) + M.sigma_vis * mc_normal(key, ctr + (uint64_t)n);
+            wc[n] = fc - z;
+          }
         }
         __syncwarp();
         if (kv > 0) {
@@ -462,8 +506,7 @@ mpap_status mc_verify_device(const mpap_roadmap* rm, int32_t n_plans, const int3
     M.p0_vel = mc->p0_vel;
     M.delta = mc->delta;
     M.trials = mc->trials;
-    const size_t smem = sizeof(double) * kMcWarps *
-                        ((size_t)std::max(rm->f_max, 1) * d * 2 + (size_t)std::max(rm->o_max, 1) * 2 * d);
+    const size_t smem = sizeof(double) * kMcWarps * mc_warp_doubles(d, std::max(rm->f_max, 1), std::max(rm->o_max, 1));
     const int heur = rm->prm.heuristic;
     cudaError_t le;
     if (d == 3) {
