@@ -40,12 +40,17 @@ namespace mpap {
 
 #define FULLW 0xffffffffu
 constexpr int kMcWarps = 4;                 // warps per k_mc block
-constexpr double kMcCullMargin = 1e-6;      // box/sight-line bounding-box gap that provably misses
+
+constexpr float kMcCullMarginF = 1e-4f;     // box vs sight-line bounding-box gap (f32) that provably misses:
+                                            // rounding of O(100) m coordinates is < 1e-5
 
 // per-warp shared memory: features [F][D], boxes [O][2D], contributions
-// [F][D] (doubles), candidate list and occluded flags [F] each (ints)
+// [F][D] (doubles); candidate list and occluded flags [F] each, near-box
+// list [O] (ints); boxes [O][2D] and candidate sight-line boxes [F][2D]
+// (floats, for the exact culls)
 __host__ __device__ constexpr size_t mc_warp_doubles(int d, int f_max, int o_max) {
-  return (size_t)f_max * d * 2 + (size_t)o_max * 2 * d + (size_t)f_max;
+  return (size_t)f_max * d * 2 + (size_t)o_max * 2 * d + (size_t)f_max + ((size_t)o_max + 1) / 2 +
+         (size_t)o_max * d + (size_t)f_max * d;
 }
 
 struct McSeg {
@@ -173,9 +178,14 @@ __global__ void __launch_bounds__(kMcWarps * 32) k_mc(const double* __restrict__
   double* wc = wb + (size_t)o_max * 2 * D;   // fix contributions [F][D] in rank order
   int* wl = reinterpret_cast<int*>(wc + (size_t)f_max * D);   // candidate / visible feature list [F]
   int* wo = wl + f_max;                                        // candidate occluded flags [F]
+  int* wn = wo + f_max;                                        // boxes near x this step [O]
+  float* wbf = reinterpret_cast<float*>(wn + ((o_max + 1) & ~1));   // boxes, f32 [O][2D]
+  float* wsb = wbf + (size_t)o_max * 2 * D;                    // candidate sight-line boxes, f32 [F][2D]
   unsigned lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
   const double R2 = max_range * max_range;
+  const float rnear = (float)max_range + 1e-3f;
+  const float rnear2 = rnear * rnear;
   const double cos2 = fov_cos_half * fov_cos_half;
   const double q = M.sigma_imu * M.sigma_imu;
   const double rv = M.sigma_vis * M.sigma_vis;
@@ -193,7 +203,11 @@ __global__ void __launch_bounds__(kMcWarps * 32) k_mc(const double* __restrict__
       F = feat_base[env + 1] - fb;
       O = obst_base[env + 1] - ob;
       for (int i = lane; i < F * D; i += 32) wf[i] = feat_all[(size_t)fb * D + i];
-      for (int i = lane; i < O * 2 * D; i += 32) wb[i] = box_all[(size_t)ob * 2 * D + i];
+      for (int i = lane; i < O * 2 * D; i += 32) {
+        const double b = box_all[(size_t)ob * 2 * D + i];
+        wb[i] = b;
+        wbf[i] = (float)b;
+      }
       cur_env = env;
       __syncwarp();
     }
@@ -290,35 +304,66 @@ __global__ void __launch_bounds__(kMcWarps * 32) k_mc(const double* __restrict__
             const int pos = nc + __popc(cm & lt);
             wl[pos] = f;
             wo[pos] = 0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {   // bounding box of the sight line [x, f], grown
+              const double fj = wf[f * D + j];
+              wsb[pos * 2 * D + j] = (float)fmin(x[j], fj) - kMcCullMarginF;
+              wsb[pos * 2 * D + D + j] = (float)fmax(x[j], fj) + kMcCullMarginF;
+            }
           }
           nc += __popc(cm);
+        }
+        // boxes that can meet a sight line: within max_range + 1e-3 of x (every
+        // candidate is within max_range, so its sight line is in that ball)
+        int nn = 0;
+        if (nc > 0) {
+          float xf[D];
+#pragma unroll
+          for (int j = 0; j < D; ++j) xf[j] = (float)x[j];
+          for (int o0 = 0; o0 < O; o0 += 32) {
+            const int o = o0 + lane;
+            bool near = false;
+            if (o < O) {
+              float g2 = 0.0f;
+#pragma unroll
+              for (int j = 0; j < D; ++j) {
+                const float e = fmaxf(fmaxf(wbf[o * 2 * D + j] - xf[j], xf[j] - wbf[o * 2 * D + D + j]), 0.0f);
+                g2 += e * e;
+              }
+              near = g2 <= rnear2;
+            }
+            const unsigned nm = __ballot_sync(FULLW, near);
+            if (near) wn[nn + __popc(nm & lt)] = o;
+            nn += __popc(nm);
+          }
         }
         __syncwarp();
         // (b) occlusion, lane per (candidate, box) pair: a candidate is in
         // view iff no box meets its sight line [x, f] (order-free OR)
-        if (O > 0 && nc > 0) {
-          const int npair = nc * O;
-          int c = lane / O, o = lane - c * O;
+        if (nn > 0 && nc > 0) {
+          const int npair = nc * nn;
+          int c = lane / nn, o = lane - c * nn;
           for (int p0 = 0; p0 < npair; p0 += 32) {
             if (p0 + lane < npair && !wo[c]) {
-              double fc[D], dl[D], inv[D];
+              const int b = wn[o];
+              const float* bf = wbf + b * 2 * D;
+              const float* sb = wsb + c * 2 * D;
               bool sep = false;
-              const double* bx = wb + o * 2 * D;
 #pragma unroll
-              for (int j = 0; j < D; ++j) {
-                fc[j] = wf[wl[c] * D + j];
-                dl[j] = fc[j] - x[j];
-                if (bx[j] > fmax(x[j], fc[j]) + kMcCullMargin || bx[D + j] < fmin(x[j], fc[j]) - kMcCullMargin)
-                  sep = true;
-              }
+              for (int j = 0; j < D; ++j)
+                if (bf[j] > sb[D + j] || bf[D + j] < sb[j]) sep = true;
               if (!sep) {
+                double dl[D], inv[D];
 #pragma unroll
-                for (int j = 0; j < D; ++j) inv[j] = (dl[j] != 0.0) ? 1.0 / dl[j] : 0.0;
-                if (mc_seg_box<D>(x, dl, inv, bx)) wo[c] = 1;
+                for (int j = 0; j < D; ++j) {
+                  dl[j] = wf[wl[c] * D + j] - x[j];
+                  inv[j] = (dl[j] != 0.0) ? 1.0 / dl[j] : 0.0;
+                }
+                if (mc_seg_box<D>(x, dl, inv, wb + b * 2 * D)) wo[c] = 1;
               }
             }
             o += 32;
-            while (o >= O) { o -= O; ++c; }
+            while (o >= nn) { o -= nn; ++c; }
           }
           __syncwarp();
         }
