@@ -122,3 +122,50 @@ def refine_beta_min(rm: Roadmap, prob, hi: float, rel_tol: float = 1e-3, per_rou
         lo, hi = float(new_lo), float(new_hi)
         rounds += 1
     return lo, hi, rounds
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2 + NEXT-4: Alg. 1 line 4, "MC sampling and refinement of bound for
+# Alg. 3" ("the perception-heuristic bound may be updated ... and
+# the exploration rerun").  A grid of bounds runs as one batched search; the
+# distinct feasible plans run as one batched Monte Carlo launch; the certified
+# plan is the one of the largest bound whose plan passes p_hat <= alpha
+# (lowest cost among certified plans: Explore's cost is non-increasing in beta
+# up to its group approximation, so the largest passing bound is selected
+# explicitly rather than by bisection).
+# ---------------------------------------------------------------------------
+
+def refine_beta_mc(rm: Roadmap, prob, betas: Sequence[float], mc: Dict[str, Any], alpha: float, env: int = 0,
+                   path_capacity: int = 1024, stream=None) -> Dict[str, Any]:
+    betas = np.sort(np.asarray(betas, dtype=np.float64))
+    paths, res = beta_sweep(rm, prob, betas, env, path_capacity=path_capacity, stream=stream)
+    plans: Dict[tuple, int] = {}
+    for k in range(len(betas)):
+        if res["status"][k] == 0:
+            plans.setdefault(tuple(paths[k][: res["path_len"][k]].tolist()), len(plans))
+    table = []
+    best = None
+    if plans:
+        keys = list(plans.keys())
+        cap = max(len(p) for p in keys)
+        pa = np.zeros((len(keys), cap), dtype=np.int32)
+        for i, p in enumerate(keys):
+            pa[i, : len(p)] = p
+        mres, _, _ = mpap_mc_verify_batch(rm, np.full(len(keys), env, np.int32), pa, [len(p) for p in keys], mc,
+                                          per_trial=False, stream=stream)
+        for k in range(len(betas)):
+            row = {"beta": float(betas[k]), "status": int(res["status"][k])}
+            if res["status"][k] == 0:
+                i = plans[tuple(paths[k][: res["path_len"][k]].tolist())]
+                row.update(cost=float(res["cost"][k]), h=float(res["h"][k]), p_hat=float(mres["p_hat"][i]),
+                           plan=i, passed=bool(mres["p_hat"][i] <= alpha))
+                if row["passed"]:
+                    best = k
+            table.append(row)
+    else:
+        table = [{"beta": float(b), "status": int(s)} for b, s in zip(betas, res["status"])]
+    out = {"table": table, "certified": best is not None}
+    if best is not None:
+        out.update(beta=float(betas[best]), path=paths[best][: res["path_len"][best]].copy(),
+                   cost=float(res["cost"][best]), p_hat=table[best]["p_hat"])
+    return out

@@ -26,7 +26,7 @@ DEFAULT_MC: Dict[str, Any] = {
     "k_d": math.sqrt(8.0),
     "p0_pos": 1e-4,
     "p0_vel": 1e-4,
-    "delta": 0.5,            # m, localisation error bound (Eq. 1)
+    "delta": 0.3,            # m, localisation error bound (Eq. 1); profiles/r01/mc_sweep_c5.json
 }
 
 

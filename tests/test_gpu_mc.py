@@ -110,3 +110,31 @@ def test_mc_c5_batch_parity(mp, orc):
             assert me[i, t] == o["max_err"], (e, t)
         assert mres["steps"][i] == orc.mc_trial(probs[e], path, mc, 0)["steps"]
     rm.free()
+
+
+def test_refine_beta_mc_parity(mp, orc):
+    """Alg. 1 line 4 (P:180, P:291): bound grid -> plans -> MC certificate;
+    the GPU's table (status, cost, p_hat per bound) and its certified bound
+    equal the oracle's search + MC over the same grid."""
+    prob = c3_small()
+    rm = mp.pb.build_problem(prob)
+    orm = orc.build_roadmap(prob)
+    mc = mc_params(trials=64, delta=0.15)
+    betas = [2.0, 3.0, 4.5, 6.0, float("inf")]
+    alpha = 0.25
+    g = mp.pb.refine_beta_mc(rm, prob, betas, mc, alpha)
+    best = None
+    for row, beta in zip(g["table"], betas):
+        o = orc.search(orm, prob, beta)
+        assert row["status"] == o["status"], beta
+        if o["status"] != 0:
+            continue
+        assert np.float32(row["cost"]) == o["cost"]
+        om = orc.mc_verify(prob, o["path"], mc)
+        assert row["p_hat"] == om["p_hat"], (beta, row["p_hat"], om["p_hat"])
+        if om["p_hat"] <= alpha:
+            best = beta
+    assert g["certified"] == (best is not None)
+    if best is not None:
+        assert g["beta"] == best
+    rm.free()
