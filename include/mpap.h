@@ -80,7 +80,15 @@ typedef struct {
   int32_t edge_peaks;     /* 0 or 1: also compute the per-edge peaks (S, C) that
                              MPAP_SEARCH_FORALL_T needs (NEXT-3; costs ~2.5% of the
                              build: two more running maxima per heuristic step)    */
-  int32_t reserved;       /* must be 0                                              */
+  int32_t lazy_edges;     /* 0 or 1 (NEXT-1 part i): the build
+                             computes Near + Cost only; collision bits and heuristic
+                             summaries of a row are evaluated when the single-query
+                             search (mpap_search*) first expands a plan at that
+                             node -- the search reads the same (coll, s, c), so the
+                             plan is identical.  Every other call on the roadmap
+                             (batch search, export, update, Monte Carlo) first
+                             evaluates all remaining rows.  Single environment
+                             only (n_envs == 1).                                    */
 } mpap_params;
 
 /* Opaque, device-resident, immutable after build: B >= 1 environments, each
@@ -333,6 +341,10 @@ mpap_status mpap_mc_verify_batch(const mpap_roadmap *rm, int32_t n_plans, const 
 mpap_status mpap_mc_verify(const mpap_roadmap *rm, int32_t env, const int32_t *path, int32_t path_len,
                            const mpap_mc_params *mc, uint64_t trial0, double *max_err, double *max_dev,
                            mpap_mc_result *result, void *cuda_stream);
+
+/* Lazy roadmaps (mpap_params.lazy_edges): rows of env whose collision bits and
+ * heuristic summaries have been evaluated so far (n for an eager roadmap). */
+mpap_status mpap_roadmap_rows_evaluated(const mpap_roadmap *rm, int32_t env, int64_t *rows);
 
 /* Releases the roadmap's device memory (NULL is a no-op).  Waits for the
  * device to be idle first (searches of this roadmap may be in flight). */

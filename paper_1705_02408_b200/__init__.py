@@ -46,6 +46,7 @@ EXPORTED_SYMBOLS = [
     "mpap_last_error", "mpap_launch_count", "mpap_prof_enable", "mpap_prof_reset", "mpap_prof_read",
     "mpap_roadmap_work", "mpap_search_ex", "mpap_search_batch_ex", "mpap_roadmap_export_peaks",
     "mpap_roadmap_set_peaks", "mpap_roadmap_update", "mpap_mc_verify", "mpap_mc_verify_batch",
+    "mpap_roadmap_rows_evaluated",
 ]
 
 
@@ -63,7 +64,7 @@ class mpap_params(C.Structure):
         ("control_weight", C.c_double), ("nominal_speed", C.c_double), ("dt", C.c_double),
         ("collision_dt", C.c_double), ("n_f", C.c_double), ("fov_cos_half", C.c_double),
         ("max_range", C.c_double), ("mlp", C.POINTER(C.c_double)), ("mlp_gain", C.c_double),
-        ("v_ref", C.c_double), ("w_ref", C.c_double), ("edge_peaks", C.c_int32), ("reserved", C.c_int32),
+        ("v_ref", C.c_double), ("w_ref", C.c_double), ("edge_peaks", C.c_int32), ("lazy_edges", C.c_int32),
     ]
 
 
@@ -119,6 +120,7 @@ _lib.mpap_mc_verify_batch.argtypes = [_vp, C.c_int32, _vp, _vp, C.c_int32, _vp, 
                                       C.c_uint64, _vp, _vp, _vp, _vp]
 _lib.mpap_mc_verify.argtypes = [_vp, C.c_int32, _vp, C.c_int32, C.POINTER(mpap_mc_params), C.c_uint64, _vp, _vp,
                                 _vp, _vp]
+_lib.mpap_roadmap_rows_evaluated.argtypes = [_vp, C.c_int32, C.POINTER(C.c_int64)]
 _lib.mpap_roadmap_export_peaks.argtypes = [_vp, C.c_int32, _vp, _vp]
 _lib.mpap_roadmap_set_peaks.argtypes = [_vp, _vp, _vp]
 _lib.mpap_roadmap_update.argtypes = [_vp, C.c_int32, _vp, C.c_int32, _vp, C.c_int32, C.c_int32, _vp,
@@ -205,11 +207,15 @@ class Roadmap:
 
 
 def make_params(pos_dim: int, dynamics: int, has_heading: int, heuristic: int, ws_lo, ws_hi,
-                mlp: Optional[np.ndarray], edge_peaks: bool = False, **p) -> mpap_params:
+                mlp: Optional[np.ndarray], edge_peaks: bool = False, lazy_edges: bool = False,
+                **p) -> mpap_params:
     """Pack an mpap_params struct (the MLP array must outlive the call that uses it).
-    ``edge_peaks`` also computes the per-edge peaks MPAP_SEARCH_FORALL_T needs."""
+    ``edge_peaks`` also computes the per-edge peaks MPAP_SEARCH_FORALL_T needs;
+    ``lazy_edges`` defers collision + heuristic of each row to its first
+    expansion by the single-query search (NEXT-1 part i)."""
     prm = mpap_params()
     prm.edge_peaks = 1 if edge_peaks else 0
+    prm.lazy_edges = 1 if lazy_edges else 0
     prm.pos_dim, prm.dynamics, prm.has_heading, prm.heuristic = pos_dim, dynamics, has_heading, heuristic
     for k in range(3):
         prm.ws_lo[k] = float(ws_lo[k]) if k < len(ws_lo) else 0.0
@@ -222,11 +228,11 @@ def make_params(pos_dim: int, dynamics: int, has_heading: int, heuristic: int, w
     return prm
 
 
-def params_from_problem(prob, edge_peaks: bool = False) -> tuple:
+def params_from_problem(prob, edge_peaks: bool = False, lazy_edges: bool = False) -> tuple:
     """(mpap_params, keepalive) from a synth.Problem (marshalling only)."""
     mlp = np.ascontiguousarray(prob.mlp, dtype=np.float64)
     prm = make_params(prob.pos_dim, prob.dynamics, prob.has_heading, prob.heuristic, prob.ws_lo, prob.ws_hi,
-                      mlp, edge_peaks=edge_peaks, **prob.params)
+                      mlp, edge_peaks=edge_peaks, lazy_edges=lazy_edges, **prob.params)
     return prm, mlp
 
 
@@ -521,3 +527,13 @@ def mpap_mc_verify(rm: Roadmap, env: int, path, mc: Dict[str, Any], trial0: int 
     r = res[0]
     return {"p_hat": float(r["p_hat"]), "exceed": int(r["exceed"]), "trials": int(r["trials"]),
             "steps": int(r["steps"]), "fixes": int(r["fixes"]), "max_err": me, "max_dev": md}
+
+
+def mpap_roadmap_rows_evaluated(rm: Roadmap, env: int = 0) -> int:
+    """Rows of env whose collision bits and heuristic summaries exist (lazy
+    roadmaps evaluate rows on first expansion; eager ones: all n)."""
+    v = C.c_int64()
+    s = _lib.mpap_roadmap_rows_evaluated(rm.handle, int(env), C.byref(v))
+    if s != MPAP_OK:
+        raise MpapError(s, "mpap_roadmap_rows_evaluated")
+    return int(v.value)

@@ -1316,6 +1316,53 @@ cudaError_t launch_near(dim3 grid, cudaStream_t st, const mpap_roadmap* rm, cons
   return cudaGetLastError();
 }
 
+// NEXT-1 part i (lazy roadmap): the edge records of every row from the
+// neighbour scratch -- dst and w (coll = 0, s = c = 0 until the row is
+// evaluated), tau and the source row -- warp per row.
+__global__ void k_lazy_init(const NearRec* __restrict__ scratch, int cap, const int64_t* __restrict__ row_ptr,
+                            int64_t N, EdgeRec* __restrict__ edges, double* __restrict__ tau_arr,
+                            int32_t* __restrict__ esrc, float2* __restrict__ peak) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < N;
+       row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t e0 = row_ptr[row], e1 = row_ptr[row + 1];
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const NearRec rec = scratch[row * (int64_t)cap + (e - e0)];
+      EdgeRec er;
+      er.dst_coll = (uint32_t)rec.v;
+      er.w = rec.w;
+      er.s = 0.0f;
+      er.c = 0.0f;
+      edges[e] = er;
+      tau_arr[e] = rec.tau;
+      esrc[e] = (int32_t)row;
+      if (peak) peak[e] = make_float2(0.0f, 0.0f);
+    }
+  }
+}
+
+// Items {row, edge} of the requested rows (or of every row not yet ready),
+// warp per row; marks the rows ready (the evaluation that follows is stream-
+// ordered before any later search).
+__global__ void k_row_items(const int32_t* __restrict__ rows, int64_t n_req, int64_t N,
+                            const int64_t* __restrict__ row_ptr, int32_t* __restrict__ ready,
+                            longlong2* __restrict__ items, unsigned long long* __restrict__ n_items) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = rows ? n_req : N;
+  for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < n;
+       k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t row = rows ? rows[k] : k;
+    if (ready[row] == 1) continue;
+    const int64_t e0 = row_ptr[row], e1 = row_ptr[row + 1];
+    unsigned long long base = 0;
+    if (lane == 0 && e1 > e0) base = atomicAdd(n_items, (unsigned long long)(e1 - e0));
+    base = __shfl_sync(FULL, base, 0);
+    for (int64_t e = e0 + lane; e < e1; e += 32) items[base + (e - e0)] = make_longlong2(row, e);
+    __syncwarp();
+    if (lane == 0) ready[row] = 1;
+  }
+}
+
 struct EdgeWork {            // what one k_edges launch processes
   const NearRec* scratch;    // build mode: neighbour scratch (cap entries per row)
   int cap;
@@ -1518,7 +1565,21 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
   unsigned long long* d_next = nullptr;   // [0..1] item counters of the two edge phases, [2] kv slots, [3] free edges
   CK(cudaMallocAsync(&d_next, 4 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(d_next, 0, 4 * sizeof(unsigned long long), st));
-  if (rm->nnz_total > 0) {
+  if (rm->lazy) {   // NEXT-1 part i: Near + Cost only; rows are evaluated on demand
+    rm->d_ready = static_cast<int32_t*>(rm_alloc(sizeof(int32_t) * std::max<int64_t>(N, 1), st));
+    if (!rm->d_ready) return set_error(MPAP_ERR_OUT_OF_MEMORY, "ready flags allocation failed");
+    CK(cudaMemsetAsync(rm->d_ready, 0, sizeof(int32_t) * N, st));
+    if (rm->nnz_total > 0) {
+      ProfScope ps("k_lazy_init", st);
+      k_lazy_init<<<(unsigned)std::min<int64_t>((N + 7) / 8, 148 * 16), 256, 0, st>>>(
+          d_scr, cap, rm->d_row_ptr, N, rm->d_edges, rm->d_tau, rm->d_esrc, rm->d_peak);
+      CK(cudaGetLastError());
+      note_launch();
+    }
+    std::vector<unsigned long long> fr(B);
+    for (int b = 0; b < B; ++b) fr[b] = (unsigned long long)(bounds[b + 1] - bounds[b]);   // coll = 0 until evaluated
+    CK(cudaMemcpyAsync(d_free, fr.data(), sizeof(unsigned long long) * B, cudaMemcpyHostToDevice, st));
+  } else if (rm->nnz_total > 0) {
     EdgeWork ew{d_scr, cap, nullptr, 0, d_free, d_work, d_next, nullptr, nullptr, d_next + 2, nullptr, d_next + 3};
     ew.flist = static_cast<longlong2*>(workspace(st, WS_FLIST, sizeof(longlong2) * rm->nnz_total));
     if (!ew.flist) return set_error(MPAP_ERR_OUT_OF_MEMORY, "free-edge list workspace allocation failed");
@@ -1621,6 +1682,50 @@ mpap_status update_roadmap_device(mpap_roadmap* rm, int env, const std::vector<d
   CK(cudaFreeAsync(d_ctr, st));
   CK(cudaStreamSynchronize(st));
   if (n_reeval) *n_reeval = (int64_t)n_items;
+  return MPAP_OK;
+}
+
+mpap_status evaluate_rows_device(mpap_roadmap* rm, const int32_t* d_rows, int64_t n_req, cudaStream_t st) {
+  if (!rm->lazy || rm->nnz_total == 0) return MPAP_OK;
+  const int64_t N = rm->node_base[rm->B];
+  if (d_rows && n_req <= 0) return MPAP_OK;
+  longlong2* d_items = nullptr;
+  unsigned long long* d_ctr = nullptr;   // [0] n_items, [1..2] item counters, [3] kv slots, [4..] work
+  CK(cudaMallocAsync(&d_items, sizeof(longlong2) * rm->nnz_total, st));
+  CK(cudaMallocAsync(&d_ctr, sizeof(unsigned long long) * (4 + W_NUM), st));
+  CK(cudaMemsetAsync(d_ctr, 0, sizeof(unsigned long long) * (4 + W_NUM), st));
+  {
+    ProfScope ps("k_row_items", st);
+    const int64_t n = d_rows ? n_req : N;
+    k_row_items<<<(unsigned)std::min<int64_t>((n + 7) / 8, 148 * 16), 256, 0, st>>>(d_rows, n_req, N, rm->d_row_ptr,
+                                                                                    rm->d_ready, d_items, d_ctr);
+    CK(cudaGetLastError());
+  }
+  note_launch();
+  unsigned long long n_items = 0;
+  CK(cudaMemcpyAsync(&n_items, d_ctr, sizeof(n_items), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (n_items > 0) {
+    unsigned long long* d_free = nullptr;
+    CK(cudaMallocAsync(&d_free, sizeof(unsigned long long) * rm->B, st));
+    CK(cudaMemsetAsync(d_free, 0, sizeof(unsigned long long) * rm->B, st));
+    EdgeWork ew{nullptr, 0, d_items, (int64_t)n_items, d_free, d_ctr + 4 - W_EDGES, d_ctr + 1, nullptr, nullptr,
+                d_ctr + 3, nullptr, nullptr};
+    ew.koff = static_cast<long long*>(workspace(st, WS_KOFF, sizeof(long long) * rm->nnz_total));
+    if (!ew.koff) return set_error(MPAP_ERR_OUT_OF_MEMORY, "kv offset workspace allocation failed");
+    CK(edge_phases(edges_smem(rm), st, rm, ew));
+    std::vector<unsigned long long> delta(rm->B), work(W_NUM - W_EDGES);
+    CK(cudaMemcpyAsync(delta.data(), d_free, sizeof(unsigned long long) * rm->B, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(work.data(), d_ctr + 4, sizeof(unsigned long long) * (W_NUM - W_EDGES), cudaMemcpyDeviceToHost,
+                       st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaFreeAsync(d_free, st));
+    for (int b = 0; b < rm->B; ++b) rm->nnz_free[b] += (int64_t)(long long)delta[b];
+    for (int i = W_EDGES; i < W_NUM; ++i) rm->work[i] += work[i - W_EDGES];
+  }
+  CK(cudaFreeAsync(d_items, st));
+  CK(cudaFreeAsync(d_ctr, st));
+  CK(cudaStreamSynchronize(st));
   return MPAP_OK;
 }
 

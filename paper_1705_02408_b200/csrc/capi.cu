@@ -229,6 +229,13 @@ using namespace mpap;
 
 static bool is_fin(double x) { return std::isfinite(x); }
 
+// Lazy roadmaps (NEXT-1 part i): calls other than the single-query search see
+// a fully evaluated roadmap -- evaluate every remaining row first.
+static mpap_status ensure_evaluated(const mpap_roadmap* rm, cudaStream_t st) {
+  if (!rm->lazy) return MPAP_OK;
+  return evaluate_rows_device(const_cast<mpap_roadmap*>(rm), nullptr, 0, st);
+}
+
 template <typename T>
 static cudaError_t rm_alloc_into(T** out, size_t bytes, cudaStream_t st) {
   *out = static_cast<T*>(rm_alloc(bytes, st));
@@ -254,8 +261,8 @@ static mpap_status validate_params(const mpap_params* p, double r) {
   if (!(p->fov_cos_half > 0.0) || p->fov_cos_half > 1.0)
     return set_error(MPAP_ERR_INVALID_ARGUMENT, "fov_cos_half must be in (0, 1]");
   if (!is_fin(p->mlp_gain)) return set_error(MPAP_ERR_INVALID_ARGUMENT, "mlp_gain not finite");
-  if ((p->edge_peaks != 0 && p->edge_peaks != 1) || p->reserved != 0)
-    return set_error(MPAP_ERR_INVALID_ARGUMENT, "edge_peaks must be 0 or 1 and reserved 0");
+  if ((p->edge_peaks != 0 && p->edge_peaks != 1) || (p->lazy_edges != 0 && p->lazy_edges != 1))
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "edge_peaks and lazy_edges must be 0 or 1");
   for (int k = 0; k < p->pos_dim; ++k)
     if (!(p->ws_lo[k] < p->ws_hi[k])) return set_error(MPAP_ERR_INVALID_ARGUMENT, "workspace lo >= hi");
   return MPAP_OK;
@@ -311,7 +318,7 @@ void mpap_roadmap_free(mpap_roadmap* rm) {
   // wait for the device, then hand the memory back to the stream-ordered pool
   cudaDeviceSynchronize();
   void* ptrs[] = {rm->d_samples, rm->d_obst, rm->d_feat, rm->d_obst_base, rm->d_feat_base, rm->d_node_base,
-                  rm->d_row_ptr, rm->d_edges, rm->d_peak, rm->d_tau, rm->d_esrc};
+                  rm->d_row_ptr, rm->d_edges, rm->d_peak, rm->d_tau, rm->d_esrc, rm->d_ready};
   for (void* p : ptrs) rm_release(p);   // device is idle: safe to reuse from any stream
   cudaSetDevice(cur);
   delete rm;
@@ -328,6 +335,7 @@ mpap_status mpap_build_roadmap_batch(int32_t n_envs, const double* samples, cons
   if (mem != MPAP_MEM_HOST && mem != MPAP_MEM_DEVICE) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad mem space");
   mpap_status s = validate_params(params, r);
   if (s != MPAP_OK) return s;
+  if (params->lazy_edges && n_envs != 1) return set_error(MPAP_ERR_INVALID_ARGUMENT, "lazy_edges needs n_envs == 1");
   const int d = params->pos_dim;
   const int need = d * (params->dynamics == MPAP_DOUBLE_INTEGRATOR ? 2 : 1) + (params->has_heading ? 2 : 0);
   if (row_stride < need || row_stride > 8)
@@ -368,6 +376,7 @@ mpap_status mpap_build_roadmap_batch(int32_t n_envs, const double* samples, cons
   P.heuristic = params->heuristic;
   P.stride = row_stride;
   P.edge_peaks = params->edge_peaks;
+  rm->lazy = params->lazy_edges != 0;
   P.hoff = d * (params->dynamics == MPAP_DOUBLE_INTEGRATOR ? 2 : 1);
   for (int k = 0; k < 3; ++k) {
     P.ws_lo[k] = params->ws_lo[k];
@@ -509,6 +518,10 @@ mpap_status mpap_roadmap_info(const mpap_roadmap* rm, int32_t env, int32_t* n, i
 
 mpap_status mpap_roadmap_export(const mpap_roadmap* rm, int32_t env, int32_t* row_ptr, uint32_t* dst_coll, float* w,
                                 float* s, float* c) {
+  if (rm) {
+    mpap_status se = ensure_evaluated(rm, nullptr);
+    if (se != MPAP_OK) return se;
+  }
   if (!rm || env < 0 || env >= rm->B || !row_ptr)
     return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad roadmap/env/row_ptr");
   int cur = 0;
@@ -604,6 +617,10 @@ mpap_status mpap_roadmap_update(mpap_roadmap* rm, int32_t env, const double* obs
   cudaGetDevice(&cur);
   if (cur != rm->device) return set_error(MPAP_ERR_INVALID_ARGUMENT, "roadmap bound to another device");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  {
+    mpap_status se = ensure_evaluated(rm, st);
+    if (se != MPAP_OK) return se;
+  }
   const int d = rm->prm.pos_dim;
   std::vector<double> nbx((size_t)n_obstacles * 2 * d), nft((size_t)n_features * d);
   const cudaMemcpyKind kind = (mem == MPAP_MEM_HOST) ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost;
@@ -653,6 +670,10 @@ mpap_status mpap_roadmap_update(mpap_roadmap* rm, int32_t env, const double* obs
 }
 
 mpap_status mpap_roadmap_export_peaks(const mpap_roadmap* rm, int32_t env, float* S, float* C) {
+  if (rm) {
+    mpap_status se = ensure_evaluated(rm, nullptr);
+    if (se != MPAP_OK) return se;
+  }
   if (!rm || env < 0 || env >= rm->B) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad roadmap/env");
   if (!rm->d_peak) return set_error(MPAP_ERR_INVALID_ARGUMENT, "roadmap carries no peaks");
   int cur = 0;
@@ -825,8 +846,26 @@ mpap_status mpap_mc_verify_batch(const mpap_roadmap* rm, int32_t n_plans, const 
     for (int32_t j = 0; j < path_lens[p]; ++j)
       if (path[j] < 0 || path[j] >= rm->n[envs[p]]) return set_error(MPAP_ERR_INVALID_ARGUMENT, "node out of range");
   }
+  mpap_status se = ensure_evaluated(rm, static_cast<cudaStream_t>(cuda_stream));
+  if (se != MPAP_OK) return se;
   return mc_verify_device(rm, n_plans, envs, paths, path_stride, path_lens, mc, trial0, max_err, max_dev, results,
                           static_cast<cudaStream_t>(cuda_stream));
+}
+
+mpap_status mpap_roadmap_rows_evaluated(const mpap_roadmap* rm, int32_t env, int64_t* rows) {
+  if (!rm || !rows || env < 0 || env >= rm->B) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad roadmap/env/rows");
+  if (!rm->lazy) {
+    *rows = rm->n[env];
+    return MPAP_OK;
+  }
+  std::vector<int32_t> r(rm->n[env]);
+  cudaError_t e = cudaMemcpy(r.data(), rm->d_ready + rm->node_base[env], sizeof(int32_t) * r.size(),
+                             cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_error(e, "rows_evaluated");
+  int64_t c = 0;
+  for (int32_t x : r) c += (x == 1);
+  *rows = c;
+  return MPAP_OK;
 }
 
 mpap_status mpap_mc_verify(const mpap_roadmap* rm, int32_t env, const int32_t* path, int32_t path_len,

@@ -70,6 +70,8 @@ struct mpap_roadmap {
   int32_t* d_esrc = nullptr;       // [nnz_total] global source row of each edge (k_fold)
   float2* d_peak = nullptr;        // [nnz_total] (S, C) prefix maxima per edge (NEXT-3); may be null (import)
   int64_t nnz_total = 0;
+  bool lazy = false;               // NEXT-1 part i: rows evaluated on first expansion (mpap_params.lazy_edges)
+  int32_t* d_ready = nullptr;      // lazy: [sum n] 0 = not evaluated, 2 = requested, 1 = evaluated
   unsigned long long work[mpap::kWorkCounters] = {};  // build work counters (mpap_roadmap_work)
   cudaStream_t alloc_stream = nullptr;                 // stream the device arrays were allocated on
   // search capacities learned from earlier regrow-and-retry rounds on this
@@ -133,6 +135,11 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st);
 // (host arrays); rm's obstacle/feature arrays already hold the new sets.
 mpap_status update_roadmap_device(mpap_roadmap* rm, int env, const std::vector<double>& cbox,
                                   const std::vector<double>& cfeat, int64_t* n_reeval, cudaStream_t st);
+
+// NEXT-1 part i: evaluate collision + heuristic of the listed global rows
+// (device array d_rows[n_req]; d_rows == nullptr: every row not yet
+// evaluated) of a lazy roadmap, marking them ready.
+mpap_status evaluate_rows_device(mpap_roadmap* rm, const int32_t* d_rows, int64_t n_req, cudaStream_t st);
 
 // search (search_kernels.cu)
 struct QueryDesc {

@@ -96,6 +96,13 @@ struct SearchArgs {
   mpap_result* results;
   mpap_wave* waves;
   int waves_cap;
+  // NEXT-1 part i (lazy roadmap, whole-grid single query): rows are evaluated
+  // on first expansion; the kernel suspends before a wave whose heads have
+  // unevaluated rows and resumes after the host evaluated them
+  int32_t* ready;   // [sum n] 1 = evaluated (null: eager roadmap)
+  int32_t* req;     // requested global rows
+  int* nreq;
+  int resume;
 };
 
 struct Ctl {
@@ -104,6 +111,7 @@ struct Ctl {
   unsigned long long relax, bpass, tcount, ssum, inserted, killed;
   unsigned long long relax_total, inserted_total;
   int waves;
+  int suspended, pswap;   // lazy: suspended before a wave; pending lists swapped at suspension
   unsigned long long best_key;
   int nties;
   int ties[32];
@@ -249,51 +257,71 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
   mpap_result* R = A.results + q;
 
   // ---- a5: init (A3.1-A3.4) ----
-  if (leader) {
-    S->gsize = 1; S->psize = 0; S->nsize = 0; S->ncand = 0; S->ntouched = 0; S->nlabels = 1; S->calloc = 0;
-    S->goal_in_g = 0; S->overflow = 0; S->any_goal = 0; S->i = 0; S->minb = LLONG_MAX;
-    S->relax_total = 0; S->inserted_total = 0; S->waves = 0;
-  }
-  team.sync();
-  bool mygoal = false;
-  for (int x = tid; x < n; x += nthr) {
-    sn[x] = 0;
-    ccnt[x] = 0;
-    if (TRACE) stamp[x] = -1;
-    const double* p = A.samples + (nbase + x) * A.stride;
-    bool in = true;
-    for (int k = 0; k < d; ++k)
-      if (p[k] < Q.goal_lo[k] || p[k] > Q.goal_hi[k]) in = false;
-    goal[x] = in ? 1 : 0;
-    mygoal |= in;
-  }
-  if (__any_sync(FULLM, mygoal) && lane == 0) S->any_goal = 1;
-  team.sync();
-  if (leader) {
-    labels[0] = make_int4(Q.start, -1, __float_as_int(0.0f), __float_as_int(0.0f));
-    lstate[0] = L_OPEN;
-    sch[(size_t)Q.start * C.K] = make_float2(0.0f, 0.0f);   // buffer 0
-    sid[(size_t)Q.start * C.K] = 0;
-    sn[Q.start] = 1;
-    G[0] = 0;
-    S->goal_in_g = goal[Q.start];
-  }
-  team.sync();
-  if (!vld(S->any_goal)) {
+  if (!A.resume) {
     if (leader) {
-      mpap_result r{};
-      r.status = MPAP_ERR_NO_GOAL_NODE;
-      *R = r;
+      S->gsize = 1; S->psize = 0; S->nsize = 0; S->ncand = 0; S->ntouched = 0; S->nlabels = 1; S->calloc = 0;
+      S->goal_in_g = 0; S->overflow = 0; S->any_goal = 0; S->i = 0; S->minb = LLONG_MAX;
+      S->relax_total = 0; S->inserted_total = 0; S->waves = 0; S->suspended = 0; S->pswap = 0;
     }
-    return;
+    team.sync();
+    bool mygoal = false;
+    for (int x = tid; x < n; x += nthr) {
+      sn[x] = 0;
+      ccnt[x] = 0;
+      if (TRACE) stamp[x] = -1;
+      const double* p = A.samples + (nbase + x) * A.stride;
+      bool in = true;
+      for (int k = 0; k < d; ++k)
+        if (p[k] < Q.goal_lo[k] || p[k] > Q.goal_hi[k]) in = false;
+      goal[x] = in ? 1 : 0;
+      mygoal |= in;
+    }
+    if (__any_sync(FULLM, mygoal) && lane == 0) S->any_goal = 1;
+    team.sync();
+    if (leader) {
+      labels[0] = make_int4(Q.start, -1, __float_as_int(0.0f), __float_as_int(0.0f));
+      lstate[0] = L_OPEN;
+      sch[(size_t)Q.start * C.K] = make_float2(0.0f, 0.0f);   // buffer 0
+      sid[(size_t)Q.start * C.K] = 0;
+      sn[Q.start] = 1;
+      G[0] = 0;
+      S->goal_in_g = goal[Q.start];
+    }
+    team.sync();
+    if (!vld(S->any_goal)) {
+      if (leader) {
+        mpap_result r{};
+        r.status = MPAP_ERR_NO_GOAL_NODE;
+        *R = r;
+      }
+      return;
+    }
   }
-
   // ---- wave loop (A3.5-A3.19) ----
-  int wave = 0;
+  int wave = A.resume ? vld(S->waves) : 0;
+  int pswap = A.resume ? vld(S->pswap) : 0;
+  if (pswap) { int32_t* tmp = pend; pend = pend2; pend2 = tmp; }
+  if (A.resume) {
+    team.sync();
+    if (leader) S->suspended = 0;
+    team.sync();
+  }
   while (true) {
     if (vld(S->goal_in_g) || vld(S->gsize) == 0) break;     // A3.5 (G = {} <=> P_open = {} here)
     const int gsize = vld(S->gsize);
     const long long i_cur = vld(S->i);
+    if (A.ready) {   // lazy roadmap: every head of G_i must have its row evaluated
+      for (int k = tid; k < gsize; k += nthr) {
+        const int64_t row = nbase + labels[G[k]].x;
+        if (vld(A.ready[row]) != 1 && atomicCAS(&A.ready[row], 0, 2) == 0)
+          A.req[atomicAdd(A.nreq, 1)] = (int32_t)row;
+      }
+      team.sync();
+      if (vld(*A.nreq) > 0) {
+        if (leader) { S->suspended = 1; S->pswap = pswap; }
+        return;
+      }
+    }
     team.sync();
     if (leader) {
       S->relax = 0; S->bpass = 0; S->tcount = 0; S->ssum = 0; S->inserted = 0; S->killed = 0;
@@ -574,6 +602,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
       // swap pending lists
       if (leader) { S->psize = vld(S->nsize); S->i = inext; }
       int32_t* tmp = pend; pend = pend2; pend2 = tmp;
+      pswap ^= 1;
     }
     team.sync();
     ++wave;
@@ -855,7 +884,45 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     A.n_env = d_nenv;
     CKS(cudaMemcpyAsync(d_qidx, todo.data(), sizeof(int32_t) * nrun, cudaMemcpyHostToDevice, st));
     CKS(cudaMemsetAsync(d_work, 0, sizeof(int), st));
-    {
+    // lazy roadmap (NEXT-1 part i): the whole-grid search suspends before a
+    // wave whose heads have unevaluated rows; evaluate them and resume
+    if (rm->lazy && !grid_mode) {
+      mpap_status se = evaluate_rows_device(const_cast<mpap_roadmap*>(rm), nullptr, 0, st);
+      if (se != MPAP_OK) return se;
+    }
+    const bool lazy_grid = rm->lazy && grid_mode;
+    int32_t* d_req = nullptr;
+    int* d_nreq = nullptr;
+    if (lazy_grid) {
+      CKS(cudaMallocAsync(&d_req, sizeof(int32_t) * std::max(rm->n_max, 1), st));
+      CKS(cudaMallocAsync(&d_nreq, sizeof(int), st));
+      A.ready = rm->d_ready;
+      A.req = d_req;
+      A.nreq = d_nreq;
+    }
+    A.resume = 0;
+    if (lazy_grid) {
+      Ctl* d_ctl = reinterpret_cast<Ctl*>(static_cast<char*>(base) + ((sb_slots + 255) & ~size_t(255)));
+      for (;;) {
+        CKS(cudaMemsetAsync(d_nreq, 0, sizeof(int), st));
+        {
+          ProfScope ps("k_search", st);
+          void* args[] = {&A, &d_ctl};
+          const void* fn = trace ? (const void*)k_search_grid<true> : (const void*)k_search_grid<false>;
+          CKS(cudaLaunchCooperativeKernel(fn, dim3(nsm * occ_grid), dim3(kST), args, 0, st));
+        }
+        note_launch();
+        int nreq = 0;
+        CKS(cudaMemcpyAsync(&nreq, d_nreq, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CKS(cudaStreamSynchronize(st));
+        if (nreq == 0) break;
+        mpap_status se = evaluate_rows_device(const_cast<mpap_roadmap*>(rm), d_req, nreq, st);
+        if (se != MPAP_OK) return se;
+        A.resume = 1;
+      }
+      CKS(cudaFreeAsync(d_req, st));
+      CKS(cudaFreeAsync(d_nreq, st));
+    } else {
       ProfScope ps("k_search", st);
       Ctl* d_ctl = reinterpret_cast<Ctl*>(static_cast<char*>(base) + ((sb_slots + 255) & ~size_t(255)));
       if (grid_mode) {
@@ -882,8 +949,8 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
       } else {
         k_search<false><<<nslots, kST, 0, st>>>(A);
       }
+      note_launch();
     }
-    note_launch();
     CKS(cudaGetLastError());
     CKS(cudaFreeAsync(d_nenv, st));
     CKS(cudaMemcpyAsync(hres.data(), d_res, sizeof(mpap_result) * nq, cudaMemcpyDeviceToHost, st));

@@ -13,8 +13,8 @@ from . import (MPAP_MEM_DEVICE, Roadmap, mpap_build_roadmap, mpap_build_roadmap_
                mpap_search, mpap_search_batch, params_from_problem)
 
 
-def build_problem(prob, stream=None, edge_peaks: bool = False) -> Roadmap:
-    prm, keep = params_from_problem(prob, edge_peaks)
+def build_problem(prob, stream=None, edge_peaks: bool = False, lazy_edges: bool = False) -> Roadmap:
+    prm, keep = params_from_problem(prob, edge_peaks, lazy_edges)
     obst = prob.obstacles if prob.obstacles.size else None
     feat = prob.features if prob.features.size else None
     rm = mpap_build_roadmap(prob.samples, obst if obst is not None else np.zeros((0, 2 * prob.pos_dim)),
