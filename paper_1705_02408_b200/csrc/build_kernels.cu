@@ -632,6 +632,47 @@ __device__ __noinline__ double mlp_out0(const double* w, double z0, double z1, d
 }
 
 
+// mlp_out0 for two inputs that share z1 (two steps of one edge): every weight
+// read from shared memory feeds two DFMAs (k_fold is bound by the shared-
+// memory load issue rate at one load per DFMA).  Same operation order per
+// input as mlp_out0.
+__device__ __noinline__ double2 mlp_out0_x2(const double* w, double z0a, double z0b, double z1, double z2a,
+                                            double z2b) {
+  const double* W1 = w;
+  const double* b1 = w + 24;
+  const double* W2 = w + 32;
+  const double* b2 = w + 96;
+  const double* W3 = w + 104;
+  const double* b3 = w + 120;
+  double ha[8], hb[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const double w0 = W1[i * 3 + 0], w1 = W1[i * 3 + 1], w2 = W1[i * 3 + 2], bb = b1[i];
+    double a = fma(w0, z0a, bb), b = fma(w0, z0b, bb);
+    a = fma(w1, z1, a);
+    b = fma(w1, z1, b);
+    a = fma(w2, z2a, a);
+    b = fma(w2, z2b, b);
+    ha[i] = (a > 0.0) ? a : 0.0;
+    hb[i] = (b > 0.0) ? b : 0.0;
+  }
+  double oa = b3[0], ob = b3[0];
+#pragma unroll 1
+  for (int i = 0; i < 8; ++i) {
+    double a = b2[i], b = b2[i];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double wij = W2[i * 8 + j];
+      a = fma(wij, ha[j], a);
+      b = fma(wij, hb[j], b);
+    }
+    const double w3 = W3[i];
+    oa = fma(w3, (a > 0.0) ? a : 0.0, oa);
+    ob = fma(w3, (b > 0.0) ? b : 0.0, ob);
+  }
+  return make_double2(oa, ob);
+}
+
 // Stationary points of the cubic position p_j(t) per axis (roots of
 // p'(t) = v0 + 2 c2 t + 3 c3 t^2), computed once per edge; -1 = none.
 template <int D>
@@ -1160,38 +1201,52 @@ __global__ void __launch_bounds__(kFoldThreads, MPAP_FOLD_MIN_BLOCKS) k_fold(con
   const uint16_t* kvp = kvbuf + koff[e];
   const double q = Dl / P.n_f;
   double s = 0.0, c = 0.0, Sp = 0.0, Cp = 0.0;
-  // the edge's counts are 8-aligned: one 16-byte load per 8 steps
+  // the edge's counts are 8-aligned: one 16-byte load per 8 steps; the MLP
+  // runs two steps per call (mlp_out0_x2), the fold stays in step order
   for (int k0 = 0; k0 < K; k0 += 8) {
     const uint4 q8 = __ldg(reinterpret_cast<const uint4*>(kvp + k0));
-    const unsigned wv[4] = {q8.x, q8.y, q8.z, q8.w};
+#pragma unroll 1
+    for (int jp = 0; jp < 8; jp += 2) {   // not unrolled: one inlined copy of the MLP
+      const unsigned wvp = (jp < 4) ? ((jp < 2) ? q8.x : q8.y) : ((jp < 6) ? q8.z : q8.w);   // steps jp, jp + 1
+      if (k0 + jp >= K) break;
+      double inc2[2];
+      int kv2[2];
+      double z0[2] = {0.0, 0.0};
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      const int k = k0 + jj;
-      if (k >= K) break;
-      const int kv = (int)((wv[jj >> 1] >> (16 * (jj & 1))) & 0xffffu);
-      double inc = Dl - (double)kv * q;
-      if (HEUR == 3) {
-        double speed = P.nominal_speed;   // |v(t)| for the MLP (kinematic: nominal)
-        if (DYN == 1) {
-          const double t = (double)k * Dl;
-          double vel[D];
-          di_vel<D>(su_l, c2, c3, t, vel);
-          double ss = 0.0;
+      for (int u = 0; u < 2; ++u) {
+        const int k = k0 + jp + u;
+        kv2[u] = (int)((wvp >> (16 * u)) & 0xffffu);
+        inc2[u] = Dl - (double)kv2[u] * q;
+        if (HEUR == 3) {
+          double speed = P.nominal_speed;   // |v(t)| for the MLP (kinematic: nominal)
+          if (DYN == 1) {
+            const double t = (double)k * Dl;
+            double vel[D];
+            di_vel<D>(su_l, c2, c3, t, vel);
+            double ss = 0.0;
 #pragma unroll
-          for (int j = 0; j < D; ++j) ss = fma(vel[j], vel[j], ss);
-          speed = sqrt(ss);
+            for (int j = 0; j < D; ++j) ss = fma(vel[j], vel[j], ss);
+            speed = sqrt(ss);
+          }
+          z0[u] = speed / P.v_ref;
         }
-        const double z0 = speed / P.v_ref;
-        const double z1 = omega / P.w_ref;
-        const double z2 = (double)kv / P.n_f;
-        const double o = mlp_out0(s_mlp, z0, z1, z2);
-        inc = inc + Dl * (P.mlp_gain * o);
       }
-      const double tt = c + inc;
-      c = (tt > 0.0) ? tt : 0.0;
-      s = s + inc;
-      Sp = (s > Sp) ? s : Sp;   // running maxima of the prefix values (NEXT-3)
-      Cp = (c > Cp) ? c : Cp;
+      if (HEUR == 3) {
+        const double z1 = omega / P.w_ref;
+        const double2 o = mlp_out0_x2(s_mlp, z0[0], z0[1], z1, (double)kv2[0] / P.n_f, (double)kv2[1] / P.n_f);
+        inc2[0] = inc2[0] + Dl * (P.mlp_gain * o.x);
+        inc2[1] = inc2[1] + Dl * (P.mlp_gain * o.y);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (k0 + jp + u >= K) break;
+        const double inc = inc2[u];
+        const double tt = c + inc;
+        c = (tt > 0.0) ? tt : 0.0;
+        s = s + inc;
+        Sp = (s > Sp) ? s : Sp;   // running maxima of the prefix values (NEXT-3)
+        Cp = (c > Cp) ? c : Cp;
+      }
     }
   }
   *reinterpret_cast<float2*>(&edges[e].s) = make_float2((float)s, (float)c);
