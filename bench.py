@@ -334,6 +334,10 @@ def main():
     roof = roofline(dom, dom_ms, dom_n, last_work, B, res, peaks, peak_src)
     roof["share_of_step"] = dom_ms / tot_ms if tot_ms > 0 else None
     roof["traffic"] = committed_traffic(dom, Q)
+    # the metric's "HBM roofline fraction" for the search itself (k_search):
+    # 16 B edge record per relaxation + 16 B label per inserted plan
+    search_roof = roofline("k_search", kern["k_search"][0], kern["k_search"][1], last_work, B, res, peaks, peak_src)
+    search_roof["traffic"] = committed_traffic("k_search", Q)
 
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
@@ -346,7 +350,8 @@ def main():
                    "lambda": B.lam, "r": B.r, "parallelism": f"dp{world} (independent queries)",
                    "l2": "flushed between timed steps (512 MiB write, outside the step events)"},
         "edges_relaxed_per_s": relax_all * args.steps / (tot_ms_max / 1e3),
-        "search_only": {"ms_per_step": search_ms / max(kern['k_search'][1], 1),
+        "search_only": {"roofline": search_roof,
+                        "ms_per_step": search_ms / max(kern['k_search'][1], 1),
                         "edges_relaxed_per_s": relax_step / (search_ms / max(kern['k_search'][1], 1) / 1e3)
                         if search_ms > 0 else None,
                         "queries_per_s": Q / (search_ms / max(kern['k_search'][1], 1) / 1e3) if search_ms else None},
