@@ -40,17 +40,21 @@ namespace mpap {
 
 #define FULLW 0xffffffffu
 constexpr int kMcWarps = 4;                 // warps per k_mc block
+#ifndef MPAP_MC_MIN_BLOCKS
+#define MPAP_MC_MIN_BLOCKS 4                // 4 x 4 warps per SM: at most 128 registers
+#endif
 
 constexpr float kMcCullMarginF = 1e-4f;     // box vs sight-line bounding-box gap (f32) that provably misses:
                                             // rounding of O(100) m coordinates is < 1e-5
 
-// per-warp shared memory: features [F][D], boxes [O][2D], contributions
-// [F][D] (doubles); candidate list and occluded flags [F] each, near-box
-// list [O] (ints); boxes [O][2D] and candidate sight-line boxes [F][2D]
-// (floats, for the exact culls)
+// per-warp shared memory: features [F][D], boxes [O][2D] (doubles); the
+// candidate sight-line boxes [F][2D] (floats, phases a-b of a step) share
+// their space with the fix contributions [F][D] (doubles, phases d-e);
+// candidate list and occluded flags [F] each, near-box list [O] (ints);
+// boxes [O][2D] (floats, for the exact culls)
 __host__ __device__ constexpr size_t mc_warp_doubles(int d, int f_max, int o_max) {
   return (size_t)f_max * d * 2 + (size_t)o_max * 2 * d + (size_t)f_max + ((size_t)o_max + 1) / 2 +
-         (size_t)o_max * d + (size_t)f_max * d;
+         (size_t)o_max * d;
 }
 
 struct McSeg {
@@ -159,7 +163,7 @@ __device__ __forceinline__ bool mc_seg_box(const double* A, const double* Dv, co
 }
 
 template <int D, int HEUR>
-__global__ void __launch_bounds__(kMcWarps * 32) k_mc(const double* __restrict__ feat_all,
+__global__ void __launch_bounds__(kMcWarps * 32, MPAP_MC_MIN_BLOCKS) k_mc(const double* __restrict__ feat_all,
                                                        const int32_t* __restrict__ feat_base,
                                                        const double* __restrict__ box_all,
                                                        const int32_t* __restrict__ obst_base,
@@ -176,11 +180,11 @@ __global__ void __launch_bounds__(kMcWarps * 32) k_mc(const double* __restrict__
   double* wf = mc_smem + (size_t)warp * mc_warp_doubles(D, f_max, o_max);
   double* wb = wf + (size_t)f_max * D;       // boxes [O][2D]
   double* wc = wb + (size_t)o_max * 2 * D;   // fix contributions [F][D] in rank order
+  float* wsb = reinterpret_cast<float*>(wc);  // candidate sight-line boxes, f32 [F][2D] (aliases wc)
   int* wl = reinterpret_cast<int*>(wc + (size_t)f_max * D);   // candidate / visible feature list [F]
   int* wo = wl + f_max;                                        // candidate occluded flags [F]
   int* wn = wo + f_max;                                        // boxes near x this step [O]
   float* wbf = reinterpret_cast<float*>(wn + ((o_max + 1) & ~1));   // boxes, f32 [O][2D]
-  float* wsb = wbf + (size_t)o_max * 2 * D;                    // candidate sight-line boxes, f32 [F][2D]
   unsigned lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
   const double R2 = max_range * max_range;
