@@ -37,3 +37,23 @@ def gather_results(local, world: int):
 def records(tensor, dtype) -> np.ndarray:
     """View gathered bytes as structured result records."""
     return tensor.cpu().numpy().view(dtype)
+
+
+def mc_trial_shard(rank: int, world: int, trials: int):
+    """Monte Carlo trials of one plan split across ranks (NEXT-4: trials are
+    independent counter-based streams, so rank r runs trials [t0, t0 + n) and
+    the per-trial results equal a single-GPU run's).  Returns (t0, n)."""
+    if not (0 <= rank < world) or trials < 0:
+        raise ValueError("bad rank/world/trials")
+    base, extra = divmod(trials, world)
+    t0 = rank * base + min(rank, extra)
+    return t0, base + (1 if rank < extra else 0)
+
+
+def reduce_exceed(local):
+    """Sum the per-plan exceedance counts (int64 tensor) over ranks: the one
+    collective of a sharded Monte Carlo verification."""
+    import torch.distributed as dist
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(local, op=dist.ReduceOp.SUM)
+    return local

@@ -49,6 +49,49 @@ def _worker(rank, world, port, Q, outdir):
     dist.destroy_process_group()
 
 
+def _mc_worker(rank, world, port, trials, outdir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "mpap_dist", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                  "paper_1705_02408_b200", "dist.py"))
+    md = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(md)
+    import oracle
+    from synth import line_problem, mc_params
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    prob = line_problem([(0.0, 0.0, 1.5, 0.0, 0.0, 0.0, 1.0, 0.0), (3.0, 0.0, 1.5, 0.0, 0.0, 0.0, 1.0, 0.0)],
+                        features=[[1.5, 3.0, 1.5]])
+    mc = mc_params(trials=trials, sigma_imu=0.5, sigma_vis=0.2, delta=0.05)
+    t0, n = md.mc_trial_shard(rank, world, trials)
+    # the oracle stands in for this rank's k_mc launch (CPU test of the host logic)
+    r = oracle.mc_verify(prob, [0, 1], mc, t0, n)
+    cnt = md.reduce_exceed(torch.tensor([r["exceed"]], dtype=torch.int64))
+    np.save(os.path.join(outdir, f"mc{rank}.npy"), np.array([int(cnt[0]), t0, n]))
+    dist.destroy_process_group()
+
+
+def test_mc_sharded_trials_two_ranks(tmp_path, orc):
+    """Sharded Monte Carlo (NEXT-4): trials split across 2 ranks, one
+    all-reduce of the exceedance count equals the single-process count."""
+    world, trials = 2, 41
+    port = _free_port()
+    tmp.start_processes(_mc_worker, args=(world, port, trials, str(tmp_path)), nprocs=world, start_method="spawn")
+    a = np.load(tmp_path / "mc0.npy")
+    b = np.load(tmp_path / "mc1.npy")
+    from synth import line_problem, mc_params
+    prob = line_problem([(0.0, 0.0, 1.5, 0.0, 0.0, 0.0, 1.0, 0.0), (3.0, 0.0, 1.5, 0.0, 0.0, 0.0, 1.0, 0.0)],
+                        features=[[1.5, 3.0, 1.5]])
+    full = orc.mc_verify(prob, [0, 1], mc_params(trials=trials, sigma_imu=0.5, sigma_vis=0.2, delta=0.05))
+    assert a[0] == b[0] == full["exceed"]
+    assert a[1] == 0 and b[1] == a[2] and a[2] + b[2] == trials
+
+
 def test_gather_two_ranks(tmp_path):
     world, Q = 2, 5
     port = _free_port()
@@ -72,3 +115,8 @@ def test_shards_disjoint_and_cover():
         assert sorted(all_envs) == list(range(64 * world))
     with pytest.raises(ValueError):
         md.shard_envs(2, 2, 4)
+    for world in (1, 2, 3, 8):
+        for trials in (0, 1, 7, 1000):
+            parts = [md.mc_trial_shard(r, world, trials) for r in range(world)]
+            assert sum(n for _, n in parts) == trials
+            assert all(parts[r][0] + parts[r][1] == parts[r + 1][0] for r in range(world - 1))

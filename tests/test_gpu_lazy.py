@@ -108,3 +108,20 @@ def test_lazy_rejects_batches(mp):
     B.prm.lazy_edges = 1
     with pytest.raises(mp.MpapError):
         B.build()
+
+
+def test_lazy_forall_t_equals_eager(mp):
+    """Lazy roadmap built with edge peaks: the Eq. 2 for-all-t search (NEXT-3)
+    reads peaks evaluated on demand and equals the eager one."""
+    prob = small("c3", 700)
+    eager = mp.pb.build_problem(prob, edge_peaks=True)
+    lazy = mp.pb.build_problem(prob, edge_peaks=True, lazy_edges=True)
+    for beta in (2.6876, 2.1931):
+        same(mp.pb.search_problem(lazy, prob, beta, forall_t=True),
+             mp.pb.search_problem(eager, prob, beta, forall_t=True))
+    Sl, Cl = mp.mpap_roadmap_export_peaks(lazy)
+    Se, Ce = mp.mpap_roadmap_export_peaks(eager)
+    assert np.array_equal(Sl.view(np.uint32), Se.view(np.uint32)) and np.array_equal(Cl.view(np.uint32),
+                                                                                      Ce.view(np.uint32))
+    lazy.free()
+    eager.free()

@@ -138,3 +138,27 @@ def test_refine_beta_mc_parity(mp, orc):
     if best is not None:
         assert g["beta"] == best
     rm.free()
+
+
+def test_mc_c2_velocity_fov_parity(mp, orc):
+    """2D double integrator with the velocity-FOV heuristic (k_mc<2, 1>)."""
+    cfg = load_config("c2")
+    cfg["n_samples"] = 500
+    prob = make_problem(cfg)
+    rm = mp.pb.build_problem(prob)
+    mc = mc_params(trials=64, sigma_imu=0.2, sigma_vis=0.05, delta=0.05)
+    r = mp.pb.search_problem(rm, prob, float("inf"))
+    assert r["status"] == 0
+    g = mp.mpap_mc_verify(rm, 0, r["path"], mc)
+    o = orc.mc_verify(prob, r["path"], mc)
+    check(g, o, 64)
+    rm.free()
+
+
+def test_mc_kinematic_rejected(mp):
+    cfg = load_config("c1")
+    prob = make_problem(cfg)
+    rm = mp.pb.build_problem(prob)
+    with pytest.raises(mp.MpapError):
+        mp.mpap_mc_verify(rm, 0, [0], mc_params(trials=4))
+    rm.free()
