@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-procs", type=int, default=0)
     ap.add_argument("--no-mc", action="store_true", help="skip the Monte Carlo verification measurement")
+    ap.add_argument("--no-lazy", action="store_true", help="skip the lazy-roadmap variant measurement")
     ap.add_argument("--mc-trials", type=int, default=1000)
     return ap.parse_args()
 
@@ -363,6 +364,9 @@ def main():
     }
     if e2e:
         line["e2e"] = e2e
+    if not args.no_lazy:
+        line["lazy_variant"] = measure_lazy(mp, B, s_d, o_d, f_d, betas, PATH_CAP, paths_d, res_d, flush, args.steps,
+                                            res)
     if not args.no_mc:
         line["mc_verify"] = measure_mc(mp, B, betas, PATH_CAP, args.mc_trials, rank == 0 and world == 1
                                        and not args.no_cpu_baseline)
@@ -373,6 +377,44 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def measure_lazy(mp, B, s_d, o_d, f_d, betas, path_cap, paths_d, res_d, flush, steps, res_eager):
+    """NEXT-1 part i variant of the same step: the roadmap is built lazily
+    (Near + Cost) and the batched search evaluates the rows its waves need
+    (suspend / evaluate the union of requested rows / resume).  Same plans --
+    checked record for record against the eager step's results; timed like the
+    headline (CUDA events, L2 flushed, inputs resident), reported beside it,
+    not as the headline."""
+    import torch
+    stream = torch.cuda.current_stream()
+    rows = [0]
+
+    def step():
+        B.prm.lazy_edges = 1
+        rm = B.build(s_d, o_d, f_d)
+        B.prm.lazy_edges = 0
+        B.search(rm, betas, path_capacity=path_cap, paths=paths_d, results=res_d)
+        rows[0] = sum(mp.mpap_roadmap_rows_evaluated(rm, e) for e in range(len(B.probs)))
+        rm.free()
+
+    step()
+    torch.cuda.synchronize()
+    ms = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        b.synchronize()
+        ms += a.elapsed_time(b)
+    res = res_d.cpu().numpy().view(mp.RESULT_DTYPE)
+    same = all(np.array_equal(res[k], res_eager[k]) for k in ("status", "path_len", "cost", "h", "relaxations"))
+    Q = len(B.probs)
+    return {"queries_per_s": Q * steps / (ms / 1e3), "ms_per_step": ms / steps, "rows_evaluated": rows[0],
+            "rows_total": int(B.n.sum()), "same_results_as_eager": bool(same)}
 
 
 def measure_mc(mp, B, betas, path_cap: int, trials: int, with_cpu: bool):

@@ -82,13 +82,14 @@ typedef struct {
                              build: two more running maxima per heuristic step)    */
   int32_t lazy_edges;     /* 0 or 1 (NEXT-1 part i): the build
                              computes Near + Cost only; collision bits and heuristic
-                             summaries of a row are evaluated when the single-query
-                             search (mpap_search*) first expands a plan at that
-                             node -- the search reads the same (coll, s, c), so the
-                             plan is identical.  Every other call on the roadmap
-                             (batch search, export, update, Monte Carlo) first
-                             evaluates all remaining rows.  Single environment
-                             only (n_envs == 1).                                    */
+                             summaries of a row are evaluated when a search
+                             (mpap_search*, mpap_search_batch*) first expands a
+                             plan at that node -- the search reads the same
+                             (coll, s, c), so every plan is identical.  The search
+                             suspends before a wave whose heads need rows, the
+                             library evaluates the rows requested by all queries
+                             of the call in one pass and resumes.  Export, update
+                             and Monte Carlo first evaluate all remaining rows.   */
 } mpap_params;
 
 /* Opaque, device-resident, immutable after build: B >= 1 environments, each

@@ -335,7 +335,6 @@ mpap_status mpap_build_roadmap_batch(int32_t n_envs, const double* samples, cons
   if (mem != MPAP_MEM_HOST && mem != MPAP_MEM_DEVICE) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad mem space");
   mpap_status s = validate_params(params, r);
   if (s != MPAP_OK) return s;
-  if (params->lazy_edges && n_envs != 1) return set_error(MPAP_ERR_INVALID_ARGUMENT, "lazy_edges needs n_envs == 1");
   const int d = params->pos_dim;
   const int need = d * (params->dynamics == MPAP_DOUBLE_INTEGRATOR ? 2 : 1) + (params->has_heading ? 2 : 0);
   if (row_stride < need || row_stride > 8)

@@ -112,6 +112,7 @@ struct Ctl {
   unsigned long long relax_total, inserted_total;
   int waves;
   int suspended, pswap;   // lazy: suspended before a wave; pending lists swapped at suspension
+  int need;               // lazy: some head of G_i has an unevaluated row
   unsigned long long best_key;
   int nties;
   int ties[32];
@@ -261,7 +262,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
     if (leader) {
       S->gsize = 1; S->psize = 0; S->nsize = 0; S->ncand = 0; S->ntouched = 0; S->nlabels = 1; S->calloc = 0;
       S->goal_in_g = 0; S->overflow = 0; S->any_goal = 0; S->i = 0; S->minb = LLONG_MAX;
-      S->relax_total = 0; S->inserted_total = 0; S->waves = 0; S->suspended = 0; S->pswap = 0;
+      S->relax_total = 0; S->inserted_total = 0; S->waves = 0; S->suspended = 0; S->pswap = 0; S->need = 0;
     }
     team.sync();
     bool mygoal = false;
@@ -303,7 +304,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
   if (pswap) { int32_t* tmp = pend; pend = pend2; pend2 = tmp; }
   if (A.resume) {
     team.sync();
-    if (leader) S->suspended = 0;
+    if (leader) { S->suspended = 0; S->need = 0; }
     team.sync();
   }
   while (true) {
@@ -311,19 +312,24 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
     const int gsize = vld(S->gsize);
     const long long i_cur = vld(S->i);
     if (A.ready) {   // lazy roadmap: every head of G_i must have its row evaluated
+      bool my_need = false;
       for (int k = tid; k < gsize; k += nthr) {
         const int64_t row = nbase + labels[G[k]].x;
-        if (vld(A.ready[row]) != 1 && atomicCAS(&A.ready[row], 0, 2) == 0)
-          A.req[atomicAdd(A.nreq, 1)] = (int32_t)row;
+        if (vld(A.ready[row]) != 1) {
+          my_need = true;
+          if (atomicCAS(&A.ready[row], 0, 2) == 0) A.req[atomicAdd(A.nreq, 1)] = (int32_t)row;
+        }
       }
+      if (my_need) atomicOr(&S->need, 1);
       team.sync();
-      if (vld(*A.nreq) > 0) {
+      if (vld(S->need)) {   // suspend; the host evaluates the requested rows and resumes
         if (leader) { S->suspended = 1; S->pswap = pswap; }
         return;
       }
     }
     team.sync();
     if (leader) {
+      S->need = 0;
       S->relax = 0; S->bpass = 0; S->tcount = 0; S->ssum = 0; S->inserted = 0; S->killed = 0;
       S->ncand = 0; S->ntouched = 0; S->calloc = 0;
     }
@@ -730,6 +736,10 @@ __global__ void __launch_bounds__(kST) k_search_cluster(SearchArgs A, Ctl* S_all
   const ClusterTeam team;
   const int slot = blockIdx.x / cg::this_cluster().num_blocks();
   Ctl* S = S_all + slot;
+  if (A.ready) {   // lazy roadmap: query = slot (static), so a suspended query resumes in its slot
+    if (slot < A.nq && (!A.resume || vld(S->suspended))) run_query<TRACE>(team, A, S, slot, slot);
+    return;
+  }
   while (true) {
     if (team.rank() == 0) S->q = atomicAdd(A.work, 1);
     team.sync();
@@ -846,7 +856,9 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     // CTA per query and as many slots as resident CTAs
     const bool grid_mode = (nrun == 1) && use_grid;
     // few queries: one cluster of kCluster CTAs per query; many: one CTA each
-    const bool cluster_mode = !grid_mode && use_cluster && nrun * kCluster <= nsm * occ;
+    // (a lazy roadmap runs batches in cluster mode, one static slot per query,
+    // so suspended queries resume in place)
+    const bool cluster_mode = !grid_mode && use_cluster && (nrun * kCluster <= nsm * occ || rm->lazy);
     const int nslots = grid_mode ? 1 : cluster_mode ? nrun : std::min(nrun, nsm * occ);
     const size_t sb_slots = carve(nullptr, caps, nslots, nullptr);
     const size_t sb = sb_slots + sizeof(Ctl) * (size_t)nslots + 256;
@@ -886,15 +898,15 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     CKS(cudaMemsetAsync(d_work, 0, sizeof(int), st));
     // lazy roadmap (NEXT-1 part i): the whole-grid search suspends before a
     // wave whose heads have unevaluated rows; evaluate them and resume
-    if (rm->lazy && !grid_mode) {
+    if (rm->lazy && !grid_mode && !cluster_mode) {
       mpap_status se = evaluate_rows_device(const_cast<mpap_roadmap*>(rm), nullptr, 0, st);
       if (se != MPAP_OK) return se;
     }
-    const bool lazy_grid = rm->lazy && grid_mode;
+    const bool lazy_grid = rm->lazy && (grid_mode || cluster_mode);
     int32_t* d_req = nullptr;
     int* d_nreq = nullptr;
     if (lazy_grid) {
-      CKS(cudaMallocAsync(&d_req, sizeof(int32_t) * std::max(rm->n_max, 1), st));
+      CKS(cudaMallocAsync(&d_req, sizeof(int32_t) * std::max<int64_t>(rm->node_base[rm->B], 1), st));
       CKS(cudaMallocAsync(&d_nreq, sizeof(int), st));
       A.ready = rm->d_ready;
       A.req = d_req;
@@ -907,9 +919,25 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
         CKS(cudaMemsetAsync(d_nreq, 0, sizeof(int), st));
         {
           ProfScope ps("k_search", st);
-          void* args[] = {&A, &d_ctl};
-          const void* fn = trace ? (const void*)k_search_grid<true> : (const void*)k_search_grid<false>;
-          CKS(cudaLaunchCooperativeKernel(fn, dim3(nsm * occ_grid), dim3(kST), args, 0, st));
+          if (grid_mode) {
+            void* args[] = {&A, &d_ctl};
+            const void* fn = trace ? (const void*)k_search_grid<true> : (const void*)k_search_grid<false>;
+            CKS(cudaLaunchCooperativeKernel(fn, dim3(nsm * occ_grid), dim3(kST), args, 0, st));
+          } else {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(nslots * kCluster);
+            cfg.blockDim = dim3(kST);
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = kCluster;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            if (trace) CKS(cudaLaunchKernelEx(&cfg, k_search_cluster<true>, A, d_ctl));
+            else CKS(cudaLaunchKernelEx(&cfg, k_search_cluster<false>, A, d_ctl));
+          }
         }
         note_launch();
         int nreq = 0;
