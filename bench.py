@@ -401,6 +401,9 @@ def measure_lazy(mp, B, s_d, o_d, f_d, betas, path_cap, paths_d, res_d, flush, s
     step()
     torch.cuda.synchronize()
     ms = 0.0
+    mp.mpap_prof_reset()
+    mp.mpap_prof_enable(True)
+    l0 = mp.mpap_launch_count()
     for _ in range(steps):
         flush.zero_()
         a = torch.cuda.Event(enable_timing=True)
@@ -410,11 +413,16 @@ def measure_lazy(mp, B, s_d, o_d, f_d, betas, path_cap, paths_d, res_d, flush, s
         b.record(stream)
         b.synchronize()
         ms += a.elapsed_time(b)
+    mp.mpap_prof_enable(False)
+    launches = mp.mpap_launch_count() - l0
+    kern = {k: mp.mpap_prof_read(k) for k in mp.KERNELS + ("k_lazy_init", "k_row_items")}
     res = res_d.cpu().numpy().view(mp.RESULT_DTYPE)
     same = all(np.array_equal(res[k], res_eager[k]) for k in ("status", "path_len", "cost", "h", "relaxations"))
     Q = len(B.probs)
     return {"queries_per_s": Q * steps / (ms / 1e3), "ms_per_step": ms / steps, "rows_evaluated": rows[0],
-            "rows_total": int(B.n.sum()), "same_results_as_eager": bool(same)}
+            "rows_total": int(B.n.sum()), "same_results_as_eager": bool(same), "gpu_launches_per_step": launches / steps,
+            "kernels_ms_per_step": {k: v[0] / steps for k, v in kern.items()},
+            "search_launches_per_step": kern["k_search"][1] / steps}
 
 
 def measure_mc(mp, B, betas, path_cap: int, trials: int, with_cpu: bool):
