@@ -131,6 +131,24 @@ mpap_status mpap_build_roadmap(const double *samples, int32_t n, int32_t row_str
                                const mpap_params *params, int32_t mem, void *cuda_stream,
                                mpap_roadmap **out);
 
+/*
+ * mpap_build_roadmap_rows -- row-sharded build of one environment (SURVEY.md
+ * §8(e); Alg. 2 is "embarrassingly parallel" over rows): the same
+ * inputs as mpap_build_roadmap, but only rows [row_begin, row_end) get their
+ * r-disc neighbours, collision bits and heuristic summaries (every sample is
+ * still a candidate neighbour); the other rows have no edges.  Rank g of G
+ * builds its block of rows; the blocks' CSRs (mpap_roadmap_export) are
+ * all-gathered and concatenated in row order, which equals the single-GPU
+ * build bit for bit, and the full CSR is wrapped with mpap_roadmap_import.
+ * Errors: as mpap_build_roadmap, plus INVALID_ARGUMENT unless
+ * 0 <= row_begin <= row_end <= n.
+ */
+mpap_status mpap_build_roadmap_rows(const double *samples, int32_t n, int32_t row_stride,
+                                    const double *obstacles, int32_t n_obstacles,
+                                    const double *features, int32_t n_features, double r,
+                                    const mpap_params *params, int32_t row_begin, int32_t row_end,
+                                    int32_t mem, void *cuda_stream, mpap_roadmap **out);
+
 /* X_goal: closed box on position (reading R20). */
 typedef struct { double lo[3], hi[3]; } mpap_goal;
 

@@ -46,7 +46,7 @@ EXPORTED_SYMBOLS = [
     "mpap_last_error", "mpap_launch_count", "mpap_prof_enable", "mpap_prof_reset", "mpap_prof_read",
     "mpap_roadmap_work", "mpap_search_ex", "mpap_search_batch_ex", "mpap_roadmap_export_peaks",
     "mpap_roadmap_set_peaks", "mpap_roadmap_update", "mpap_mc_verify", "mpap_mc_verify_batch",
-    "mpap_roadmap_rows_evaluated",
+    "mpap_roadmap_rows_evaluated", "mpap_build_roadmap_rows",
 ]
 
 
@@ -120,6 +120,9 @@ _lib.mpap_mc_verify_batch.argtypes = [_vp, C.c_int32, _vp, _vp, C.c_int32, _vp, 
                                       C.c_uint64, _vp, _vp, _vp, _vp]
 _lib.mpap_mc_verify.argtypes = [_vp, C.c_int32, _vp, C.c_int32, C.POINTER(mpap_mc_params), C.c_uint64, _vp, _vp,
                                 _vp, _vp]
+_lib.mpap_build_roadmap_rows.argtypes = [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, _vp, C.c_int32, C.c_double,
+                                         C.POINTER(mpap_params), C.c_int32, C.c_int32, C.c_int32, _vp,
+                                         C.POINTER(_vp)]
 _lib.mpap_roadmap_rows_evaluated.argtypes = [_vp, C.c_int32, C.POINTER(C.c_int64)]
 _lib.mpap_roadmap_export_peaks.argtypes = [_vp, C.c_int32, _vp, _vp]
 _lib.mpap_roadmap_set_peaks.argtypes = [_vp, _vp, _vp]
@@ -281,6 +284,29 @@ def mpap_build_roadmap(samples, obstacles, features, r: float, params: mpap_para
     del k1, k2, k3
     if s != MPAP_OK:
         raise MpapError(s, "mpap_build_roadmap")
+    return Roadmap(out.value)
+
+
+def mpap_build_roadmap_rows(samples, obstacles, features, r: float, params: mpap_params, row_begin: int,
+                            row_end: int, stream=None) -> Roadmap:
+    """Row-sharded build: only rows [row_begin, row_end) of
+    the single environment get edges; every sample is a candidate neighbour."""
+    n = int(samples.shape[0])
+    stride = int(samples.shape[1])
+    d = params.pos_dim
+    no = int(obstacles.shape[0]) if obstacles is not None and np.size(obstacles) else 0
+    nf = int(features.shape[0]) if features is not None and np.size(features) else 0
+    mem = MPAP_MEM_DEVICE if _is_cuda_tensor(samples) else MPAP_MEM_HOST
+    sp, k1 = _ptr(samples, np.float64)
+    op, k2 = _ptr(obstacles if no else np.zeros(2 * d), np.float64)
+    fp, k3 = _ptr(features if nf else np.zeros(d), np.float64)
+    out = C.c_void_p()
+    st = _stream(stream)
+    s = _lib.mpap_build_roadmap_rows(sp, n, stride, op, no, fp, nf, float(r), C.byref(params), int(row_begin),
+                                     int(row_end), mem, C.c_void_p(st) if st else None, C.byref(out))
+    del k1, k2, k3
+    if s != MPAP_OK:
+        raise MpapError(s, "mpap_build_roadmap_rows")
     return Roadmap(out.value)
 
 

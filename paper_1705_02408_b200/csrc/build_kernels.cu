@@ -221,6 +221,10 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_near(const double* __restri
   const int u = blockIdx.x * kNearWarps + warp;
   if (u >= nb) return;  // warp-uniform
   const int64_t row = node_base[b] + u;
+  if (row < P.row_lo || row >= P.row_hi) {   // row-sharded build: another rank owns this row
+    if (lane == 0) cnt[row] = 0;
+    return;
+  }
   const int stride = P.stride;
   const double* envs = samples + node_base[b] * stride;
   double su[NS];

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -324,10 +325,33 @@ void mpap_roadmap_free(mpap_roadmap* rm) {
   delete rm;
 }
 
+static mpap_status build_batch_impl(int32_t n_envs, const double* samples, const int32_t* n, int32_t row_stride,
+                                    const double* obstacles, const int32_t* n_obstacles, const double* features,
+                                    const int32_t* n_features, double r, const mpap_params* params, int32_t mem,
+                                    void* cuda_stream, int64_t row_lo, int64_t row_hi, mpap_roadmap** out);
+
 mpap_status mpap_build_roadmap_batch(int32_t n_envs, const double* samples, const int32_t* n, int32_t row_stride,
                                      const double* obstacles, const int32_t* n_obstacles, const double* features,
                                      const int32_t* n_features, double r, const mpap_params* params, int32_t mem,
                                      void* cuda_stream, mpap_roadmap** out) {
+  return build_batch_impl(n_envs, samples, n, row_stride, obstacles, n_obstacles, features, n_features, r, params,
+                          mem, cuda_stream, 0, INT64_MAX, out);
+}
+
+mpap_status mpap_build_roadmap_rows(const double* samples, int32_t n, int32_t row_stride, const double* obstacles,
+                                    int32_t n_obstacles, const double* features, int32_t n_features, double r,
+                                    const mpap_params* params, int32_t row_begin, int32_t row_end, int32_t mem,
+                                    void* cuda_stream, mpap_roadmap** out) {
+  if (row_begin < 0 || row_end < row_begin || row_end > n)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "row range must satisfy 0 <= begin <= end <= n");
+  return build_batch_impl(1, samples, &n, row_stride, obstacles, &n_obstacles, features, &n_features, r, params, mem,
+                          cuda_stream, row_begin, row_end, out);
+}
+
+static mpap_status build_batch_impl(int32_t n_envs, const double* samples, const int32_t* n, int32_t row_stride,
+                                    const double* obstacles, const int32_t* n_obstacles, const double* features,
+                                    const int32_t* n_features, double r, const mpap_params* params, int32_t mem,
+                                    void* cuda_stream, int64_t row_lo, int64_t row_hi, mpap_roadmap** out) {
   if (!out) return set_error(MPAP_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   if (n_envs < 1 || !n || !n_obstacles || !n_features || !samples)
@@ -392,6 +416,8 @@ mpap_status mpap_build_roadmap_batch(int32_t n_envs, const double* samples, cons
   P.v_ref = params->v_ref;
   P.w_ref = params->w_ref;
   P.r = r;
+  P.row_lo = row_lo;   // row-sharded build (mpap_build_roadmap_rows); all rows otherwise
+  P.row_hi = row_hi;
   if (params->mlp) std::memcpy(P.mlp, params->mlp, sizeof(double) * kMlpSize);
   rm->n.assign(n, n + n_envs);
   rm->n_obst.assign(n_obstacles, n_obstacles + n_envs);

@@ -29,6 +29,7 @@ struct DevParams {
   double control_weight, nominal_speed, dt, collision_dt, n_f, fov_cos_half, max_range;
   double mlp_gain, v_ref, w_ref;
   double r;
+  int64_t row_lo, row_hi;  // global rows whose edges are built (row-sharded build); others get none
   double mlp[kMlpSize];
 };
 

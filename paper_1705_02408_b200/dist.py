@@ -1,8 +1,11 @@
 """Multi-GPU plumbing: independent environment+query units
 are sharded across ranks with no data-path collective; the only exchange is
 one all-gather of the fixed-size 48-byte result records (mpap_result) per
-batch, never inside the wave loop.  torch.distributed with NCCL on GPUs
-(gloo on CPU for tests).
+batch, never inside the wave loop.  A large single roadmap is built
+row-sharded (rank g builds rows [g n/G, (g+1) n/G), mpap_build_roadmap_rows)
+and its CSR blocks are all-gathered once and concatenated in row order.
+Monte Carlo trials of a plan shard with one all-reduce of the exceedance
+counts.  torch.distributed with NCCL on GPUs (gloo on CPU for tests).
 """
 from __future__ import annotations
 
@@ -57,3 +60,74 @@ def reduce_exceed(local):
     if dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(local, op=dist.ReduceOp.SUM)
     return local
+
+
+def row_block(rank: int, world: int, n: int):
+    """Rows [b, e) of rank `rank` in a row-sharded build of n rows."""
+    if not (0 <= rank < world) or n < 0:
+        raise ValueError("bad rank/world/n")
+    base, extra = divmod(n, world)
+    b = rank * base + min(rank, extra)
+    return b, b + base + (1 if rank < extra else 0)
+
+
+def csr_block(full: dict, b: int, e: int) -> dict:
+    """The block of rows [b, e) of an exported CSR (row counts + the rows'
+    edge arrays, dst | coll << 31 packed as in the C ABI)."""
+    rp = np.asarray(full["row_ptr"], dtype=np.int64)
+    lo, hi = int(rp[b]), int(rp[e])
+    dc = (np.asarray(full["dst"][lo:hi], dtype=np.uint32) |
+          (np.asarray(full["coll"][lo:hi], dtype=np.uint32) << np.uint32(31)))
+    return {"b": b, "e": e, "counts": np.diff(rp[b:e + 1]).astype(np.int32), "dst_coll": dc,
+            "w": np.asarray(full["w"][lo:hi], np.float32), "s": np.asarray(full["s"][lo:hi], np.float32),
+            "c": np.asarray(full["c"][lo:hi], np.float32)}
+
+
+def assemble_csr(blocks, n: int) -> dict:
+    """Concatenate row blocks (any order; they must tile [0, n)) into one CSR:
+    row_ptr [n+1] int32, dst_coll, w, s, c."""
+    blocks = sorted(blocks, key=lambda k: k["b"])
+    if blocks[0]["b"] != 0 or blocks[-1]["e"] != n or any(x["e"] != y["b"] for x, y in zip(blocks, blocks[1:])):
+        raise ValueError("row blocks do not tile [0, n)")
+    counts = np.concatenate([k["counts"] for k in blocks])
+    row_ptr = np.zeros(n + 1, np.int64)
+    np.cumsum(counts, out=row_ptr[1:])
+    cat = {f: np.concatenate([k[f] for k in blocks]) for f in ("dst_coll", "w", "s", "c")}
+    return {"row_ptr": row_ptr.astype(np.int32), **cat}
+
+
+def gather_csr_blocks(block: dict, world: int):
+    """All-gather every rank's CSR block (one collective round: sizes, then the
+    padded 16-byte edge records and row counts)."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return [block]
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    meta = torch.tensor([block["b"], block["e"], block["dst_coll"].size], dtype=torch.int64, device=dev)
+    metas = [torch.empty_like(meta) for _ in range(world)]
+    dist.all_gather(metas, meta)
+    metas = [m.cpu().numpy() for m in metas]
+    max_rows = int(max(m[1] - m[0] for m in metas))
+    max_nnz = int(max(m[2] for m in metas))
+    rec = np.zeros((max(max_nnz, 1), 4), np.uint32)
+    nnz = block["dst_coll"].size
+    rec[:nnz, 0] = block["dst_coll"]
+    for j, f in enumerate(("w", "s", "c")):
+        rec[:nnz, j + 1] = block[f].view(np.uint32)
+    cnt = np.zeros(max(max_rows, 1), np.int32)
+    cnt[: block["counts"].size] = block["counts"]
+    t_rec = torch.from_numpy(rec.view(np.int32)).to(dev)
+    t_cnt = torch.from_numpy(cnt).to(dev)
+    recs = [torch.empty_like(t_rec) for _ in range(world)]
+    cnts = [torch.empty_like(t_cnt) for _ in range(world)]
+    dist.all_gather(recs, t_rec)
+    dist.all_gather(cnts, t_cnt)
+    out = []
+    for m, r_, c_ in zip(metas, recs, cnts):
+        b, e, k = int(m[0]), int(m[1]), int(m[2])
+        r_ = r_.cpu().numpy().view(np.uint32)[:k]
+        out.append({"b": b, "e": e, "counts": c_.cpu().numpy()[: e - b], "dst_coll": r_[:, 0].copy(),
+                    "w": r_[:, 1].copy().view(np.float32), "s": r_[:, 2].copy().view(np.float32),
+                    "c": r_[:, 3].copy().view(np.float32)})
+    return out

@@ -9,7 +9,8 @@ from typing import Any, Dict, List, Sequence
 
 import numpy as np
 
-from . import (MPAP_MEM_DEVICE, Roadmap, mpap_build_roadmap, mpap_build_roadmap_batch, mpap_mc_verify_batch,
+from . import (MPAP_MEM_DEVICE, Roadmap, mpap_build_roadmap, mpap_build_roadmap_batch, mpap_build_roadmap_rows,
+               mpap_mc_verify_batch, mpap_roadmap_export, mpap_roadmap_import,
                mpap_search, mpap_search_batch, params_from_problem)
 
 
@@ -21,6 +22,30 @@ def build_problem(prob, stream=None, edge_peaks: bool = False, lazy_edges: bool 
                             feat if feat is not None else np.zeros((0, prob.pos_dim)), prob.r, prm, stream=stream)
     del keep
     return rm
+
+
+def build_problem_rows(prob, row_begin: int, row_end: int, stream=None) -> Roadmap:
+    """Row-sharded build of one environment (rows [row_begin, row_end))."""
+    prm, keep = params_from_problem(prob)
+    obst = prob.obstacles if prob.obstacles.size else np.zeros((0, 2 * prob.pos_dim))
+    feat = prob.features if prob.features.size else np.zeros((0, prob.pos_dim))
+    rm = mpap_build_roadmap_rows(prob.samples, obst, feat, prob.r, prm, row_begin, row_end, stream=stream)
+    del keep
+    return rm
+
+
+def build_problem_sharded(prob, rank: int, world: int, stream=None) -> Roadmap:
+    """rank builds its row block, the blocks are all-gathered
+    (one collective) and concatenated, and every rank wraps the full CSR for
+    search (mpap_roadmap_import: search-only, no geometry)."""
+    from .dist import assemble_csr, csr_block, gather_csr_blocks, row_block
+    b, e = row_block(rank, world, prob.n)
+    part = build_problem_rows(prob, b, e, stream=stream)
+    block = csr_block(mpap_roadmap_export(part), b, e)
+    part.free()
+    full = assemble_csr(gather_csr_blocks(block, world), prob.n)
+    return mpap_roadmap_import(prob.samples[:, : prob.pos_dim], full["row_ptr"], full["dst_coll"], full["w"],
+                               full["s"], full["c"], prob.r, stream=stream)
 
 
 def search_problem(rm: Roadmap, prob, beta: float, env: int = 0, lam=None, trace_waves: int = 0,

@@ -92,6 +92,56 @@ def test_mc_sharded_trials_two_ranks(tmp_path, orc):
     assert a[1] == 0 and b[1] == a[2] and a[2] + b[2] == trials
 
 
+def _csr_worker(rank, world, port, outdir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "mpap_dist", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                  "paper_1705_02408_b200", "dist.py"))
+    md = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(md)
+    import oracle
+    from synth import load_config, make_problem
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = load_config("c1")
+    cfg["n_samples"] = 150
+    prob = make_problem(cfg)
+    b, e = md.row_block(rank, world, prob.n)
+    # this rank's row block (the oracle's rows stand in for k_near/k_edges on the rank's GPU)
+    rows = [oracle.build_row(prob, u) for u in range(b, e)]
+    block = {"b": b, "e": e, "counts": np.array([r["dst"].size for r in rows], np.int32),
+             "dst_coll": np.concatenate([r["dst"].astype(np.uint32) | (r["coll"].astype(np.uint32) << np.uint32(31))
+                                         for r in rows]),
+             "w": np.concatenate([r["w"] for r in rows]), "s": np.concatenate([r["s"] for r in rows]),
+             "c": np.concatenate([r["c"] for r in rows])}
+    full = md.assemble_csr(md.gather_csr_blocks(block, world), prob.n)
+    np.savez(os.path.join(outdir, f"csr{rank}.npz"), **full)
+    dist.destroy_process_group()
+
+
+def test_row_sharded_csr_two_ranks(tmp_path, orc):
+    """Row-sharded build: the all-gathered, concatenated
+    row blocks equal the single-process CSR bit for bit on every rank."""
+    world = 2
+    port = _free_port()
+    tmp.start_processes(_csr_worker, args=(world, port, str(tmp_path)), nprocs=world, start_method="spawn")
+    from synth import load_config, make_problem
+    cfg = load_config("c1")
+    cfg["n_samples"] = 150
+    o = orc.build_roadmap(make_problem(cfg))
+    for rank in range(world):
+        g = np.load(tmp_path / f"csr{rank}.npz")
+        assert np.array_equal(g["row_ptr"], o["row_ptr"])
+        assert np.array_equal(g["dst_coll"] & 0x7FFFFFFF, o["dst"].astype(np.uint32))
+        assert np.array_equal(g["dst_coll"] >> 31, o["coll"].astype(np.uint32))
+        for k in ("w", "s", "c"):
+            assert np.array_equal(g[k].view(np.uint32), o[k].view(np.uint32)), k
+
+
 def test_gather_two_ranks(tmp_path):
     world, Q = 2, 5
     port = _free_port()
@@ -116,6 +166,10 @@ def test_shards_disjoint_and_cover():
     with pytest.raises(ValueError):
         md.shard_envs(2, 2, 4)
     for world in (1, 2, 3, 8):
+        for n in (0, 1, 5, 4001):
+            blocks = [md.row_block(r, world, n) for r in range(world)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == n
+            assert all(blocks[r][1] == blocks[r + 1][0] for r in range(world - 1))
         for trials in (0, 1, 7, 1000):
             parts = [md.mc_trial_shard(r, world, trials) for r in range(world)]
             assert sum(n for _, n in parts) == trials
