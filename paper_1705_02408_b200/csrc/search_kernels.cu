@@ -47,6 +47,7 @@ namespace cg = cooperative_groups;
 #define FULLM 0xffffffffu
 constexpr int kST = 512;              // threads per search CTA
 constexpr int kCluster = 8;           // CTAs per query in cluster mode (portable cluster size)
+constexpr int kMrgCap = 48;           // merge: a node's candidates / staircase staged in shared memory up to this size
 enum : uint8_t { L_OPEN = 0, L_CLOSED = 1, L_DEAD = 2 };
 enum { OVF_LABELS = 1, OVF_CAND = 2, OVF_STAIR = 4 };
 constexpr int kRetryBase = 100;       // result.status = kRetryBase + OVF_* mask
@@ -427,6 +428,14 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
     team.sync();
     // ---- a8 RemoveDominated + insert (A3.10-A3.15): warp per touched node ----
     {
+      // per-warp shared-memory staging of the node's candidates (sorted copy,
+      // then survivors) and of its non-dominated staircase: the all-pairs
+      // dominance loops read them from shared memory (global fallback above
+      // kMrgCap entries)
+      __shared__ int4 s_cand[kST / 32][2][kMrgCap];
+      __shared__ float2 s_sch[kST / 32][kMrgCap];
+      __shared__ int32_t s_sid[kST / 32][kMrgCap];
+      const int wl = threadIdx.x >> 5;
       unsigned long long my_ins = 0, my_kill = 0;
       for (int t = warp; t < nt; t += nw) {
         const int x = touched[t];
@@ -441,15 +450,31 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
         int32_t* nsi = sid + ((size_t)(par ^ 1) * n + x) * (size_t)C.K;
         int4* srt = cand + beg;   // candidate buffer is free after grouping: sorted copy
         int4* sv = cs + beg;      // then the grouped range holds the sorted survivors
+        const int4* cin = cs + beg;
+        if (kc <= kMrgCap) {      // stage the candidates; sort into / survivors in shared memory
+          for (int q = lane; q < kc; q += 32) s_cand[wl][0][q] = cs[beg + q];
+          cin = s_cand[wl][0];
+          srt = s_cand[wl][1];
+          sv = s_cand[wl][0];     // written after the sort has read every staged candidate
+        }
+        if (m <= kMrgCap) {       // stage the staircase (its dead marks stay in the copy)
+          for (int j = lane; j < m; j += 32) {
+            s_sch[wl][j] = st[j];
+            s_sid[wl][j] = si[j];
+          }
+          st = s_sch[wl];
+          si = s_sid[wl];
+        }
+        __syncwarp();
         // 1. sort the node's candidates by (cost asc, h desc), ties by index
         for (int q0 = 0; q0 < kc; q0 += 32) {
           const int qq = q0 + lane;
           if (qq < kc) {
-            const int4 cq = cs[beg + qq];
+            const int4 cq = cin[qq];
             const float qc = __int_as_float(cq.y), qh = __int_as_float(cq.z);
             int rank = 0;
             for (int r2 = 0; r2 < kc; ++r2) {
-              const int4 cr = cs[beg + r2];
+              const int4 cr = cin[r2];
               const float rc = __int_as_float(cr.y), rh = __int_as_float(cr.z);
               if (key_less(rc, rh, qc, qh) || (rc == qc && rh == qh && r2 < qq)) ++rank;
             }
