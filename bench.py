@@ -134,10 +134,12 @@ def make_shard(cfg, rank: int, world: int, Q: int):
     return [make_problem(cfg, env_index=e) for e in shard_envs(rank, world, Q)]
 
 
-def cpu_baseline(cfg, beta: float, procs: int):
+def cpu_baseline(cfg, beta: float, procs: int, gpu_env0=None, gpu_path0=None):
     """The oracle as it stands on one environment+query of the workload:
     build rows spread over `procs` processes (each the sequential oracle),
-    search single-threaded."""
+    search single-threaded.  With the GPU's result record and plan for env 0
+    of the timed step, also reports the parity gate (status, plan, cost and
+    perception bits, relaxations equal)."""
     import oracle
     from synth import make_problem
     oracle.build()
@@ -147,11 +149,20 @@ def cpu_baseline(cfg, beta: float, procs: int):
     t1 = time.perf_counter()
     res = oracle.search(rm, prob, beta)
     t2 = time.perf_counter()
-    return {"value": 1.0 / (t2 - t0), "unit": "queries/s", "cores": procs, "kind": "oracle",
-            "sample": f"1 {cfg['name']} environment+query (env 0, n={prob.n}): oracle build {t1 - t0:.2f} s "
-                      f"over {procs} processes + oracle search {t2 - t1:.3f} s (1 thread), beta={beta}",
-            "edges_relaxed_per_s": res["relaxations"] / (t2 - t0),
-            "search_only_edges_relaxed_per_s": res["relaxations"] / max(t2 - t1, 1e-9)}
+    out = {"value": 1.0 / (t2 - t0), "unit": "queries/s", "cores": procs, "kind": "oracle",
+           "sample": f"1 {cfg['name']} environment+query (env 0, n={prob.n}): oracle build {t1 - t0:.2f} s "
+                     f"over {procs} processes + oracle search {t2 - t1:.3f} s (1 thread), beta={beta}",
+           "edges_relaxed_per_s": res["relaxations"] / (t2 - t0),
+           "search_only_edges_relaxed_per_s": res["relaxations"] / max(t2 - t1, 1e-9)}
+    if gpu_env0 is not None:
+        g = gpu_env0
+        ok = int(g["status"]) == int(res["status"]) and int(g["relaxations"]) == int(res["relaxations"])
+        if ok and res["status"] == 0:
+            ok = (gpu_path0.tolist() == res["path"].tolist()
+                  and np.float32(g["cost"]).view(np.uint32) == np.float32(res["cost"]).view(np.uint32)
+                  and np.float32(g["h"]).view(np.uint32) == np.float32(res["h"]).view(np.uint32))
+        out["parity_gate_env0"] = bool(ok)
+    return out
 
 
 def run_reference(args, cfg, beta):
@@ -278,6 +289,7 @@ def main():
 
     # results of the last step (outside the timed region)
     res = res_d.cpu().numpy().view(mp.RESULT_DTYPE)
+    paths_h = paths_d.cpu().numpy()
     relax_step = int(res["relaxations"].sum())
     feasible = int((res["status"] == 0).sum())
     ok = bool(np.all((res["status"] == 0) | (res["status"] == 3)))
@@ -371,7 +383,8 @@ def main():
         line["mc_verify"] = measure_mc(mp, B, betas, PATH_CAP, args.mc_trials, rank == 0 and world == 1
                                        and not args.no_cpu_baseline)
     if (rank == 0) and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg, beta, args.cpu_procs or os.cpu_count() or 1)
+        line["cpu_baseline"] = cpu_baseline(cfg, beta, args.cpu_procs or os.cpu_count() or 1, res[0],
+                                            paths_h[0][: int(res[0]["path_len"])])
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
