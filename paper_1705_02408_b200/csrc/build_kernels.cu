@@ -785,44 +785,59 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
   const double R2 = R * R;
   const double cos2 = P.fov_cos_half * P.fov_cos_half;
   constexpr int heur = HEUR;
-  const float half_fov = acosf((float)P.fov_cos_half);
   const unsigned lt = lanemask_lt();
-  bool ang = false;
-  float ux = 0.0f, uy = 0.0f, c1 = 0.0f, s1 = 0.0f, smax = -1.0f;
+  // bearing cull half angle: FOV half angle + 2e-3 rad margin (cos, sin)
+  float chf = 0.0f, shf = 0.0f;
   if (heur >= 2) {
-    const float ax = (float)hu0, ay = (float)hu1;
-    const float sb = (float)(((double)(K - 1) * Dl) / T);
-    const float bx = fmaf(sb, (float)hv0 - ax, ax), by = fmaf(sb, (float)hv1 - ay, ay);
-    const float ex = bx - ax, ey = by - ay;
-    const float ee = ex * ex + ey * ey;
-    float tq = (ee > 0.0f) ? -(ax * ex + ay * ey) / ee : 0.0f;
-    tq = fminf(fmaxf(tq, 0.0f), 1.0f);
-    const float qx = ax + tq * ex, qy = ay + tq * ey;
-    if (qx * qx + qy * qy > 1e-4f) {
-      const float na = rsqrtf(ax * ax + ay * ay), nb = rsqrtf(bx * bx + by * by);
-      const float dax = ax * na, day = ay * na, dbx = bx * nb, dby = by * nb;
-      const float mx = dax + dbx, my = day + dby;
-      const float mn = sqrtf(mx * mx + my * my);
-      if (mn > 1e-2f) {
-        ux = mx / mn;
-        uy = my / mn;
-        const float dev = 0.5f * atan2f(fabsf(dax * dby - day * dbx), dax * dbx + day * dby);
-        const float beta0 = acosf((float)P.fov_cos_half) + dev + 2e-3f;   // half angle + arc + margin
-        const float wmax = 3.1315927f - beta0;                             // keep the total below pi - 0.01
-        if (wmax > 0.0f) {
-          ang = true;
-          c1 = cosf(beta0);
-          s1 = sinf(beta0);
-          smax = (wmax >= 1.5707963f) ? 2.0f : sinf(wmax);
-        }
-      }
-    }
+    const float hf = acosf((float)P.fov_cos_half) + 2e-3f;
+    chf = cosf(hf);
+    shf = sinf(hf);
   }
   for (int k0 = 0; k0 < K; k0 += 32) {
     const int nk = min(32, K - k0);
     const double ta = (double)k0 * Dl, tb = (double)(k0 + nk - 1) * Dl;
     double lo[D], hi[D];
     chunk_bbox<D, DYN>(su, sv, c2, c3, r0, r1, T, ta, tb, lo, hi);
+    // Heading arc of the chunk (heading heuristics): the step headings lie on
+    // the chord between the interpolated headings at the chunk's first and
+    // last step, so their directions are within dev of the chord's mid
+    // direction (ux, uy).  beta0 = half FOV + margin + dev; a feature whose
+    // bearing from the chunk is beyond beta0 (+ the chunk's angular radius)
+    // fails every step's FOV test.
+    bool ang = false;
+    float ux = 0.0f, uy = 0.0f, c1 = 0.0f, s1 = 0.0f, smax = -1.0f;
+    if (heur >= 2) {
+      const float sa = (float)(ta / T), sb = (float)(tb / T);
+      const float hx0 = (float)hu0, hy0 = (float)hu1, gx = (float)hv0 - hx0, gy = (float)hv1 - hy0;
+      const float ax = fmaf(sa, gx, hx0), ay = fmaf(sa, gy, hy0);
+      const float bx = fmaf(sb, gx, hx0), by = fmaf(sb, gy, hy0);
+      const float ex = bx - ax, ey = by - ay;
+      const float ee = ex * ex + ey * ey;
+      float tq = (ee > 0.0f) ? -(ax * ex + ay * ey) / ee : 0.0f;
+      tq = fminf(fmaxf(tq, 0.0f), 1.0f);
+      const float qx = ax + tq * ex, qy = ay + tq * ey;
+      if (qx * qx + qy * qy > 1e-4f) {
+        const float na = rsqrtf(ax * ax + ay * ay), nb2 = rsqrtf(bx * bx + by * by);
+        const float dax = ax * na, day = ay * na, dbx = bx * nb2, dby = by * nb2;
+        const float mx = dax + dbx, my = day + dby;
+        const float mn = sqrtf(mx * mx + my * my);
+        if (mn > 1e-2f) {
+          ux = mx / mn;
+          uy = my / mn;
+          // |da + db| = 2 cos(dev), |da - db| = 2 sin(dev)
+          const float cd = 0.5f * mn;
+          const float sd = 0.5f * sqrtf((dax - dbx) * (dax - dbx) + (day - dby) * (day - dby));
+          c1 = chf * cd - shf * sd;   // cos(beta0)
+          s1 = shf * cd + chf * sd;   // sin(beta0)
+          if (c1 > -0.99995f) {       // beta0 < pi - 0.01
+            ang = true;
+            // omega may reach pi - 0.01 - beta0: unbounded if that is >= pi / 2,
+            // else sin(pi - 0.01 - beta0) = sin(beta0 + 0.01)
+            smax = (c1 >= 0.0099998f) ? 2.0f : s1 * 0.99995f + c1 * 0.0099998f;
+          }
+        }
+      }
+    }
     // Conservative single-precision culls (only discard features whose exact
     // test provably fails; margins >> float rounding):
     //  * range: distance(feature, chunk box) > R + 1e-3;
