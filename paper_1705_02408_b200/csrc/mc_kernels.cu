@@ -218,12 +218,15 @@ __global__ void __launch_bounds__(kMcWarps * 32, MPAP_MC_MIN_BLOCKS) k_mc(const 
     const uint64_t key = mc_mix(M.seed + 0x9E3779B97F4A7C15ULL * ((uint64_t)tr + 1ULL));
     const int64_t s0 = seg_off[p], s1 = seg_off[p + 1];
     double x[D], v[D], xh[D], vh[D];
-    {
-      const McSeg& S = segs[s0 < s1 ? s0 : 0];
-      // a zero-edge plan (start in goal) never reads the state
 #pragma unroll
-      for (int j = 0; j < D; ++j) { x[j] = S.su[j]; v[j] = S.su[D + j]; xh[j] = x[j]; vh[j] = v[j]; }
+    for (int j = 0; j < D; ++j) { x[j] = 0.0; v[j] = 0.0; }
+    if (s0 < s1) {   // a zero-edge plan (start in goal) has no steps and zero errors
+      const McSeg& S = segs[s0];
+#pragma unroll
+      for (int j = 0; j < D; ++j) { x[j] = S.su[j]; v[j] = S.su[D + j]; }
     }
+#pragma unroll
+    for (int j = 0; j < D; ++j) { xh[j] = x[j]; vh[j] = v[j]; }
     double p11 = M.p0_pos, p12 = 0.0, p22 = M.p0_vel;
     double me = 0.0, md = 0.0;
     uint64_t ctr = 0;
