@@ -115,12 +115,18 @@ def test_struct_layouts_match_header(mp, tmp_path):
     """The ctypes mirrors of mpap_params / mpap_goal / mpap_result / mpap_wave
     have the C header's sizes and field offsets (compiled here with gcc)."""
     structs = {"mpap_params": mp.mpap_params, "mpap_goal": mp.mpap_goal, "mpap_result": mp.mpap_result,
-               "mpap_wave": mp.mpap_wave}
+               "mpap_wave": mp.mpap_wave, "mpap_mc_params": mp.mpap_mc_params}
+    dtypes = {"mpap_mc_result": mp.MC_RESULT_DTYPE, "mpap_result_np": mp.RESULT_DTYPE}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "mpap.h"', "int main(void) {"]
     for name, cls in structs.items():
         lines.append(f'  printf("{name} size %zu\\n", sizeof({name}));')
         for f in cls._fields_:
             lines.append(f'  printf("{name} {f[0]} %zu\\n", offsetof({name}, {f[0]}));')
+    for name, dt in dtypes.items():
+        cname = name.replace("_np", "")
+        lines.append(f'  printf("{name} size %zu\\n", sizeof({cname}));')
+        for f in dt.names:
+            lines.append(f'  printf("{name} {f} %zu\\n", offsetof({cname}, {f}));')
     lines.append("  return 0; }")
     src = tmp_path / "layout.c"
     src.write_text("\n".join(lines))
@@ -131,6 +137,10 @@ def test_struct_layouts_match_header(mp, tmp_path):
         if not ln:
             continue
         name, field, val = ln.split()
-        cls = structs[name]
-        want = C.sizeof(cls) if field == "size" else getattr(cls, field).offset
+        if name in dtypes:
+            dt = dtypes[name]
+            want = dt.itemsize if field == "size" else dt.fields[field][1]
+        else:
+            cls = structs[name]
+            want = C.sizeof(cls) if field == "size" else getattr(cls, field).offset
         assert int(val) == want, (name, field, val, want)
