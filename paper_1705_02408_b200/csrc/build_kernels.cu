@@ -959,11 +959,16 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
           if (dot < 0.0) continue;
           if (dot * dot < cos2 * (hh * dd)) continue;
         }
+        ++W.occl_segs;
+        const unsigned long long fm = use_mask ? L.fmask[i] : ~0ull;
+        if (fm == 0ull) {   // no box meets the chunk-feature box: unobstructed (warp-uniform)
+          ++kv;
+          continue;
+        }
         double fp[D];
 #pragma unroll
         for (int j = 0; j < D; ++j) fp[j] = L.f[j][i];
-        ++W.occl_segs;
-        const unsigned rr = use_mask ? seg_hits_boxes<D, true>(x, fp, dl, L.box, nb, L.fmask[i])
+        const unsigned rr = use_mask ? seg_hits_boxes<D, true>(x, fp, dl, L.box, nb, fm)
                                      : seg_hits_boxes<D, false>(x, fp, dl, L.box, nb, 0ull);
         W.occl_tests += rr >> 1;
         if (!(rr & 1u)) ++kv;
