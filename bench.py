@@ -378,7 +378,7 @@ def main():
         line["e2e"] = e2e
     if not args.no_lazy:
         line["lazy_variant"] = measure_lazy(mp, B, s_d, o_d, f_d, betas, PATH_CAP, paths_d, res_d, flush, args.steps,
-                                            res)
+                                            res, world)
     if not args.no_mc:
         line["mc_verify"] = measure_mc(mp, B, betas, PATH_CAP, args.mc_trials, rank == 0 and world == 1
                                        and not args.no_cpu_baseline)
@@ -392,7 +392,7 @@ def main():
     return 0
 
 
-def measure_lazy(mp, B, s_d, o_d, f_d, betas, path_cap, paths_d, res_d, flush, steps, res_eager):
+def measure_lazy(mp, B, s_d, o_d, f_d, betas, path_cap, paths_d, res_d, flush, steps, res_eager, world=1):
     """NEXT-1 part i variant of the same step: the roadmap is built lazily
     (Near + Cost) and the batched search evaluates the rows its waves need
     (suspend / evaluate the union of requested rows / resume).  Same plans --
@@ -432,7 +432,13 @@ def measure_lazy(mp, B, s_d, o_d, f_d, betas, path_cap, paths_d, res_d, flush, s
     res = res_d.cpu().numpy().view(mp.RESULT_DTYPE)
     same = all(np.array_equal(res[k], res_eager[k]) for k in ("status", "path_len", "cost", "h", "relaxations"))
     Q = len(B.probs)
-    return {"queries_per_s": Q * steps / (ms / 1e3), "ms_per_step": ms / steps, "rows_evaluated": rows[0],
+    if world > 1:   # whole-job value: all ranks' queries over the slowest rank's time
+        import torch.distributed as dist
+        t = torch.tensor([ms, float(same)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.MIN)
+        ms, same = float(t[0].item()), bool(t[1].item())
+    return {"queries_per_s": world * Q * steps / (ms / 1e3), "ms_per_step": ms / steps, "rows_evaluated": rows[0],
             "rows_total": int(B.n.sum()), "same_results_as_eager": bool(same), "gpu_launches_per_step": launches / steps,
             "kernels_ms_per_step": {k: v[0] / steps for k, v in kern.items()},
             "search_launches_per_step": kern["k_search"][1] / steps}
@@ -464,7 +470,8 @@ def measure_mc(mp, B, betas, path_cap: int, trials: int, with_cpu: bool):
         return {"plans": 0}
     t = (ms + ms_plan) / runs / 1e3
     steps = float(mres["steps"].sum()) * trials
-    out = {"plans": int(ok.size), "trials_per_plan": trials, "ms_per_batch": (ms + ms_plan) / runs,
+    out = {"scope": "this rank's plans (per GPU)", "plans": int(ok.size), "trials_per_plan": trials,
+           "ms_per_batch": (ms + ms_plan) / runs,
            "k_mc_ms": ms / max(n, 1), "trials_per_s": ok.size * trials / t, "trial_steps_per_s": steps / t,
            "p_hat_mean": float(mres["p_hat"].mean()), "fix_fraction": float(mres["fixes"].sum() / max(steps, 1)),
            "params": {k: mc[k] for k in ("sigma_imu", "sigma_vis", "delta", "k_p", "k_d", "u_max")}}
