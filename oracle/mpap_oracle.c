@@ -21,9 +21,12 @@
  *                  R31-R36 (NEXT-4).
  *
  * Pins: tests/test_oracle_*.py (closed forms, brute force, Dijkstra in the
- * exact regime, dense-sampling collision, SPEC worked examples).  Functions
- * whose result has no independent pin are listed in DESIGN.md §4 as
- * "parity unpinned".
+ * exact regime, dense-sampling collision, SPEC worked examples; Monte Carlo:
+ * double-integrated white-noise variance, exact fixes, Kalman consistency,
+ * zero-noise tracking).  Parity unpinned: orc_search at
+ * lambda = 0.5 on the C1-C5 roadmaps beyond its invariants, and whole-edge
+ * heuristic summaries on the generated environments (pinned only through
+ * their primitives).
  *
  * Compile: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared
  * (no implicit FMA contraction, no fast-math: every + - * / sqrt is one
