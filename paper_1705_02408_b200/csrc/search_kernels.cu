@@ -46,7 +46,7 @@ namespace cg = cooperative_groups;
 
 #define FULLM 0xffffffffu
 constexpr int kST = 512;              // threads per search CTA
-constexpr int kCluster = 8;           // CTAs per query in cluster mode (portable cluster size)
+constexpr int kCluster = 8;           // largest CTAs per query in cluster mode (portable cluster size)
 constexpr int kMrgCap = 48;           // merge: a node's candidates / staircase staged in shared memory up to this size
 enum : uint8_t { L_OPEN = 0, L_CLOSED = 1, L_DEAD = 2 };
 enum { OVF_LABELS = 1, OVF_CAND = 2, OVF_STAIR = 4 };
@@ -880,10 +880,13 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     // one query: the whole grid works on it (cooperative launch); otherwise one
     // CTA per query and as many slots as resident CTAs
     const bool grid_mode = (nrun == 1) && use_grid;
-    // few queries: one cluster of kCluster CTAs per query; many: one CTA each
-    // (a lazy roadmap runs batches in cluster mode, one static slot per query,
-    // so suspended queries resume in place)
-    const bool cluster_mode = !grid_mode && use_cluster && (nrun * kCluster <= nsm * occ || rm->lazy);
+    // few queries: one cluster per query, as many CTAs per cluster (8, 4 or 2)
+    // as keep every cluster resident; many: one CTA each.  (A lazy roadmap
+    // runs batches in cluster mode, one static slot per query, so suspended
+    // queries resume in place.)
+    int csize = kCluster;
+    while (csize > 2 && nrun * csize > nsm * occ) csize >>= 1;
+    const bool cluster_mode = !grid_mode && use_cluster && (nrun * csize <= nsm * occ || rm->lazy);
     const int nslots = grid_mode ? 1 : cluster_mode ? nrun : std::min(nrun, nsm * occ);
     const size_t sb_slots = carve(nullptr, caps, nslots, nullptr);
     const size_t sb = sb_slots + sizeof(Ctl) * (size_t)nslots + 256;
@@ -950,12 +953,12 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
             CKS(cudaLaunchCooperativeKernel(fn, dim3(nsm * occ_grid), dim3(kST), args, 0, st));
           } else {
             cudaLaunchConfig_t cfg{};
-            cfg.gridDim = dim3(nslots * kCluster);
+            cfg.gridDim = dim3(nslots * csize);
             cfg.blockDim = dim3(kST);
             cfg.stream = st;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = kCluster;
+            attr[0].val.clusterDim.x = csize;
             attr[0].val.clusterDim.y = 1;
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
@@ -984,13 +987,13 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
         CKS(cudaLaunchCooperativeKernel(fn, dim3(nsm * occ_grid), dim3(kST), args, 0, st));
       } else if (cluster_mode) {
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(nslots * kCluster);
+        cfg.gridDim = dim3(nslots * csize);
         cfg.blockDim = dim3(kST);
         cfg.dynamicSmemBytes = 0;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = kCluster;
+        attr[0].val.clusterDim.x = csize;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
