@@ -139,3 +139,17 @@ def test_lazy_forall_t_equals_eager(mp):
                                                                                       Ce.view(np.uint32))
     lazy.free()
     eager.free()
+
+
+def test_lazy_c4_full_single_query(mp):
+    """C4 at full size: the whole-grid lazy search equals the eager one at the
+    agnostic bound and at 2 beta_min (39 waves of suspend / evaluate / resume)."""
+    cfg = load_config("c4")
+    prob = make_problem(cfg)
+    eager = mp.pb.build_problem(prob)
+    for beta in (INF, 17.303):
+        lazy = mp.pb.build_problem(prob, lazy_edges=True)
+        same(mp.pb.search_problem(lazy, prob, beta), mp.pb.search_problem(eager, prob, beta))
+        assert mp.mpap_roadmap_rows_evaluated(lazy) < prob.n
+        lazy.free()
+    eager.free()

@@ -162,3 +162,20 @@ def test_mc_kinematic_rejected(mp):
     with pytest.raises(mp.MpapError):
         mp.mpap_mc_verify(rm, 0, [0], mc_params(trials=4))
     rm.free()
+
+
+def test_mc_c4_full_plan_sampled(mp, orc):
+    """C4 at full size (n = 16 001, 200 boxes, 400 features): MC of the
+    agnostic plan in one launch; sampled trials recomputed by the oracle."""
+    cfg = load_config("c4")
+    prob = make_problem(cfg)
+    rm = mp.pb.build_problem(prob)
+    r = mp.pb.search_problem(rm, prob, float("inf"))
+    assert r["status"] == 0
+    mc = mc_params(trials=128)
+    g = mp.mpap_mc_verify(rm, 0, r["path"], mc)
+    for t in (0, 77, 127):
+        o = orc.mc_trial(prob, r["path"], mc, t)
+        assert g["max_err"][t] == o["max_err"] and g["max_dev"][t] == o["max_dev"], t
+    assert g["steps"] == orc.mc_trial(prob, r["path"], mc, 0)["steps"]
+    rm.free()
