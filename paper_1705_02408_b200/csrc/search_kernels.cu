@@ -842,7 +842,7 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
   CKS(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   if (trace) CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_grid, k_search_grid<true>, kST, 0));
   else CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_grid, k_search_grid<false>, kST, 0));
-  const bool use_grid = coop && occ_grid > 0 && getenv("MPAP_SEARCH_CTA") == nullptr;
+  const bool use_grid = coop && occ_grid > 0 && getenv("MPAP_SEARCH_CTA") == nullptr && getenv("MPAP_SEARCH_NO_GRID") == nullptr;
   const bool use_cluster = getenv("MPAP_SEARCH_CTA") == nullptr && getenv("MPAP_SEARCH_NO_CLUSTER") == nullptr;
   SlotCaps caps;
   caps.n = rm->n_max;
