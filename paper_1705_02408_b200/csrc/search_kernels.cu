@@ -880,8 +880,10 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     // one query: the whole grid works on it (cooperative launch); otherwise one
     // CTA per query and as many slots as resident CTAs
     const bool grid_mode = (nrun == 1) && use_grid;
-    // few queries: one cluster per query, as many CTAs per cluster (8, 4 or 2)
-    // as keep every cluster resident; many: one CTA each.  (A lazy roadmap
+    // few queries: one cluster per query of 8, 4 or 2 CTAs -- the largest
+    // with nrun x size <= SMs x (one-CTA-kernel occupancy); for the bench's
+    // 64 queries that is 4 (measured: 2.0 ms vs 2.2 / 3.6 ms for 2 / 8 CTAs,
+    // 3.5 ms for one CTA per query); many: one CTA each.  (A lazy roadmap
     // runs batches in cluster mode, one static slot per query, so suspended
     // queries resume in place.)
     int csize = kCluster;
