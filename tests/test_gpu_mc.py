@@ -179,3 +179,15 @@ def test_mc_c4_full_plan_sampled(mp, orc):
         assert g["max_err"][t] == o["max_err"] and g["max_dev"][t] == o["max_dev"], t
     assert g["steps"] == orc.mc_trial(prob, r["path"], mc, 0)["steps"]
     rm.free()
+
+
+def test_mc_large_trial_ids(mp, orc):
+    """Trial ids beyond 32 bits (64-bit counter streams on both sides)."""
+    prob = line([[2.0, 3.0, 1.5], [1.0, -2.0, 1.0]], heuristic=2, max_range=4.0)
+    rm = mp.pb.build_problem(prob)
+    mc = mc_params(trials=8, sigma_imu=0.4, sigma_vis=0.1, delta=0.05)
+    t0 = (1 << 40) + 12345
+    g = mp.mpap_mc_verify(rm, 0, [0, 1, 2], mc, trial0=t0)
+    o = orc.mc_verify(prob, [0, 1, 2], mc, t0)
+    check(g, o, 8)
+    rm.free()

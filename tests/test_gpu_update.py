@@ -130,3 +130,18 @@ def test_update_rejects_bad_input(mp):
     with pytest.raises(mp.MpapError) as ei:
         mp.mpap_roadmap_update(imp, 0, np.zeros((0, 4)), np.zeros((0, 2)))
     assert ei.value.status == mp.MPAP_ERR_INVALID_ARGUMENT
+
+
+def test_update_of_a_lazy_roadmap(mp, orc):
+    """A partially evaluated lazy roadmap (NEXT-1 part i) that is then updated
+    (part ii) equals the oracle's full build of the new environment."""
+    prob = small("c3", 500)
+    lazy = mp.pb.build_problem(prob, lazy_edges=True)
+    mp.pb.search_problem(lazy, prob, INF)          # evaluates some rows only
+    assert mp.mpap_roadmap_rows_evaluated(lazy) < prob.n
+    rng = np.random.default_rng(5)
+    name, boxes, feats = _changes(prob, rng)[0]
+    mp.mpap_roadmap_update(lazy, 0, boxes, feats)
+    new = dataclasses.replace(prob, obstacles=boxes, features=feats)
+    assert_roadmap_equal(mp.mpap_roadmap_export(lazy), orc.build_roadmap(new))
+    lazy.free()
