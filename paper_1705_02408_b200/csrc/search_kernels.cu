@@ -47,6 +47,7 @@ namespace cg = cooperative_groups;
 #define FULLM 0xffffffffu
 constexpr int kST = 512;              // threads per search CTA
 constexpr int kCluster = 8;           // largest CTAs per query in cluster mode (portable cluster size)
+constexpr int kSeqQueries = 8;       // batches up to this size run query by query on the whole grid
 constexpr int kMrgCap = 48;           // merge: a node's candidates / staircase staged in shared memory up to this size
 enum : uint8_t { L_OPEN = 0, L_CLOSED = 1, L_DEAD = 2 };
 enum { OVF_LABELS = 1, OVF_CAND = 2, OVF_STAIR = 4 };
@@ -844,6 +845,18 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
   else CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_grid, k_search_grid<false>, kST, 0));
   const bool use_grid = coop && occ_grid > 0 && getenv("MPAP_SEARCH_CTA") == nullptr && getenv("MPAP_SEARCH_NO_GRID") == nullptr;
   const bool use_cluster = getenv("MPAP_SEARCH_CTA") == nullptr && getenv("MPAP_SEARCH_NO_CLUSTER") == nullptr;
+  // A handful of queries (a perception-bound sweep) runs one after the other
+  // on the whole grid: 8-CTA clusters would leave most SMs idle (C4 sweep of 6
+  // bounds: 370 ms batched vs 158 ms in sequence).
+  if (nq > 1 && nq <= kSeqQueries && use_grid && !rm->lazy) {
+    for (int32_t k = 0; k < nq; ++k) {
+      mpap_status s = search_batch_device(rm, 1, h_queries + k, lambda, paths + (size_t)k * path_cap, path_cap,
+                                          results + k, trace ? h_waves + (size_t)k * waves_cap : nullptr,
+                                          waves_cap, mem, st);
+      if (s != MPAP_OK) return s;
+    }
+    return MPAP_OK;
+  }
   SlotCaps caps;
   caps.n = rm->n_max;
   caps.K = std::max(64, rm->hint_K);
