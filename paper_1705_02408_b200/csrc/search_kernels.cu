@@ -48,6 +48,7 @@ namespace cg = cooperative_groups;
 constexpr int kST = 512;              // threads per search CTA
 constexpr int kCluster = 8;           // largest CTAs per query in cluster mode (portable cluster size)
 constexpr int kSeqQueries = 8;       // batches up to this size run query by query on the whole grid
+constexpr int kSeqLargeN = 8000;     // ... and so do batches on one environment of at least this many nodes
 constexpr int kMrgCap = 48;           // merge: a node's candidates / staircase staged in shared memory up to this size
 enum : uint8_t { L_OPEN = 0, L_CLOSED = 1, L_DEAD = 2 };
 enum { OVF_LABELS = 1, OVF_CAND = 2, OVF_STAIR = 4 };
@@ -847,8 +848,13 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
   const bool use_cluster = getenv("MPAP_SEARCH_CTA") == nullptr && getenv("MPAP_SEARCH_NO_CLUSTER") == nullptr;
   // A handful of queries (a perception-bound sweep) runs one after the other
   // on the whole grid: 8-CTA clusters would leave most SMs idle (C4 sweep of 6
-  // bounds: 370 ms batched vs 158 ms in sequence).
-  if (nq > 1 && nq <= kSeqQueries && use_grid && !rm->lazy) {
+  // bounds: 370 ms batched vs 158 ms in sequence).  So does any
+  // batch on one large environment (bound sweeps / refinement of a big
+  // roadmap: each query is heavy enough to fill the grid).
+  bool one_large_env = nq > 1;
+  for (int32_t k = 0; k < nq && one_large_env; ++k)
+    one_large_env = h_queries[k].env == h_queries[0].env && rm->n[h_queries[0].env] >= kSeqLargeN;
+  if (nq > 1 && (nq <= kSeqQueries || one_large_env) && use_grid && !rm->lazy) {
     for (int32_t k = 0; k < nq; ++k) {
       mpap_status s = search_batch_device(rm, 1, h_queries + k, lambda, paths + (size_t)k * path_cap, path_cap,
                                           results + k, trace ? h_waves + (size_t)k * waves_cap : nullptr,
