@@ -113,6 +113,10 @@ def lib():
         L.orc_edge_increments.argtypes = [C.POINTER(OrcEnv), C.POINTER(OrcParams), C.c_int, C.c_int,
                                           C.c_double, C.c_double, dp, C.c_int]
         L.orc_edge_increments.restype = C.c_int
+        L.orc_mlp_out0.argtypes = [dp, C.c_double, C.c_double, C.c_double]
+        L.orc_mlp_out0.restype = C.c_double
+        L.orc_di_state.argtypes = [dp, dp, C.c_int, C.c_double, C.c_double, dp, dp]
+        L.orc_di_state.restype = None
         L.orc_fold_summary.argtypes = [dp, C.c_int, dp, dp]
         L.orc_fold_summary.restype = None
         L.orc_fold_stepwise.argtypes = [C.c_double, dp, C.c_int]
@@ -242,6 +246,24 @@ def edge_increments(prob, u: int, v: int, c64: float, tau: float) -> np.ndarray:
     out = np.zeros(max(K, 1))
     lib().orc_edge_increments(C.byref(ctx.env), C.byref(ctx.prm), u, v, c64, tau, _ptr(out, C.c_double), K)
     return out[:K]
+
+
+def mlp_out0(weights, z) -> float:
+    """First output of the 3-8-8-2 ReLU net (R12) at input z (3 values)."""
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    assert w.size == 122
+    return float(lib().orc_mlp_out0(_ptr(w, C.c_double), float(z[0]), float(z[1]), float(z[2])))
+
+
+def di_state(su, sv, d: int, tau: float, t: float):
+    """(position, velocity) at time t on the double-integrator edge cubic (R7 step 6)."""
+    a = np.ascontiguousarray(su, dtype=np.float64)
+    b = np.ascontiguousarray(sv, dtype=np.float64)
+    x = np.zeros(3)
+    v = np.zeros(3)
+    lib().orc_di_state(_ptr(a, C.c_double), _ptr(b, C.c_double), d, float(tau), float(t),
+                       _ptr(x, C.c_double), _ptr(v, C.c_double))
+    return x[:d].copy(), v[:d].copy()
 
 
 def collision(prob, u: int, v: int, tau: float) -> bool:

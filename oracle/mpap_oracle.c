@@ -23,7 +23,12 @@
  * Pins: tests/test_oracle_*.py (closed forms, brute force, Dijkstra in the
  * exact regime, dense-sampling collision, SPEC worked examples; Monte Carlo:
  * double-integrated white-noise variance, exact fixes, Kalman consistency,
- * zero-noise tracking).  Parity unpinned: orc_search at
+ * zero-noise tracking).  tests/test_oracle_pins.py pins mlp_out0 (exact
+ * rational forward pass), the double-integrator branch of orc_collision
+ * (dense sampling of the independently solved cubic's polyline, targeted
+ * boxes), di_traj/di_pos/di_vel (independent linear solve) and the FOV cone
+ * around the interpolated heading (atan2 angles, distinct headings).
+ * Parity unpinned: orc_search at
  * lambda = 0.5 on the C1-C5 roadmaps beyond its invariants, and whole-edge
  * heuristic summaries on the generated environments (pinned only through
  * their primitives).
@@ -237,6 +242,15 @@ static void di_vel(const double *su, const double *c2, const double *c3, int d, 
   for (int j = 0; j < d; ++j) v[j] = fma(t, fma(t, 3.0 * c3[j], 2.0 * c2[j]), v0[j]);
 }
 
+/* Exported for the pins: position and velocity at time t of the edge's cubic
+ * (di_traj + di_pos + di_vel, unchanged). */
+void orc_di_state(const double *su, const double *sv, int d, double tau, double t, double *x, double *v) {
+  double c2[3], c3[3];
+  di_traj(su, sv, d, tau, c2, c3);
+  di_pos(su, c2, c3, d, t, x);
+  di_vel(su, c2, c3, d, t, v);
+}
+
 /* ------------------------------------------------------------------------ */
 /* Collision(u, v) (A2.5 P:215) -- reading R8                         */
 /* ------------------------------------------------------------------------ */
@@ -316,6 +330,9 @@ static double mlp_out0(const double *w, double z0, double z1, double z2) {
   for (int j = 0; j < 8; ++j) o = fma(W3[0 * 8 + j], h2[j], o);
   return o;
 }
+
+/* Exported for the pins (tests/test_oracle_build.py): the same function. */
+double orc_mlp_out0(const double *w, double z0, double z1, double z2) { return mlp_out0(w, z0, z1, z2); }
 
 /* Per-step increments inc_k (k = 0..K-1) of edge u->v; returns K, or the
  * required size if it exceeds cap (then inc is not written past cap). */
