@@ -386,6 +386,15 @@ void mpap_prof_enable(int32_t on);
 void mpap_prof_reset(void);
 int32_t mpap_prof_read(const char *kernel, double *total_ms, int64_t *launches);
 
+/* FP64 issue-rate microbenchmark on the current device (measurement only; the
+ * roofline denominator of the FP64-bound build kernels):
+ * kind 0 = DFMA, 1 = DADD, 2 = DMUL.  Writes the best of 5 timed launches as
+ * instructions per second (one instruction = one op, the convention of
+ * mpap_roadmap_work's counters) and that launch's milliseconds (ms may be
+ * NULL).  INVALID_ARGUMENT for a NULL ops_per_s or an unknown kind; CUDA
+ * errors as MPAP_ERR_CUDA. */
+mpap_status mpap_prof_fp64_peak(int32_t kind, double *ops_per_s, double *ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -46,7 +46,7 @@ EXPORTED_SYMBOLS = [
     "mpap_last_error", "mpap_launch_count", "mpap_prof_enable", "mpap_prof_reset", "mpap_prof_read",
     "mpap_roadmap_work", "mpap_search_ex", "mpap_search_batch_ex", "mpap_roadmap_export_peaks",
     "mpap_roadmap_set_peaks", "mpap_roadmap_update", "mpap_mc_verify", "mpap_mc_verify_batch",
-    "mpap_roadmap_rows_evaluated", "mpap_build_roadmap_rows",
+    "mpap_roadmap_rows_evaluated", "mpap_build_roadmap_rows", "mpap_prof_fp64_peak",
 ]
 
 
@@ -147,6 +147,8 @@ _lib.mpap_prof_enable.restype = None
 _lib.mpap_prof_reset.restype = None
 _lib.mpap_prof_read.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
 _lib.mpap_prof_read.restype = C.c_int32
+_lib.mpap_prof_fp64_peak.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+_lib.mpap_prof_fp64_peak.restype = C.c_int
 for _f in ("mpap_build_roadmap_batch", "mpap_build_roadmap", "mpap_search", "mpap_search_batch",
            "mpap_search_ex", "mpap_search_batch_ex", "mpap_roadmap_export_peaks", "mpap_roadmap_set_peaks",
            "mpap_roadmap_update", "mpap_roadmap_import", "mpap_roadmap_info", "mpap_roadmap_export"):
@@ -488,6 +490,17 @@ def mpap_prof_read(kernel: str) -> tuple:
     n = C.c_int64()
     _lib.mpap_prof_read(kernel.encode(), C.byref(ms), C.byref(n))
     return float(ms.value), int(n.value)
+
+
+def mpap_prof_fp64_peak(kind: str = "dfma") -> tuple:
+    """(ops/s, ms) of the FP64 issue-rate microbenchmark: kind dfma, dadd or dmul."""
+    k = {"dfma": 0, "dadd": 1, "dmul": 2}[kind]
+    ops = C.c_double()
+    ms = C.c_double()
+    s = _lib.mpap_prof_fp64_peak(k, C.byref(ops), C.byref(ms))
+    if s != MPAP_OK:
+        raise MpapError(s, "mpap_prof_fp64_peak")
+    return float(ops.value), float(ms.value)
 
 
 KERNELS = ("k_near", "k_scan", "k_collide", "k_heuristic", "k_fold", "k_search")
