@@ -234,6 +234,25 @@ mpap_status mpap_search_batch_ex(const mpap_roadmap *rm, int32_t n_queries, cons
                                  void *cuda_stream);
 
 /*
+ * mpap_search_batch_trace -- mpap_search_batch_ex that also records the
+ * per-wave counters (SURVEY.md §8(c) counters; the mpap_wave of mpap_search)
+ * of every query, in the same launch configuration as the untraced batch
+ * (one cluster or one CTA per query; whole grid query by query for small
+ * batches), with the counting template of the search kernels.
+ *   waves           host, [n_queries][waves_capacity]; query q's waves k <
+ *                   min(results[q].waves, waves_capacity) are written to
+ *                   waves[q * waves_capacity + k]; the rest is unspecified.
+ *   waves_capacity  >= 0 (0 = mpap_search_batch_ex).
+ * Errors as mpap_search_batch_ex; INVALID_ARGUMENT for waves == NULL with a
+ * positive capacity.  Synchronises before returning when waves_capacity > 0.
+ */
+mpap_status mpap_search_batch_trace(const mpap_roadmap *rm, int32_t n_queries, const int32_t *envs,
+                                    const int32_t *starts, const mpap_goal *goals,
+                                    const double *perception_bounds, double lambda, uint32_t flags,
+                                    int32_t *paths, int32_t path_capacity, mpap_result *results, int32_t mem,
+                                    mpap_wave *waves, int32_t waves_capacity, void *cuda_stream);
+
+/*
  * mpap_roadmap_import -- wrap a precomputed single-environment CSR (P:337:
  * neighbours and edge data "precomputed offline") so mpap_search can run on it.
  *   n, pos_dim      node count (>= 1) and position dimension (2 or 3).
@@ -375,6 +394,12 @@ const char *mpap_last_error(void);
 /* Number of kernel launches issued by this thread's calls so far (bench
  * evidence: "gpu_launches"). */
 int64_t mpap_launch_count(void);
+
+/* Search launches so far (all threads) per team kind -- evidence of which
+ * launch configuration ran: team 0 = the whole grid on one query
+ * (cooperative launch), 1 = one thread-block cluster per query, 2 = one CTA
+ * per query.  Returns -1 for another team value. */
+int64_t mpap_search_launches(int32_t team);
 
 /* Per-kernel CUDA-event timing for measurement (bench.py): when enabled,
  * every kernel launch of this library is bracketed by an event pair recorded

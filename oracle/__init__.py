@@ -87,7 +87,7 @@ WAVE_FIELDS = ["i", "group", "relax", "beta_pass", "inserted", "killed", "touche
 
 
 class OrcWave(C.Structure):
-    _fields_ = [(f, C.c_int64) for f in WAVE_FIELDS]
+    _fields_ = [(f, C.c_int64) for f in WAVE_FIELDS] + [("e_rows", C.c_int64)]
 
 
 def _ptr(a: np.ndarray, ct):
@@ -403,6 +403,10 @@ def search_csr(n: int, row_ptr, dst, coll, w, s, c, goal, start: int, beta: floa
         "cost": np.float32(res.cost), "h": np.float32(res.h), "h_peak": np.float32(res.h_peak),
         "waves": int(res.waves), "relaxations": int(res.relaxations), "labels_inserted": int(res.labels_inserted),
         "wave_counters": wave_arr,
+        # SURVEY §8(d) algorithmic-bytes counters: E_rows (distinct-head row
+        # entries per wave), sum G, F_reads (= stair_sum), L_ins
+        "e_rows": int(sum(waves[k].e_rows for k in range(nw))),
+        "e_rows_per_wave": [int(waves[k].e_rows) for k in range(nw)],
     }
 
 

@@ -597,6 +597,8 @@ typedef struct {      /* per non-empty wave counters (§8(c) counters)    */
   int64_t killed;     /* pre-existing open plans removed (A3.15)          */
   int64_t touched;    /* nodes receiving >= 1 beta-passing candidate      */
   int64_t stair_sum;  /* sum over touched x of |ND(P(x))| before the wave */
+  int64_t e_rows;     /* sum over DISTINCT heads x of G_i of deg_free(x):
+                         the CSR entries the wave must read once (§8(d) E_rows) */
 } orc_wave;
 
 typedef struct { int32_t *a; int64_t n, cap; } ivec;
@@ -701,8 +703,9 @@ int orc_search_ex(int32_t n, const int32_t *row_ptr, const int32_t *dst, const u
   ivec *P = (ivec *)calloc((size_t)n, sizeof(ivec));
   ivec open = {0}, G = {0}, nopen = {0};
   uint8_t *touched = (uint8_t *)calloc((size_t)n, 1);
-  ivec touched_list = {0};
-  if (!P || !touched) { res->status = 5; return 5; }
+  uint8_t *rowseen = (uint8_t *)calloc((size_t)n, 1);
+  ivec touched_list = {0}, heads = {0};
+  if (!P || !touched || !rowseen) { res->status = 5; return 5; }
 
   /* A3.1-A3.4 */
   int32_t root = lab_push(&L, start, -1, 0.0f, 0.0f);
@@ -729,6 +732,17 @@ int orc_search_ex(int32_t n, const int32_t *row_ptr, const int32_t *dst, const u
     wv.group = G.n;
     int nonempty = G.n > 0;
     const int64_t first_new = L.n;   /* labels created this wave: [first_new, L.n) */
+
+    /* §8(d) E_rows: collision-free entries of the distinct heads of G_i */
+    for (int64_t k = 0; k < G.n; ++k) {
+      int32_t u = L.node[G.a[k]];
+      if (rowseen[u]) continue;
+      rowseen[u] = 1;
+      iv_push(&heads, u);
+      for (int32_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) wv.e_rows += !coll[e];
+    }
+    for (int64_t k = 0; k < heads.n; ++k) rowseen[heads.a[k]] = 0;
+    heads.n = 0;
 
     /* A3.6-A3.14: for all p in G, for all x in N(p.head) */
     for (int64_t k = 0; k < G.n; ++k) {
@@ -862,6 +876,7 @@ int orc_search_ex(int32_t n, const int32_t *row_ptr, const int32_t *dst, const u
   free(pa); free(pb);
   for (int32_t x = 0; x < n; ++x) free(P[x].a);
   free(P); free(open.a); free(G.a); free(nopen.a); free(touched); free(touched_list.a);
+  free(rowseen); free(heads.a);
   free(L.node); free(L.parent); free(L.cost); free(L.h); free(L.open); free(L.inP);
   return res->status;
 }

@@ -47,6 +47,7 @@ EXPORTED_SYMBOLS = [
     "mpap_roadmap_work", "mpap_search_ex", "mpap_search_batch_ex", "mpap_roadmap_export_peaks",
     "mpap_roadmap_set_peaks", "mpap_roadmap_update", "mpap_mc_verify", "mpap_mc_verify_batch",
     "mpap_roadmap_rows_evaluated", "mpap_build_roadmap_rows", "mpap_prof_fp64_peak",
+    "mpap_search_batch_trace", "mpap_search_launches",
 ]
 
 
@@ -116,6 +117,9 @@ _lib.mpap_search_ex.argtypes = [_vp, C.c_int32, C.c_int32, C.POINTER(mpap_goal),
                                 _i32p, C.c_int32, C.POINTER(mpap_result), C.POINTER(mpap_wave), C.c_int32, _vp]
 _lib.mpap_search_batch_ex.argtypes = [_vp, C.c_int32, _i32p, _i32p, C.POINTER(mpap_goal), C.POINTER(C.c_double),
                                       C.c_double, C.c_uint32, _vp, C.c_int32, _vp, C.c_int32, _vp]
+_lib.mpap_search_batch_trace.argtypes = [_vp, C.c_int32, _i32p, _i32p, C.POINTER(mpap_goal),
+                                         C.POINTER(C.c_double), C.c_double, C.c_uint32, _vp, C.c_int32, _vp,
+                                         C.c_int32, _vp, C.c_int32, _vp]
 _lib.mpap_mc_verify_batch.argtypes = [_vp, C.c_int32, _vp, _vp, C.c_int32, _vp, C.POINTER(mpap_mc_params),
                                       C.c_uint64, _vp, _vp, _vp, _vp]
 _lib.mpap_mc_verify.argtypes = [_vp, C.c_int32, _vp, C.c_int32, C.POINTER(mpap_mc_params), C.c_uint64, _vp, _vp,
@@ -149,6 +153,8 @@ _lib.mpap_prof_read.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c
 _lib.mpap_prof_read.restype = C.c_int32
 _lib.mpap_prof_fp64_peak.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
 _lib.mpap_prof_fp64_peak.restype = C.c_int
+_lib.mpap_search_launches.argtypes = [C.c_int32]
+_lib.mpap_search_launches.restype = C.c_int64
 for _f in ("mpap_build_roadmap_batch", "mpap_build_roadmap", "mpap_search", "mpap_search_batch",
            "mpap_search_ex", "mpap_search_batch_ex", "mpap_roadmap_export_peaks", "mpap_roadmap_set_peaks",
            "mpap_roadmap_update", "mpap_roadmap_import", "mpap_roadmap_info", "mpap_roadmap_export"):
@@ -373,11 +379,14 @@ def mpap_search(rm: Roadmap, env: int, start: int, goal_lo, goal_hi, perception_
 
 
 def mpap_search_batch(rm: Roadmap, envs, starts, goals_lo, goals_hi, perception_bounds, lam: float,
-                      path_capacity: int, paths=None, results=None, stream=None, forall_t: bool = False):
+                      path_capacity: int, paths=None, results=None, stream=None, forall_t: bool = False,
+                      trace_waves: int = 0):
     """Batch of independent queries (one CTA per query, dynamic scheduling).
     With ``paths``/``results`` CUDA tensors (int32 [Q, cap], uint8 [Q*48]) the
     call is asynchronous and writes on the device; otherwise host numpy outputs
-    are returned."""
+    are returned.  ``trace_waves`` > 0 calls mpap_search_batch_trace and also
+    returns the per-wave counters: (paths, results, [int64 [waves_q, 8] per
+    query])."""
     Q = len(envs)
     ea = np.ascontiguousarray(envs, dtype=np.int32)
     sa = np.ascontiguousarray(starts, dtype=np.int32)
@@ -395,6 +404,18 @@ def mpap_search_batch(rm: Roadmap, envs, starts, goals_lo, goals_hi, perception_
         host_paths = np.zeros((Q, path_capacity), dtype=np.int32)
         host_res = np.zeros(Q, dtype=RESULT_DTYPE)
         pp, rp = C.c_void_p(host_paths.ctypes.data), C.c_void_p(host_res.ctypes.data)
+    if trace_waves > 0:
+        wv = np.zeros((max(Q, 1), trace_waves, 8), dtype=np.int64)
+        s = _lib.mpap_search_batch_trace(rm.handle, Q, ea.ctypes.data_as(_i32p), sa.ctypes.data_as(_i32p), gs,
+                                         ba.ctypes.data_as(C.POINTER(C.c_double)), float(lam),
+                                         MPAP_SEARCH_FORALL_T if forall_t else 0, pp, int(path_capacity), rp, mem,
+                                         C.c_void_p(wv.ctypes.data), int(trace_waves),
+                                         C.c_void_p(st) if st else None)
+        if s != MPAP_OK:
+            raise MpapError(s, "mpap_search_batch_trace")
+        res_h = host_res if host_res is not None else results.cpu().numpy().view(RESULT_DTYPE)
+        counters = [wv[q, : min(int(res_h["waves"][q]), trace_waves)].copy() for q in range(Q)]
+        return host_paths, host_res, counters
     s = _lib.mpap_search_batch_ex(rm.handle, Q, ea.ctypes.data_as(_i32p), sa.ctypes.data_as(_i32p), gs,
                                   ba.ctypes.data_as(C.POINTER(C.c_double)), float(lam),
                                   MPAP_SEARCH_FORALL_T if forall_t else 0, pp, int(path_capacity), rp, mem,
@@ -490,6 +511,14 @@ def mpap_prof_read(kernel: str) -> tuple:
     n = C.c_int64()
     _lib.mpap_prof_read(kernel.encode(), C.byref(ms), C.byref(n))
     return float(ms.value), int(n.value)
+
+
+SEARCH_TEAMS = {"grid": 0, "cluster": 1, "cta": 2}
+
+
+def mpap_search_launches() -> Dict[str, int]:
+    """Search launches so far per team kind (grid / cluster / cta)."""
+    return {k: int(_lib.mpap_search_launches(v)) for k, v in SEARCH_TEAMS.items()}
 
 
 def mpap_prof_fp64_peak(kind: str = "dfma") -> tuple:

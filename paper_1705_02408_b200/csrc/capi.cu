@@ -22,6 +22,9 @@ static std::atomic<long long> g_launches{0};
 
 void note_launch(int k) { g_launches.fetch_add(k); }
 
+static std::atomic<long long> g_team_launches[3];
+void note_team(int team) { g_team_launches[team].fetch_add(1); }
+
 void* workspace(cudaStream_t st, int tag, size_t bytes) {
   struct Key {
     int dev;
@@ -287,6 +290,10 @@ const char* mpap_status_str(mpap_status s) {
 const char* mpap_last_error(void) { return g_last_error.c_str(); }
 
 int64_t mpap_launch_count(void) { return (int64_t)g_launches.load(); }
+
+int64_t mpap_search_launches(int32_t team) {
+  return (team >= 0 && team < 3) ? (int64_t)g_team_launches[team].load() : -1;
+}
 
 void mpap_prof_enable(int32_t on) { g_prof_on.store(on ? 1 : 0); }
 
@@ -826,6 +833,17 @@ mpap_status mpap_search_batch_ex(const mpap_roadmap* rm, int32_t n_queries, cons
                                  const int32_t* starts, const mpap_goal* goals, const double* perception_bounds,
                                  double lambda, uint32_t flags, int32_t* paths, int32_t path_capacity,
                                  mpap_result* results, int32_t mem, void* cuda_stream) {
+  return mpap_search_batch_trace(rm, n_queries, envs, starts, goals, perception_bounds, lambda, flags, paths,
+                                 path_capacity, results, mem, nullptr, 0, cuda_stream);
+}
+
+mpap_status mpap_search_batch_trace(const mpap_roadmap* rm, int32_t n_queries, const int32_t* envs,
+                                    const int32_t* starts, const mpap_goal* goals, const double* perception_bounds,
+                                    double lambda, uint32_t flags, int32_t* paths, int32_t path_capacity,
+                                    mpap_result* results, int32_t mem, mpap_wave* waves, int32_t waves_capacity,
+                                    void* cuda_stream) {
+  if (waves_capacity < 0 || (waves_capacity > 0 && !waves))
+    return set_error(MPAP_ERR_INVALID_ARGUMENT, "waves is NULL or waves_capacity < 0");
   if (!rm || n_queries < 0 || (n_queries > 0 && (!envs || !starts || !goals || !perception_bounds || !paths ||
                                                   !results)) || path_capacity < 1)
     return set_error(MPAP_ERR_INVALID_ARGUMENT, "NULL argument or path_capacity < 1");
@@ -842,7 +860,8 @@ mpap_status mpap_search_batch_ex(const mpap_roadmap* rm, int32_t n_queries, cons
     if (s != MPAP_OK) return s;
     to_desc(qs[k], envs[k], starts[k], &goals[k], perception_bounds[k], flags);
   }
-  return search_batch_device(rm, n_queries, qs.data(), lambda, paths, path_capacity, results, nullptr, 0, mem,
+  return search_batch_device(rm, n_queries, qs.data(), lambda, paths, path_capacity, results,
+                             waves_capacity > 0 ? waves : nullptr, waves_capacity, mem,
                              static_cast<cudaStream_t>(cuda_stream));
 }
 

@@ -100,6 +100,8 @@ struct HostTimer {
 
 // launch bookkeeping shared by the translation units (host side)
 void note_launch(int k = 1);
+// search launches per team kind (mpap_search_launches): 0 grid, 1 cluster, 2 CTA
+void note_team(int team);
 
 // Optional per-kernel CUDA-event timing (mpap_prof_enable): a scope records
 // an event pair on the launching stream around one kernel launch.

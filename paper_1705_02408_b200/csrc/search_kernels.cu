@@ -989,6 +989,7 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
           }
         }
         note_launch();
+        note_team(grid_mode ? 0 : 1);
         int nreq = 0;
         CKS(cudaMemcpyAsync(&nreq, d_nreq, sizeof(int), cudaMemcpyDeviceToHost, st));
         CKS(cudaStreamSynchronize(st));
@@ -1027,6 +1028,7 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
         k_search<false><<<nslots, kST, 0, st>>>(A);
       }
       note_launch();
+      note_team(grid_mode ? 0 : cluster_mode ? 1 : 2);
     }
     CKS(cudaGetLastError());
     CKS(cudaFreeAsync(d_nenv, st));

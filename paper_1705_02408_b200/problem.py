@@ -86,10 +86,13 @@ class Batch:
                                         self.prm, stream=stream)
 
     def search(self, rm: Roadmap, betas: Sequence[float], path_capacity: int = 1024, paths=None, results=None,
-               stream=None):
-        envs = np.arange(len(self.probs), dtype=np.int32)
-        return mpap_search_batch(rm, envs, self.starts, self.goals_lo, self.goals_hi, betas, self.lam,
-                                 path_capacity, paths=paths, results=results, stream=stream)
+               stream=None, envs=None, trace_waves: int = 0):
+        """One query per environment (envs=None) or the given environment
+        index per query; betas per query."""
+        envs = np.arange(len(self.probs), dtype=np.int32) if envs is None else np.asarray(envs, np.int32)
+        return mpap_search_batch(rm, envs, self.starts[envs], [self.goals_lo[e] for e in envs],
+                                 [self.goals_hi[e] for e in envs], betas, self.lam, path_capacity, paths=paths,
+                                 results=results, stream=stream, trace_waves=trace_waves)
 
     def mc_verify(self, rm: Roadmap, paths, results, mc: Dict[str, Any], trial0: int = 0, per_trial: bool = False,
                   stream=None):

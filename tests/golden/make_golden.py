@@ -4,7 +4,11 @@ Calls only oracle/ (and the synth/ input generators); nothing here touches
 the CUDA path.  The GPU parity tests compare libmpap.so against these stored
 oracle outputs, because the full-size oracle build takes minutes of CPU.
 
-    python tests/golden/make_golden.py [c3] [c5] [c4]
+    python tests/golden/make_golden.py [c3] [c5] [c4] [c5_bench]
+
+c5_bench: the bench's rank-0 shard (C5 environments 0..63) at four bounds
+each -- the 64-query batch the bench times (beta = configs/c5.json betas[1])
+and a 256-query batch -- with CSR digests of every environment.
 """
 from __future__ import annotations
 
@@ -21,6 +25,9 @@ sys.path.insert(0, ROOT)
 import oracle  # noqa: E402
 from synth import load_config, make_problem  # noqa: E402
 
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from digest import csr_digests  # noqa: E402
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
@@ -35,7 +42,8 @@ def run_one(prob, betas, procs):
     free = rm["coll"] == 0
     out = {"name": prob.name, "n": int(prob.n), "nnz": int(len(rm["dst"])), "nnz_free": int(free.sum()),
            "w_sum": float(rm["w"].astype(np.float64).sum()), "s_sum": float(rm["s"][free].astype(np.float64).sum()),
-           "c_sum": float(rm["c"][free].astype(np.float64).sum()), "oracle_build_s": tb, "searches": []}
+           "c_sum": float(rm["c"][free].astype(np.float64).sum()), "oracle_build_s": tb,
+           "digests": csr_digests(rm), "searches": []}
     for beta in betas:
         t = time.time()
         r = oracle.search(rm, prob, beta)
@@ -43,7 +51,8 @@ def run_one(prob, betas, procs):
             "beta": beta if np.isfinite(beta) else "inf", "status": r["status"], "path": r["path"].tolist(),
             "cost": f32hex(r["cost"]), "h": f32hex(r["h"]), "h_peak": f32hex(r["h_peak"]), "waves": r["waves"],
             "relaxations": r["relaxations"], "labels_inserted": r["labels_inserted"],
-            "wave_counters": r["wave_counters"].tolist(), "oracle_search_s": time.time() - t,
+            "wave_counters": r["wave_counters"].tolist(), "e_rows": r["e_rows"],
+            "oracle_search_s": time.time() - t,
         })
         print(prob.name, beta, r["status_str"], r["cost"], r["h"], r["waves"], r["relaxations"], flush=True)
     return out
@@ -65,6 +74,15 @@ def main(argv):
             envs.append(run_one(prob, [float(b) if b != "inf" else float("inf") for b in cfg["golden_betas"]],
                                 procs))
         json.dump({"envs": envs}, open(os.path.join(HERE, "c5_full.json"), "w"), indent=1)
+    if "c5_bench" in which:
+        cfg = load_config("c5")
+        betas = [float(cfg["betas"][1]), float("inf"), 2.2, 3.2]
+        envs = []
+        for k in range(int(cfg["queries_per_gpu"])):
+            prob = make_problem(cfg, env_index=k)
+            envs.append(run_one(prob, betas, procs))
+        json.dump({"betas": ["inf" if not np.isfinite(b) else b for b in betas], "envs": envs},
+                  open(os.path.join(HERE, "c5_bench.json"), "w"), indent=None)
     if "c4" in which:
         cfg = load_config("c4")
         prob = make_problem(cfg)

@@ -187,8 +187,11 @@ def test_search_full_size_c3_golden(mp):
 
 
 def test_batch_full_size_c5_golden(mp):
-    """The bench's launch configuration: one batched build of 8 C5
-    environments + one batched search, vs the stored oracle results."""
+    """One batched build of 8 C5 environments + one batched search of 8
+    queries, vs the stored oracle results.  A batch of at most 8 queries runs
+    query by query on the whole grid (search_batch_device); the bench's own
+    64-query cluster launch and the 256-query one-CTA-per-query launch are
+    compared in tests/test_gpu_fullsize.py."""
     cfg = load_config("c5")
     gold = json.load(open(os.path.join(GOLDEN, "c5_full.json")))["envs"]
     probs = [make_problem(cfg, env_index=k) for k in range(len(gold))]

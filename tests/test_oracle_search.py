@@ -265,3 +265,21 @@ def test_c1_exact_regime_beta_monotone(orc, c1):
     dist = dijkstra(M, directed=True, indices=0)
     goal = orc.goal_mask(p).astype(bool)
     assert abs(costs[0] - dist[goal].min()) <= 1e-6 * costs[0]
+
+
+def test_e_rows_counter(orc, c1):
+    """SURVEY §8(d) E_rows = per wave, the collision-free CSR entries of the
+    DISTINCT head nodes of G_i.  Pins: a chain graph (one label per node, so
+    E_rows = relaxations, wave by wave); on C1, E_rows <= relaxations per wave
+    and a wave with #G_i = 1 has E_rows = relax, while waves whose heads carry
+    several labels read each row once (E_rows < relaxations in total)."""
+    g = csr(4, [(0, 1, 1.0, 0.0, 0.0), (1, 2, 1.0, 0.0, 0.0), (2, 3, 1.0, 0.0, 0.0), (1, 3, 5.0, 0.0, 0.0)])
+    r = run(orc, g, [3], INF, 0.5, 1.0)
+    assert r["e_rows_per_wave"] == r["wave_counters"][:, 2].tolist()
+    p, rm = c1
+    res = orc.search(rm, p, 0.3)
+    wc = res["wave_counters"]
+    er = np.asarray(res["e_rows_per_wave"])
+    assert np.all(er <= wc[:, 2]) and er.sum() == res["e_rows"]
+    assert np.all(er[wc[:, 1] == 1] == wc[wc[:, 1] == 1, 2])
+    assert er.sum() < wc[:, 2].sum()      # some heads carry several labels at beta = 0.3
