@@ -16,6 +16,16 @@ resident in HBM; `e2e` = the same through the C ABI with pinned HOST buffers
 (H2D of the inputs and D2H of the results inside the timed region).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mpap|reference]
+                    [--queries-per-gpu Q] [--rowshard] [--launcher-selftest]
+
+--gpus N (N > 1) outside torchrun re-launches this script as N ranks under
+torch.distributed.run (one process per GPU, NCCL, 127.0.0.1 rendezvous);
+rank 0 prints the one JSON line.  Every run ends with a hard parity gate:
+the timed step's results (and, outside the timed region, the same batch's
+per-wave counters and CSR digests) are compared with the oracle's stored
+outputs (tests/golden/, written by tests/golden/make_golden.py, oracle only)
+or, for environments no golden covers, with the oracle run live; a mismatch
+prints the line with "parity_gate": {"passed": false, ...} and exits 3.
 """
 from __future__ import annotations
 
@@ -58,7 +68,65 @@ def parse():
     ap.add_argument("--no-mc", action="store_true", help="skip the Monte Carlo verification measurement")
     ap.add_argument("--no-lazy", action="store_true", help="skip the lazy-roadmap variant measurement")
     ap.add_argument("--mc-trials", type=int, default=1000)
+    ap.add_argument("--rowshard", action="store_true",
+                    help="time the row-sharded build of one large roadmap (default config c4) instead")
+    ap.add_argument("--launcher-selftest", action="store_true",
+                    help="CPU/gloo check of the rank launcher and the result gather (no GPU work)")
+    ap.add_argument("--no-gate", action="store_true", help="diagnostics only: skip the parity gate")
     return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# rank launcher: --gpus N outside torchrun -> N processes under torchrun
+# ---------------------------------------------------------------------------
+def spawn_ranks(n: int) -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # stderr: shows the NVLink/NVLS transport NCCL picked
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def launcher_selftest(args) -> int:
+    """Ranks started by spawn_ranks (or torchrun) on CPU with gloo: every rank
+    writes its shard's fixed-size result records, the records are gathered with
+    the bench's collective (dist.gather_results) and the step time is reduced
+    MAX over ranks, exactly as in the GPU bench; rank 0 prints one line."""
+    import torch
+    import torch.distributed as dist
+    from paper_1705_02408_b200.dist import shard_envs
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    Q = args.queries_per_gpu or 4
+    envs = shard_envs(rank, world, Q)
+    rec = np.zeros(Q, dtype=np.dtype([("env", np.int64), ("rank", np.int64), ("pad", np.int64, 4)]))
+    rec["env"] = envs
+    rec["rank"] = rank
+    local = torch.from_numpy(rec.view(np.uint8).copy())
+    if world > 1:
+        from paper_1705_02408_b200.dist import gather_results
+        allrec = gather_results(local, world).numpy().view(rec.dtype)
+        t = torch.tensor([1.0 + rank], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    else:
+        allrec, t_max = rec, 1.0
+    ok = allrec["env"].tolist() == list(range(world * Q)) and allrec["rank"].tolist() == \
+        [r for r in range(world) for _ in range(Q)]
+    if rank == 0:
+        print(json.dumps({"launcher_selftest": True, "n_gpus": world, "gathered_queries": int(allrec.size),
+                          "records_in_rank_order": bool(ok), "max_over_ranks": t_max}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0 if ok else 3
 
 
 # ---------------------------------------------------------------------------
@@ -206,11 +274,19 @@ def run_reference(args, cfg, beta):
 
 def main():
     args = parse()
+    if args.impl == "mpap" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
+    if args.launcher_selftest:
+        return launcher_selftest(args)
     from synth import load_config
+    if args.rowshard and args.config == "c5":
+        args.config = "c4"
     cfg = load_config(args.config)
     beta = args.beta if not math.isnan(args.beta) else float(cfg["betas"][1])
     if args.impl == "reference":
         return run_reference(args, cfg, beta)
+    if args.rowshard:
+        return run_rowshard(args, cfg, beta)
 
     import torch
     import torch.distributed as dist
@@ -342,14 +418,30 @@ def main():
 
     # ---- roofline of the dominant kernel ----
     peaks, peak_src = load_peaks()
+    fp64 = measure_fp64_peak(mp)
     dom = max(mp.KERNELS, key=lambda k: kern[k][0])
     dom_ms, dom_n = kern[dom]
-    roof = roofline(dom, dom_ms, dom_n, last_work, B, res, peaks, peak_src)
+    roof = roofline(dom, dom_ms, dom_n, last_work, B, res, peaks, peak_src, fp64)
     roof["share_of_step"] = dom_ms / tot_ms if tot_ms > 0 else None
     roof["traffic"] = committed_traffic(dom, Q)
+
+    # ---- parity gate (hard): timed results, per-wave counters, CSR digests ----
+    gate = {"passed": True, "skipped": True}
+    gold = golden_index(cfg, beta)
+    if not args.no_gate:
+        gate = parity_gate(mp, B, probs, rank, world, Q, cfg, beta, gold, res, paths_h, s_d, o_d, f_d, PATH_CAP,
+                           args)
+        g = torch.tensor([1.0 if gate["passed"] else 0.0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(g, op=dist.ReduceOp.MIN)
+        gate["passed_all_ranks"] = bool(g.item() == 1.0)
+
     # the metric's "HBM roofline fraction" for the search itself (k_search):
-    # 16 B edge record per relaxation + 16 B label per inserted plan
-    search_roof = roofline("k_search", kern["k_search"][0], kern["k_search"][1], last_work, B, res, peaks, peak_src)
+    # SURVEY §8(d) algorithmic bytes 16 E_rows + 12 sum G + 8 F_reads + 16 L_ins
+    # (oracle counters, stored with the goldens), and the simpler 16 B per
+    # relaxation + 16 B per inserted label beside it
+    search_roof = roofline("k_search", kern["k_search"][0], kern["k_search"][1], last_work, B, res, peaks, peak_src,
+                           fp64, alg_bytes=search_alg_bytes(gold, rank, Q))
     search_roof["traffic"] = committed_traffic("k_search", Q)
 
     line = {
@@ -370,9 +462,11 @@ def main():
                         "queries_per_s": Q / (search_ms / max(kern['k_search'][1], 1) / 1e3) if search_ms else None},
         "kernels_ms_per_step": {k: kern[k][0] / args.steps for k in mp.KERNELS},
         "feasible_fraction": feasible_all / (world * Q), "all_status_ok": ok,
-        "roofline": roof, "gpu_launches": int(launches), "clocks": clocks, "wall_s": wall,
-        "step_ms": [round(x, 3) for x in step_ms],
+        "roofline": roof, "fp64_peak_measured": fp64, "gpu_launches": int(launches), "clocks": clocks,
+        "wall_s": wall, "step_ms": [round(x, 3) for x in step_ms],
         "step_host_ms": [round(x, 3) for x in host_ms],
+        "search_teams": mp.mpap_search_launches(),
+        "parity_gate": gate,
     }
     if e2e:
         line["e2e"] = e2e
@@ -389,7 +483,249 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
-    return 0
+    return 0 if gate.get("passed_all_ranks", gate["passed"]) else 3
+
+
+# ---------------------------------------------------------------------------
+# parity gate
+# ---------------------------------------------------------------------------
+GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
+
+
+def golden_index(cfg, beta):
+    """{global env index: oracle record of the search at `beta`} from the
+    stored goldens (c5_bench.json: envs 0..63 at four bounds; c5_all.json:
+    every C5 environment at the bench bound), plus the environments' CSR
+    digests.  Empty for other configs or bounds."""
+    out = {}
+    if cfg["name"] != "c5":
+        return out
+    for fn in ("c5_all.json", "c5_bench.json"):
+        path = os.path.join(GOLDEN_DIR, fn)
+        if not os.path.exists(path):
+            continue
+        g = json.load(open(path))
+        for env in g["envs"]:
+            k = int(env["name"].split("[")[1].rstrip("]"))
+            for srch in env["searches"]:
+                b = float("inf") if srch["beta"] == "inf" else float(srch["beta"])
+                if b == beta:
+                    out[k] = {"search": srch, "digests": env.get("digests"), "nnz": env["nnz"]}
+    return out
+
+
+def _f32hex(x):
+    return np.float32(x).tobytes().hex()
+
+
+def _same(rec, path, s, counters=None):
+    if int(rec["status"]) != s["status"] or int(rec["waves"]) != s["waves"]:
+        return False
+    if int(rec["relaxations"]) != s["relaxations"] or int(rec["labels_inserted"]) != s["labels_inserted"]:
+        return False
+    if s["status"] == 0:
+        if path.tolist() != s["path"] or _f32hex(rec["cost"]) != s["cost"] or _f32hex(rec["h"]) != s["h"]:
+            return False
+        if _f32hex(rec["h_peak"]) != s["h_peak"]:
+            return False
+    if counters is not None and counters.tolist() != s["wave_counters"]:
+        return False
+    return True
+
+
+def parity_gate(mp, B, probs, rank, world, Q, cfg, beta, gold, res, paths_h, s_d, o_d, f_d, path_cap, args):
+    """Bit-exact comparison of this rank's timed-step results with the oracle
+    (SURVEY §8(d) "parity gates in every benchmark run"): every environment of
+    the shard a golden covers (status, waves, relaxations, inserted labels,
+    plan, cost / h / h_peak bits); outside the timed region the same batch is
+    rebuilt and searched once more with per-wave counters in the same launch
+    configuration (mpap_search_batch_trace) and the CSR digests of up to 8
+    covered environments are checked.  A shard no golden covers is checked
+    against the oracle run live on its first environment."""
+    sys.path.insert(0, GOLDEN_DIR)
+    from digest import csr_digests
+    envs = [rank * Q + k for k in range(Q)]
+    covered = [k for k in range(Q) if envs[k] in gold]
+    out = {"passed": True, "source": "golden" if covered else "oracle (live)", "envs_checked": 0,
+           "wave_counters_checked": 0, "digests_checked": 0, "mismatches": []}
+    rm = B.build(s_d, o_d, f_d)
+    try:
+        _, tres, tw = B.search(rm, [beta] * Q, path_capacity=path_cap, trace_waves=512)
+        if covered:
+            for k in covered:
+                s = gold[envs[k]]["search"]
+                pl = int(res[k]["path_len"]) if res[k]["status"] == 0 else 0
+                if not _same(res[k], paths_h[k][:pl], s):
+                    out["mismatches"].append(f"env {envs[k]}: timed result")
+                if not _same(tres[k], paths_h[k][:pl], s, counters=tw[k]):
+                    out["mismatches"].append(f"env {envs[k]}: traced result / wave counters")
+                out["envs_checked"] += 1
+                out["wave_counters_checked"] += 1
+            for k in covered[:: max(1, len(covered) // 8)][:8]:
+                if csr_digests(mp.mpap_roadmap_export(rm, k)) != gold[envs[k]]["digests"]:
+                    out["mismatches"].append(f"env {envs[k]}: CSR digest")
+                out["digests_checked"] += 1
+        else:
+            import oracle
+            oracle.build()
+            procs = max(1, (args.cpu_procs or os.cpu_count() or 1) // max(world, 1))
+            orm = oracle.build_roadmap_parallel(probs[0], procs)
+            o = oracle.search(orm, probs[0], beta)
+            s = {"status": o["status"], "waves": o["waves"], "relaxations": o["relaxations"],
+                 "labels_inserted": o["labels_inserted"], "path": o["path"].tolist(), "cost": _f32hex(o["cost"]),
+                 "h": _f32hex(o["h"]), "h_peak": _f32hex(o["h_peak"]), "wave_counters": o["wave_counters"].tolist()}
+            pl = int(res[0]["path_len"]) if res[0]["status"] == 0 else 0
+            if not _same(res[0], paths_h[0][:pl], s) or not _same(tres[0], paths_h[0][:pl], s, counters=tw[0]):
+                out["mismatches"].append(f"env {envs[0]}: result vs live oracle")
+            g = mp.mpap_roadmap_export(rm, 0)
+            if csr_digests(g) != csr_digests(orm):
+                out["mismatches"].append(f"env {envs[0]}: CSR vs live oracle")
+            out.update(envs_checked=1, wave_counters_checked=1, digests_checked=1)
+    finally:
+        rm.free()
+    out["passed"] = not out["mismatches"]
+    out["mismatches"] = out["mismatches"][:10]
+    return out
+
+
+def search_alg_bytes(gold, rank, Q):
+    """SURVEY §8(d) algorithmic bytes of this rank's timed search, summed
+    over its queries from the oracle's counters: 16 E_rows + 12 sum_i |G_i| +
+    8 F_reads (clean staircase entries read) + 16 L_ins.  None unless every
+    query of the shard has a golden record carrying E_rows."""
+    tot = {"e_rows": 0, "sum_g": 0, "f_reads": 0, "l_ins": 0}
+    for k in range(Q):
+        g = gold.get(rank * Q + k)
+        if g is None or "e_rows" not in g["search"]:
+            return None
+        s = g["search"]
+        wc = np.asarray(s["wave_counters"], dtype=np.int64).reshape(-1, 8)
+        tot["e_rows"] += int(s["e_rows"])
+        tot["sum_g"] += int(wc[:, 1].sum())
+        tot["f_reads"] += int(wc[:, 7].sum())
+        tot["l_ins"] += int(s["labels_inserted"])
+    tot["bytes"] = 16 * tot["e_rows"] + 12 * tot["sum_g"] + 8 * tot["f_reads"] + 16 * tot["l_ins"]
+    return tot
+
+
+def measure_fp64_peak(mp):
+    """FP64 issue peak measured on this GPU (mpap_prof_fp64_peak: DFMA, DADD
+    streams; one instruction = one counted op), in T ops/s."""
+    out = {}
+    for kind in ("dfma", "dadd"):
+        ops, ms = mp.mpap_prof_fp64_peak(kind)
+        out[kind + "_tops"] = ops / 1e12
+    out["tops"] = max(out["dfma_tops"], out["dadd_tops"])
+    return out
+
+
+def run_rowshard(args, cfg, beta):
+    """SURVEY §8(e) row-sharded precompute of ONE large roadmap (C4, n =
+    16 001): rank g builds rows [g n/G, (g+1) n/G) (mpap_build_roadmap_rows),
+    the CSR blocks are all-gathered once (dist.gather_csr_blocks) and
+    concatenated in row order, every rank wraps the full CSR
+    (mpap_roadmap_import) and runs the query.  Step = build block + gather +
+    assemble + import + search; value = queries/s of the whole job (max over
+    ranks).  Gate: the assembled CSR's digests and the search equal the
+    oracle's stored C4 outputs."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import build_ext
+    if rank == 0 or world == 1:
+        build_ext.build()
+    if world > 1:
+        dist.barrier()
+    import paper_1705_02408_b200 as mp
+    from paper_1705_02408_b200.dist import assemble_csr, csr_block, gather_csr_blocks, row_block
+    from paper_1705_02408_b200.problem import build_problem_rows, search_problem
+    from synth import make_problem
+    prob = make_problem(cfg)
+    b, e = row_block(rank, world, prob.n)
+    stream = torch.cuda.current_stream()
+    phases = {"build_block": 0.0, "gather_assemble_import": 0.0, "search": 0.0}
+    state = {}
+
+    def step(timed):
+        a = torch.cuda.Event(enable_timing=True)
+        m = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        part = build_problem_rows(prob, b, e)
+        m.record(stream)
+        m.synchronize()
+        t1 = time.perf_counter()
+        block = csr_block(mp.mpap_roadmap_export(part), b, e)
+        part.free()
+        full = assemble_csr(gather_csr_blocks(block, world), prob.n)
+        rm = mp.mpap_roadmap_import(prob.samples[:, : prob.pos_dim], full["row_ptr"], full["dst_coll"], full["w"],
+                                    full["s"], full["c"], prob.r)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        res = search_problem(rm, prob, beta, path_capacity=4096)
+        t3 = time.perf_counter()
+        if timed:
+            phases["build_block"] += a.elapsed_time(m)
+            phases["gather_assemble_import"] += (t2 - t1) * 1e3
+            phases["search"] += (t3 - t2) * 1e3
+        state["full"], state["res"] = full, res
+        rm.free()
+
+    for _ in range(args.warmup):
+        step(False)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(True)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3
+    t = torch.tensor([ms] + [phases[k] for k in phases], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t[0].item())
+    # gate vs the oracle's stored C4 roadmap and search
+    sys.path.insert(0, GOLDEN_DIR)
+    from digest import csr_digests
+    full, res = state["full"], state["res"]
+    gate = {"passed": True, "skipped": True}
+    gpath = os.path.join(GOLDEN_DIR, f"{cfg['name']}_full.json")
+    if os.path.exists(gpath):
+        gold = json.load(open(gpath))
+        dc = full["dst_coll"]
+        dig = csr_digests({"row_ptr": full["row_ptr"], "dst": dc & np.uint32(0x7fffffff), "coll": dc >> np.uint32(31),
+                           "w": full["w"], "s": full["s"], "c": full["c"]})
+        srch = [x for x in gold["searches"] if x["beta"] != "inf" and float(x["beta"]) == beta]
+        ok = dig == gold.get("digests")
+        if srch:
+            x = srch[0]
+            ok = ok and res["status"] == x["status"] and res["relaxations"] == x["relaxations"] and \
+                (x["status"] != 0 or (res["path"].tolist() == x["path"] and _f32hex(res["cost"]) == x["cost"]
+                                      and _f32hex(res["h"]) == x["h"]))
+        gate = {"passed": bool(ok), "digests_equal": dig == gold.get("digests"), "search_checked": bool(srch)}
+    nnz = int(full["row_ptr"][-1])
+    if rank == 0:
+        line = {"metric": METRIC + " (row-sharded single-roadmap build variant)", "value": args.steps / (ms_max / 1e3),
+                "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+                "config": {"workload": f"{cfg['name']}: one roadmap n={prob.n} row-sharded over {world} GPU(s), one "
+                                       f"CSR all-gather, then the single query at beta={beta}",
+                           "rows_per_rank": e - b, "nnz": nnz},
+                "phases_ms_per_step_max_over_ranks": {k: float(t[i + 1].item()) / args.steps
+                                                      for i, k in enumerate(phases)},
+                "edges_built_per_s": nnz * args.steps / (ms_max / 1e3),
+                "parity_gate": gate}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0 if gate["passed"] else 3
 
 
 def measure_lazy(mp, B, s_d, o_d, f_d, betas, path_cap, paths_d, res_d, flush, steps, res_eager, world=1):
@@ -527,25 +863,38 @@ def committed_traffic(kernel: str, Q: int):
     return None
 
 
-def roofline(kernel, ms, launches, work, B, res, peaks, peak_src):
+def roofline(kernel, ms, launches, work, B, res, peaks, peak_src, fp64=None, alg_bytes=None):
     """Achieved vs peak for the dominant kernel: algorithmic work per launch ÷
     its average launch duration (CUDA events on the launching stream)."""
     avg_s = (ms / max(launches, 1)) / 1e3
     if kernel == "k_search":
-        # 16 B edge record per relaxation + 16 B label per inserted plan (DESIGN.md §7)
-        nbytes = 16.0 * float(res["relaxations"].sum()) + 16.0 * float(res["labels_inserted"].sum())
+        simple = 16.0 * float(res["relaxations"].sum()) + 16.0 * float(res["labels_inserted"].sum())
+        nbytes = float(alg_bytes["bytes"]) if alg_bytes else simple
         ach = nbytes / avg_s / 1e9 if avg_s > 0 else 0.0
         peak = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
-        return {"kernel": kernel, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "traffic": None, "peak_source": peak_src}
+        out = {"kernel": kernel, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+               "frac": ach / peak, "traffic": None, "peak_source": peak_src,
+               "bytes_formula": "16 E_rows + 12 sum G + 8 F_reads + 16 L_ins (SURVEY 8(d), oracle counters)"
+               if alg_bytes else "16 B per relaxation + 16 B per inserted label",
+               "bytes_per_launch": nbytes}
+        if alg_bytes:
+            out["counters"] = alg_bytes
+            out["simple_bytes_per_launch"] = simple
+            out["simple_achieved"] = simple / avg_s / 1e9 if avg_s > 0 else 0.0
+        return out
     ops = fp64_ops(kernel, work)
     mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    peak = SMS * FP64_LANES_PER_SM * mhz * 1e6 / 1e12
+    derived = SMS * FP64_LANES_PER_SM * mhz * 1e6 / 1e12
+    peak = fp64["tops"] if fp64 else derived
     ach = ops / avg_s / 1e12 if avg_s > 0 else 0.0
     return {"kernel": kernel, "bound": "alu", "achieved": ach, "peak": peak,
-            "unit": "TFLOP/s (fp64 ops, non-FMA issue peak)", "frac": ach / peak if peak else None, "traffic": None,
-            "peak_source": f"derived: {SMS} SMs x {FP64_LANES_PER_SM} FP64 lanes x {mhz:.0f} MHz ({peak_src} clock)",
-            "work": {k: int(v) for k, v in work.items()}}
+            "unit": "T fp64 ops/s (one DFMA/DADD/DMUL instruction = one op)", "frac": ach / peak if peak else None,
+            "traffic": None,
+            "peak_source": "measured: FP64 issue-rate microbenchmark on this GPU (mpap_prof_fp64_peak, best of DFMA "
+                           "and DADD streams)" if fp64 else f"derived ({peak_src} clock)",
+            "peak_derived": derived,
+            "peak_derived_source": f"{SMS} SMs x {FP64_LANES_PER_SM} FP64 lanes x {mhz:.0f} MHz",
+            "ops_per_launch": ops, "work": {k: int(v) for k, v in work.items()}}
 
 
 if __name__ == "__main__":

@@ -115,7 +115,10 @@ typedef struct mpap_roadmap mpap_roadmap;
  *   out             receives the roadmap handle; free with mpap_roadmap_free.
  * Errors: INVALID_ARGUMENT (null pointers, n < 1, pos_dim not 2/3, row_stride
  * too small, lo >= hi in a box, non-finite samples, r <= 0, params out of
- * range), OUT_OF_MEMORY, CUDA.  Synchronises `cuda_stream` before returning.
+ * range, an environment with more than 65535 features or whose features and
+ * boxes exceed the edge kernels' per-warp shared-memory working set:
+ * 32 (F (d + 1) + 2 d O) + 8192 bytes <= 227 KB, e.g. F <= 1600 at O = 200,
+ * d = 3), OUT_OF_MEMORY, CUDA.  Synchronises `cuda_stream` before returning.
  */
 mpap_status mpap_build_roadmap_batch(int32_t n_envs, const double *samples, const int32_t *n,
                                      int32_t row_stride, const double *obstacles,
@@ -199,6 +202,11 @@ mpap_status mpap_search(const mpap_roadmap *rm, int32_t env, int32_t start, cons
  *                   MPAP_MEM_DEVICE: asynchronous; outputs are written on the
  *                   device in stream order; the caller synchronises.
  * Returns OK if the batch executed; each query's outcome is results[q].status.
+ * Row q of `paths` is defined for its first results[q].path_len entries (when
+ * results[q].status is OK); entries past path_len are unspecified.  If a
+ * query cannot run (OUT_OF_MEMORY at the capacity regrow limit, a CUDA
+ * error), every other query's record is still written and the first such
+ * status is returned.
  */
 mpap_status mpap_search_batch(const mpap_roadmap *rm, int32_t n_queries, const int32_t *envs,
                               const int32_t *starts, const mpap_goal *goals,
@@ -301,7 +309,8 @@ mpap_status mpap_roadmap_export(const mpap_roadmap *rm, int32_t env, int32_t *ro
  *                   (validated as in the build).
  *   n_reevaluated   out (may be NULL): number of edges re-evaluated.
  * Synchronises the device.  Errors: INVALID_ARGUMENT (bad env, arrays, an
- * imported roadmap), OUT_OF_MEMORY, CUDA.
+ * imported roadmap, the size limits of mpap_build_roadmap_batch), OUT_OF_MEMORY,
+ * CUDA.
  */
 mpap_status mpap_roadmap_update(mpap_roadmap *rm, int32_t env, const double *obstacles, int32_t n_obstacles,
                                 const double *features, int32_t n_features, int32_t mem, void *cuda_stream,

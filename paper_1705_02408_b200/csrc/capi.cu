@@ -272,6 +272,22 @@ static mpap_status validate_params(const mpap_params* p, double r) {
   return MPAP_OK;
 }
 
+// Per-environment size limits of the edge kernels: the per-step visible
+// counts are uint16 (k_heuristic -> k_fold), and each warp stages the
+// environment's features (D + 1 doubles each) and boxes (2D doubles) in shared
+// memory (kEdgeWarps warps per block, <= 227 KB per block with the static
+// arrays).  Larger environments are rejected, never wrapped or truncated.
+static mpap_status check_env_sizes(int d, int64_t n_obstacles, int64_t n_features) {
+  constexpr int64_t kEdgeWarps = 4, kStaticBytes = 8 * 1024, kSmemMax = 227 * 1024;
+  if (n_features > 65535) return set_error(MPAP_ERR_INVALID_ARGUMENT, "more than 65535 features in one environment");
+  const int64_t bytes = 8 * kEdgeWarps * (n_features * (d + 1) + n_obstacles * 2 * d) + kStaticBytes;
+  if (bytes > kSmemMax)
+    return set_error(MPAP_ERR_INVALID_ARGUMENT,
+                     "environment too large for the edge kernels' shared-memory working set "
+                     "(32 (F (d + 1) + 2 d O) bytes + 8 KB must fit in 227 KB)");
+  return MPAP_OK;
+}
+
 extern "C" {
 
 const char* mpap_status_str(mpap_status s) {
@@ -374,6 +390,8 @@ static mpap_status build_batch_impl(int32_t n_envs, const double* samples, const
   for (int b = 0; b < n_envs; ++b) {
     if (n[b] < 1) return set_error(MPAP_ERR_INVALID_ARGUMENT, "n < 1");
     if (n_obstacles[b] < 0 || n_features[b] < 0) return set_error(MPAP_ERR_INVALID_ARGUMENT, "negative count");
+    mpap_status se = check_env_sizes(params->pos_dim, n_obstacles[b], n_features[b]);
+    if (se != MPAP_OK) return se;
     N += n[b];
     O += n_obstacles[b];
     F += n_features[b];
@@ -645,6 +663,10 @@ mpap_status mpap_roadmap_update(mpap_roadmap* rm, int32_t env, const double* obs
   if (mem != MPAP_MEM_HOST && mem != MPAP_MEM_DEVICE) return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad mem space");
   if (n_obstacles < 0 || n_features < 0 || (n_obstacles > 0 && !obstacles) || (n_features > 0 && !features))
     return set_error(MPAP_ERR_INVALID_ARGUMENT, "bad obstacle/feature arrays");
+  {
+    mpap_status se = check_env_sizes(rm->prm.pos_dim, n_obstacles, n_features);
+    if (se != MPAP_OK) return se;
+  }
   int cur = 0;
   cudaGetDevice(&cur);
   if (cur != rm->device) return set_error(MPAP_ERR_INVALID_ARGUMENT, "roadmap bound to another device");

@@ -49,6 +49,9 @@ constexpr int kST = 512;              // threads per search CTA
 constexpr int kCluster = 8;           // largest CTAs per query in cluster mode (portable cluster size)
 constexpr int kSeqQueries = 8;       // batches up to this size run query by query on the whole grid
 constexpr int kSeqLargeN = 8000;     // ... and so do batches on one environment of at least this many nodes
+constexpr int kSeqLargeMaxQ = 32;    //     of at most this many queries (C4 refinement rounds of 32 bounds,
+                                     //     measured; larger batches fill the SMs with clusters / CTAs)
+constexpr int kMaxTies = 32;           // (cost, h) ties listed for the R16 tie-break; more -> leader scan
 constexpr int kMrgCap = 48;           // merge: a node's candidates / staircase staged in shared memory up to this size
 enum : uint8_t { L_OPEN = 0, L_CLOSED = 1, L_DEAD = 2 };
 enum { OVF_LABELS = 1, OVF_CAND = 2, OVF_STAIR = 4 };
@@ -118,7 +121,7 @@ struct Ctl {
   int need;               // lazy: some head of G_i has an unevaluated row
   unsigned long long best_key;
   int nties;
-  int ties[32];
+  int ties[kMaxTies];
 };
 
 // A team runs one query: a CTA (batched queries, __syncthreads) or the whole
@@ -688,7 +691,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
       const unsigned long long key = ((unsigned long long)__float_as_uint(ch.x) << 32) | __float_as_uint(ch.y);
       if (key == best_key) {
         const int slot_t = atomicAdd(&S->nties, 1);
-        if (slot_t < 32) S->ties[slot_t] = si[j];
+        if (slot_t < kMaxTies) S->ties[slot_t] = si[j];
       }
     }
   }
@@ -696,10 +699,10 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
   if (leader) {
     // lexicographic tie-break on node sequences (R16); chains reversed into
     // the (now unused) G / pend2 arrays
-    int best = vld(S->ties[0]);
-    const int nties = min(vld(S->nties), 32);
-    for (int k = 1; k < nties; ++k) {
-      const int cand_id = vld(S->ties[k]);
+    const int nties = vld(S->nties);
+    int best = -1;
+    auto consider = [&](int cand_id) {
+      if (best < 0) { best = cand_id; return; }
       int la = 0, lb = 0;
       for (int x = cand_id; x >= 0; x = labels[x].y) G[la++] = labels[x].x;
       for (int x = best; x >= 0; x = labels[x].y) pend2[lb++] = labels[x].x;
@@ -710,6 +713,24 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
       }
       if (!decided) less = la < lb;
       if (less) best = cand_id;
+    };
+    if (nties <= kMaxTies) {
+      for (int k = 0; k < nties; ++k) consider(vld(S->ties[k]));
+    } else {
+      // more (cost, h) ties than the shared list holds (rare): the leader
+      // scans every goal node's staircase itself -- all ties are compared
+      for (int x = 0; x < n; ++x) {
+        if (!goal[x]) continue;
+        const int snx = sn[x];
+        const int m = snx & kStairCountMask;
+        const float2* st = sch + stair_base(snx, x, n, C.K);
+        const int32_t* si = sid + stair_base(snx, x, n, C.K);
+        for (int j = 0; j < m; ++j) {
+          const float2 ch = st[j];
+          const unsigned long long key = ((unsigned long long)__float_as_uint(ch.x) << 32) | __float_as_uint(ch.y);
+          if (key == best_key) consider(si[j]);
+        }
+      }
     }
     int len = 0;
     float hp = 0.0f;
@@ -851,17 +872,20 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
   // bounds: 370 ms batched vs 158 ms in sequence).  So does any
   // batch on one large environment (bound sweeps / refinement of a big
   // roadmap: each query is heavy enough to fill the grid).
-  bool one_large_env = nq > 1;
+  bool one_large_env = nq > 1 && nq <= kSeqLargeMaxQ;
   for (int32_t k = 0; k < nq && one_large_env; ++k)
     one_large_env = h_queries[k].env == h_queries[0].env && rm->n[h_queries[0].env] >= kSeqLargeN;
   if (nq > 1 && (nq <= kSeqQueries || one_large_env) && use_grid && !rm->lazy) {
+    // every query runs and writes its record; the first failing status is
+    // returned after all of them (as the batched path does)
+    mpap_status first = MPAP_OK;
     for (int32_t k = 0; k < nq; ++k) {
       mpap_status s = search_batch_device(rm, 1, h_queries + k, lambda, paths + (size_t)k * path_cap, path_cap,
                                           results + k, trace ? h_waves + (size_t)k * waves_cap : nullptr,
                                           waves_cap, mem, st);
-      if (s != MPAP_OK) return s;
+      if (s != MPAP_OK && first == MPAP_OK) first = s;
     }
-    return MPAP_OK;
+    return first;
   }
   SlotCaps caps;
   caps.n = rm->n_max;
@@ -1055,6 +1079,10 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     todo.swap(again);
   }
   if (status == MPAP_OK && !todo.empty()) status = set_error(MPAP_ERR_OUT_OF_MEMORY, "search capacity regrow limit");
+  for (int k : todo) {   // queries that could not complete carry the error, never a stale record
+    hres[k] = mpap_result{};
+    hres[k].status = status;
+  }
   // write retry counts into the results
   for (int k = 0; k < nq; ++k) hres[k].retries = retries[k];
   if (mem == MPAP_MEM_DEVICE) {

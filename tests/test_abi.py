@@ -23,7 +23,7 @@ def mp():
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "mpap.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(mpap_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(mpap_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_declares_the_north_star_calls():
@@ -144,3 +144,22 @@ def test_struct_layouts_match_header(mp, tmp_path):
             cls = structs[name]
             want = C.sizeof(cls) if field == "size" else getattr(cls, field).offset
         assert int(val) == want, (name, field, val, want)
+
+
+@pytest.mark.parametrize("nfeat,nobst", [(65536, 0), (3000, 0), (1000, 1200)])
+def test_build_rejects_oversized_environment(mp, nfeat, nobst):
+    """Per-environment limits (uint16 visible counts; the edge kernels' shared
+    working set 32 (F (d + 1) + 2 d O) + 8192 <= 227 KB) are validated before
+    any device work -- never wrapped or truncated."""
+    samples = np.array([[0.1, 0.1], [0.5, 0.5]])
+    feats = np.full((nfeat, 2), 0.9)
+    obst = np.tile(np.array([[0.3, 0.3, 0.4, 0.4]]), (max(nobst, 1), 1))
+    prm = _params(mp)
+    lib = mp.lib()
+    out = C.c_void_p()
+    n, no, nf = C.c_int32(2), C.c_int32(nobst), C.c_int32(nfeat)
+    s = lib.mpap_build_roadmap_batch(1, samples.ctypes.data, C.byref(n), 2, obst.ctypes.data, C.byref(no),
+                                     feats.ctypes.data, C.byref(nf), 0.5, C.byref(prm), 0, None, C.byref(out))
+    assert s == mp.MPAP_ERR_INVALID_ARGUMENT
+    assert out.value is None
+    assert b"feature" in lib.mpap_last_error() or b"shared" in lib.mpap_last_error()

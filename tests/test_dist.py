@@ -174,3 +174,24 @@ def test_shards_disjoint_and_cover():
             parts = [md.mc_trial_shard(r, world, trials) for r in range(world)]
             assert sum(n for _, n in parts) == trials
             assert all(parts[r][0] + parts[r][1] == parts[r + 1][0] for r in range(world - 1))
+
+
+def test_bench_launcher_spawns_ranks():
+    """bench.py --gpus 2 outside torchrun re-launches itself as 2 ranks
+    (torch.distributed.run, 127.0.0.1 rendezvous); the ranks gather their
+    shards' result records with the bench's collective and reduce the time
+    MAX over ranks; rank 0 alone prints one JSON line (gloo on CPU)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--launcher-selftest",
+                          "--queries-per-gpu", "3"], capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["gathered_queries"] == 6 and d["records_in_rank_order"]
+    assert d["max_over_ranks"] == 2.0

@@ -378,3 +378,21 @@ def test_search_full_size_c4_golden(mp):
     info = mp.mpap_roadmap_info(rm)
     assert info["nnz"] == gold["nnz"] and info["nnz_free"] == gold["nnz_free"]
     _golden_check(mp, rm, prob, gold)
+
+
+def test_many_goal_ties(mp, orc):
+    """More (cost, h) ties at the goal than the 32-entry tie list (R16): 48
+    goal nodes reached at identical cost and h through 2-hop chains; the
+    lexicographically smallest node sequence must win, as in the oracle
+    (which scans every tie).  Ties are reached via intermediate nodes with
+    descending ids so the winner is not the first goal node."""
+    n_goal = 48
+    n = 1 + 2 * n_goal
+    edges = []
+    for k in range(n_goal):
+        mid = n_goal - k          # intermediate nodes 1..48 (descending)
+        goalk = n_goal + 1 + k    # goal nodes 49..96
+        edges.append((0, mid, 0.25, 0.0, 0.0))
+        edges.append((mid, goalk, 0.25, 0.0, 0.0))
+    goal = set(range(n_goal + 1, n))
+    _import_and_compare(mp, orc, n, edges, goal, [INF, 1.0], [0.5, 1.0])
