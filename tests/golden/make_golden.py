@@ -4,7 +4,7 @@ Calls only oracle/ (and the synth/ input generators); nothing here touches
 the CUDA path.  The GPU parity tests compare libmpap.so against these stored
 oracle outputs, because the full-size oracle build takes minutes of CPU.
 
-    python tests/golden/make_golden.py [c3] [c5] [c4] [c5_bench]
+    python tests/golden/make_golden.py [c3] [c5] [c4] [c5_bench] [c5_all]
 
 c5_bench: the bench's rank-0 shard (C5 environments 0..63) at four bounds
 each -- the 64-query batch the bench times (beta = configs/c5.json betas[1])
@@ -83,6 +83,28 @@ def main(argv):
             envs.append(run_one(prob, betas, procs))
         json.dump({"betas": ["inf" if not np.isfinite(b) else b for b in betas], "envs": envs},
                   open(os.path.join(HERE, "c5_bench.json"), "w"), indent=None)
+    if "c5_all" in which:
+        # every C5 environment at the bench bound (the parity gate of every
+        # rank of the weak-scaling bench, and of a 512-query single-GPU run);
+        # environments of c5_bench.json are taken from there (same oracle run)
+        cfg = load_config("c5")
+        beta = float(cfg["betas"][1])
+        have = {}
+        bench_path = os.path.join(HERE, "c5_bench.json")
+        if os.path.exists(bench_path):
+            bj = json.load(open(bench_path))
+            k0 = [float("inf") if b == "inf" else float(b) for b in bj["betas"]].index(beta)
+            for env in bj["envs"]:
+                e = dict(env)
+                e["searches"] = [env["searches"][k0]]
+                have[env["name"]] = e
+        envs = []
+        for k in range(int(cfg["n_queries"])):
+            prob = make_problem(cfg, env_index=k)
+            envs.append(have.get(prob.name) or run_one(prob, [beta], procs))
+            if k % 16 == 15:   # checkpoint (the full run takes over an hour on 8 cores)
+                json.dump({"beta": beta, "envs": envs}, open(os.path.join(HERE, "c5_all.json"), "w"))
+        json.dump({"beta": beta, "envs": envs}, open(os.path.join(HERE, "c5_all.json"), "w"))
     if "c4" in which:
         cfg = load_config("c4")
         prob = make_problem(cfg)
