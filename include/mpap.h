@@ -117,8 +117,9 @@ typedef struct mpap_roadmap mpap_roadmap;
  * too small, lo >= hi in a box, non-finite samples, r <= 0, params out of
  * range, an environment with more than 65535 features or whose features and
  * boxes exceed the edge kernels' per-warp shared-memory working set:
- * 32 (F (d + 1) + 2 d O) + 8192 bytes <= 227 KB, e.g. F <= 1600 at O = 200,
- * d = 3), OUT_OF_MEMORY, CUDA.  Synchronises `cuda_stream` before returning.
+ * 16 (F4 (2 d + 7) + 6 d O4) + 8192 bytes <= 227 KB with F4, O4 = F, O rounded
+ * up to a multiple of 4, e.g. F <= 796 at O = 200, d = 3), OUT_OF_MEMORY, CUDA.  Synchronises `cuda_stream` before
+ * returning.
  */
 mpap_status mpap_build_roadmap_batch(int32_t n_envs, const double *samples, const int32_t *n,
                                      int32_t row_stride, const double *obstacles,

@@ -49,6 +49,11 @@ constexpr int kWarps = MPAP_KWARPS;       // warps per block of the edge kernels
 constexpr int kNearWarps = 8;             // warps per block of k_near
 constexpr double kCullMargin = 1e-6;      // absolute; >> rounding of O(100) coordinates
 
+// min / max of finite doubles for the conservative culls (fmin / fmax carry
+// NaN handling: ~10 instructions each on sm_100a; these are 3)
+__device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -417,7 +422,25 @@ struct WarpLists {
   double* box;                  // [O_max][2D]
   unsigned long long* fmask;    // [F_max] per-feature box masks
   const double* mlp;            // [122] block-shared MLP weights
+  float4* fenv;                 // [F_max] the current environment's features (float x, y, z), staged per env
+  float* boxf;                  // [O_max][2D] the chunk's culled boxes (float), for the occluder masks
+  int* fidx;                    // [F_max] the chunk's kept features' indices into fenv
 };
+#ifndef MPAP_CULL_FENV
+#define MPAP_CULL_FENV 1     // feature cull from per-environment float copies staged in shared memory
+#endif
+#ifndef MPAP_FMASK_F32
+#define MPAP_FMASK_F32 0     // occluder masks in single precision, lanes over boxes (measured slower: 177.4 -> 196.3 ms)
+#endif
+// Per-warp shared scratch layout (in doubles; counts fs, os rounded up to a
+// multiple of 4 so every array stays 16-byte aligned):
+//   f[D][fs], box[os][2D], fmask[fs], fenv[fs] float4 (MPAP_CULL_FENV),
+//   boxf[os][2D] float (MPAP_FMASK_F32), fidx[fs] int (both).
+__host__ __device__ constexpr size_t warp_scratch_doubles(int D, size_t fs, size_t os) {
+  return fs * (D + 1) + os * 2 * D + (MPAP_CULL_FENV ? fs * 2 : 0) + (MPAP_FMASK_F32 ? os * D : 0) +
+         ((MPAP_CULL_FENV && MPAP_FMASK_F32) ? fs / 2 : 0);
+}
+__host__ __device__ constexpr size_t round4(int x) { return (size_t)((x + 3) & ~3); }
 
 // Work counters: warp-uniform counts go to the warp's shared-memory slots
 // (written by lane 0 only); per-lane counts live in four registers and are
@@ -442,11 +465,11 @@ struct Work {
 };
 
 __device__ __forceinline__ double warp_min(double x) {
-  for (int o = 16; o > 0; o >>= 1) x = fmin(x, __shfl_xor_sync(FULL, x, o));
+  for (int o = 16; o > 0; o >>= 1) x = dmin(x, __shfl_xor_sync(FULL, x, o));
   return x;
 }
 __device__ __forceinline__ double warp_max(double x) {
-  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(FULL, x, o));
+  for (int o = 16; o > 0; o >>= 1) x = dmax(x, __shfl_xor_sync(FULL, x, o));
   return x;
 }
 
@@ -455,7 +478,7 @@ __device__ __forceinline__ double warp_max(double x) {
 // interval is empty by a margin far above rounding).
 template <int D>
 __device__ int cull_boxes(const double* __restrict__ box, int O, const double* lo, const double* hi, double m,
-                          double* out, int lane) {
+                          double* out, int lane, float* outf = nullptr) {
   int nc = 0;
   const unsigned lt = lanemask_lt();
   __syncwarp();
@@ -473,9 +496,14 @@ __device__ int cull_boxes(const double* __restrict__ box, int O, const double* l
     }
     const unsigned msk = __ballot_sync(FULL, keep);
     if (keep) {
-      double* dst = out + (size_t)(nc + __popc(msk & lt)) * 2 * D;
+      const int pos = nc + __popc(msk & lt);
+      double* dst = out + (size_t)pos * 2 * D;
 #pragma unroll
       for (int k = 0; k < 2 * D; ++k) dst[k] = bl[k];
+      if (outf) {
+#pragma unroll
+        for (int k = 0; k < 2 * D; ++k) outf[(size_t)pos * 2 * D + k] = (float)bl[k];
+      }
     }
     nc += __popc(msk);
   }
@@ -497,8 +525,8 @@ __device__ __forceinline__ unsigned seg_hits_boxes(const double* A, const double
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     inv[k] = (Dv[k] != 0.0) ? __drcp_rn(Dv[k]) : 0.0;   // == 1.0 / Dv[k]
-    slo[k] = fmin(A[k], B[k]) - kCullMargin;
-    shi[k] = fmax(A[k], B[k]) + kCullMargin;
+    slo[k] = dmin(A[k], B[k]) - kCullMargin;
+    shi[k] = dmax(A[k], B[k]) + kCullMargin;
   }
   unsigned tests = 0;
   int i = -1;
@@ -574,7 +602,7 @@ __device__ __forceinline__ bool edge_collision(const DevParams& P, const double*
     di_pos<D>(su, c2, c3, t, x);
     if (outside_ws<D>(x, P)) out = true;
 #pragma unroll
-    for (int j = 0; j < D; ++j) { lo[j] = fmin(lo[j], x[j]); hi[j] = fmax(hi[j], x[j]); }
+    for (int j = 0; j < D; ++j) { lo[j] = dmin(lo[j], x[j]); hi[j] = dmax(hi[j], x[j]); }
   }
   if (__any_sync(FULL, out)) return true;
 #pragma unroll
@@ -722,18 +750,18 @@ __device__ __forceinline__ void chunk_bbox(const double* su, const double* sv, c
   }
 #pragma unroll
   for (int j = 0; j < D; ++j) {
-    lo[j] = fmin(xa[j], xb[j]);
-    hi[j] = fmax(xa[j], xb[j]);
+    lo[j] = dmin(xa[j], xb[j]);
+    hi[j] = dmax(xa[j], xb[j]);
     if (DYN == 1) {
       if (r0[j] > ta && r0[j] < tb) {
         const double x = fma(r0[j], fma(r0[j], fma(r0[j], c3[j], c2[j]), su[D + j]), su[j]);
-        lo[j] = fmin(lo[j], x);
-        hi[j] = fmax(hi[j], x);
+        lo[j] = dmin(lo[j], x);
+        hi[j] = dmax(hi[j], x);
       }
       if (r1[j] > ta && r1[j] < tb) {
         const double x = fma(r1[j], fma(r1[j], fma(r1[j], c3[j], c2[j]), su[D + j]), su[j]);
-        lo[j] = fmin(lo[j], x);
-        hi[j] = fmax(hi[j], x);
+        lo[j] = dmin(lo[j], x);
+        hi[j] = dmax(hi[j], x);
       }
     }
   }
@@ -854,11 +882,14 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
     for (int f0 = 0; f0 < F; f0 += 32) {
       const int f = f0 + lane;
       bool keep = false;
-      double fc[D];
       if (f < F) {
-#pragma unroll
-        for (int q = 0; q < D; ++q) fc[q] = __ldg(feat + (size_t)f * D + q);
-        const float fx = (float)fc[0], fy = (float)fc[1], fz = (D == 3) ? (float)fc[D - 1] : 0.0f;
+#if MPAP_CULL_FENV
+        const float4 fv = L.fenv[f];   // the environment's features, staged as float once per environment
+        const float fx = fv.x, fy = fv.y, fz = fv.z;
+#else
+        const double* fp = feat + (size_t)f * D;
+        const float fx = (float)__ldg(fp), fy = (float)__ldg(fp + 1), fz = (D == 3) ? (float)__ldg(fp + D - 1) : 0.0f;
+#endif
         const float ex = fmaxf(fmaxf(flx - fx, fx - fhx), 0.0f);
         const float ey = fmaxf(fmaxf(fly - fy, fy - fhy), 0.0f);
         const float ez = (D == 3) ? fmaxf(fmaxf(flz - fz, fz - fhz), 0.0f) : 0.0f;
@@ -882,23 +913,28 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
       if (keep) {
         const int pos = nf + __popc(msk & lt);
 #pragma unroll
-        for (int q = 0; q < D; ++q) L.f[q][pos] = fc[q];
+        for (int q = 0; q < D; ++q) L.f[q][pos] = __ldg(feat + (size_t)f * D + q);   // exact coordinates
+        if (MPAP_CULL_FENV && MPAP_FMASK_F32) L.fidx[pos] = f;
       }
       nf += __popc(msk);
     }
-    const int nb = (nf > 0) ? cull_boxes<D>(box, O, lo, hi, m, L.box, lane) : 0;
+    const int nb = (nf > 0) ? cull_boxes<D>(box, O, lo, hi, m, L.box, lane, MPAP_FMASK_F32 ? L.boxf : nullptr) : 0;
     W.add(lane, W_CULL_TESTS, F + (nf > 0 ? O : 0));
     // per kept feature: which of the chunk's boxes meet the box spanned by the
-    // chunk and the feature (every sight line to it lies inside that box)
+    // chunk and the feature (every sight line to it lies inside that box).
+    // Lanes over boxes (lane j: boxes j and j + 32), one ballot per feature;
+    // single precision with a 1e-4 m margin (>> the float rounding of
+    // coordinates below 1e3 m): a superset of the exact overlaps.
     const bool use_mask = nb > 0 && nb <= 64;
+#if !MPAP_FMASK_F32
     if (use_mask) {
       for (int i = lane; i < nf; i += 32) {
         double fl[D], fh[D];
 #pragma unroll
         for (int q = 0; q < D; ++q) {
           const double fq = L.f[q][i];
-          fl[q] = fmin(lo[q], fq) - kCullMargin;
-          fh[q] = fmax(hi[q], fq) + kCullMargin;
+          fl[q] = dmin(lo[q], fq) - kCullMargin;
+          fh[q] = dmax(hi[q], fq) + kCullMargin;
         }
         unsigned long long msk = 0ull;
         for (int bb = 0; bb < nb; ++bb) {
@@ -914,6 +950,39 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
       W.add(lane, W_CULL_TESTS, nf * nb);
       __syncwarp();
     }
+#else
+    if (use_mask) {
+      constexpr float mg = 1e-4f;
+      const bool h0 = lane < nb, h1 = lane + 32 < nb;
+      float b0[2 * D], b1[2 * D];
+#pragma unroll
+      for (int k = 0; k < 2 * D; ++k) {
+        b0[k] = h0 ? L.boxf[(size_t)lane * 2 * D + k] : 0.0f;
+        b1[k] = h1 ? L.boxf[(size_t)(lane + 32) * 2 * D + k] : 0.0f;
+      }
+      const float clo[3] = {flx, fly, flz}, chi[3] = {fhx, fhy, fhz};
+      for (int i = 0; i < nf; ++i) {
+#if MPAP_CULL_FENV
+        const float4 fk = L.fenv[L.fidx[i]];
+#else
+        const float4 fk = make_float4((float)L.f[0][i], (float)L.f[1][i], (D == 3) ? (float)L.f[D - 1][i] : 0.0f, 0.0f);
+#endif
+        const float fq[3] = {fk.x, fk.y, fk.z};
+        bool s0 = !h0, s1 = !h1;
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+          const float fl = fminf(clo[q], fq[q]) - mg;
+          const float fh = fmaxf(chi[q], fq[q]) + mg;
+          s0 |= b0[q] > fh || b0[D + q] < fl;
+          s1 |= b1[q] > fh || b1[D + q] < fl;
+        }
+        const unsigned m0 = __ballot_sync(FULL, !s0), m1 = __ballot_sync(FULL, !s1);
+        if (lane == 0) L.fmask[i] = (unsigned long long)m0 | ((unsigned long long)m1 << 32);
+      }
+      W.add(lane, W_CULL_TESTS, nf * nb);
+      __syncwarp();
+    }
+#endif
     W.add(lane, W_STEPS, nk);
     W.add(lane, W_RANGE_TESTS, nk * nf);
     if (heur != 0) W.add(lane, W_FOV_TESTS, nk * nf);
@@ -1019,7 +1088,7 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
                                                           unsigned long long* __restrict__ work,
                                                           unsigned long long* __restrict__ next_item) {
   constexpr int NS = 2 * D + 2;   // p, v (double integrator), heading
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   __shared__ double s_state[kWarps][2][NS];
   __shared__ unsigned s_work[kWarps][W_NUM];
   __shared__ double s_mlp[kMlpSize];
@@ -1029,13 +1098,21 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpLists<D> L;
   {
-    double* base = smem + (size_t)warp * ((size_t)f_max * (D + 1) + (size_t)o_max * 2 * D);
+    const size_t fs = round4(f_max), os = round4(o_max);
+    double* base = smem + (size_t)warp * warp_scratch_doubles(D, fs, os);
 #pragma unroll
-    for (int q = 0; q < D; ++q) L.f[q] = base + (size_t)q * f_max;
-    L.box = base + (size_t)D * f_max;
-    L.fmask = reinterpret_cast<unsigned long long*>(L.box + (size_t)o_max * 2 * D);
+    for (int q = 0; q < D; ++q) L.f[q] = base + (size_t)q * fs;
+    L.box = base + (size_t)D * fs;
+    L.fmask = reinterpret_cast<unsigned long long*>(L.box + os * 2 * D);
+    double* nxt = reinterpret_cast<double*>(L.fmask + fs);
+    L.fenv = reinterpret_cast<float4*>(nxt);
+    if (MPAP_CULL_FENV) nxt += fs * 2;
+    L.boxf = reinterpret_cast<float*>(nxt);
+    if (MPAP_FMASK_F32) nxt += os * D;
+    L.fidx = reinterpret_cast<int*>(nxt);
     L.mlp = s_mlp;
   }
+  int staged_env = -1;   // environment whose features L.fenv holds (PHASE 1)
   const int64_t NI = items ? n_items : node_base[B];
   const int stride = P.stride;
   Work W;
@@ -1073,6 +1150,15 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
     const double* ebox = obst + (size_t)obst_base[b] * 2 * D;
     const double* efeat = feat + (size_t)feat_base[b] * D;
     const double* envs = samples + node_base[b] * stride;
+    if (MPAP_CULL_FENV && PHASE == 1 && b != staged_env) {   // stage the environment's features as float
+      __syncwarp();
+      for (int i = lane; i < F; i += 32) {
+        const double* fp = efeat + (size_t)i * D;
+        L.fenv[i] = make_float4((float)__ldg(fp), (float)__ldg(fp + 1), (D == 3) ? (float)__ldg(fp + D - 1) : 0.0f,
+                                0.0f);
+      }
+      staged_env = b;
+    }
     __syncwarp();
     if (lane < NS) su[lane] = (lane < stride) ? envs[u * stride + lane] : 0.0;
     int nfree = 0;
@@ -1354,7 +1440,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_affected(const double* __restri
             }
             if (near) {
 #pragma unroll
-              for (int k = 0; k < D; ++k) { vlo[k] = fmin(vlo[k], fc[k]); vhi[k] = fmax(vhi[k], fc[k]); }
+              for (int k = 0; k < D; ++k) { vlo[k] = dmin(vlo[k], fc[k]); vhi[k] = dmax(vhi[k], fc[k]); }
             }
           }
         }
@@ -1556,8 +1642,7 @@ cudaError_t edge_phases(size_t smem, cudaStream_t st, const mpap_roadmap* rm, Ed
 }
 
 size_t edges_smem(const mpap_roadmap* rm) {
-  const int d = rm->prm.pos_dim;
-  return sizeof(double) * (size_t)kWarps * ((size_t)rm->f_max * (d + 1) + (size_t)rm->o_max * 2 * d);
+  return sizeof(double) * (size_t)kWarps * warp_scratch_doubles(rm->prm.pos_dim, round4(rm->f_max), round4(rm->o_max));
 }
 }  // namespace
 

@@ -280,11 +280,16 @@ static mpap_status validate_params(const mpap_params* p, double r) {
 static mpap_status check_env_sizes(int d, int64_t n_obstacles, int64_t n_features) {
   constexpr int64_t kEdgeWarps = 4, kStaticBytes = 8 * 1024, kSmemMax = 227 * 1024;
   if (n_features > 65535) return set_error(MPAP_ERR_INVALID_ARGUMENT, "more than 65535 features in one environment");
-  const int64_t bytes = 8 * kEdgeWarps * (n_features * (d + 1) + n_obstacles * 2 * d) + kStaticBytes;
+  // per warp at most fs (d + 3.5) + 3 d os doubles with fs, os = F, O rounded
+  // up to a multiple of 4 (warp_scratch_doubles in build_kernels.cu, both
+  // single-precision cull options on)
+  const int64_t fs = (n_features + 3) & ~3, os = (n_obstacles + 3) & ~3;
+  const int64_t bytes = 4 * kEdgeWarps * (fs * (2 * d + 7) + os * 6 * d) + kStaticBytes;
   if (bytes > kSmemMax)
     return set_error(MPAP_ERR_INVALID_ARGUMENT,
                      "environment too large for the edge kernels' shared-memory working set "
-                     "(32 (F (d + 1) + 2 d O) bytes + 8 KB must fit in 227 KB)");
+                     "(16 (F4 (2 d + 7) + 6 d O4) bytes + 8 KB, F4 / O4 = F / O rounded up to a multiple of 4, "
+                     "must fit in 227 KB)");
   return MPAP_OK;
 }
 
