@@ -153,6 +153,16 @@ struct ClusterTeam {
   __device__ __forceinline__ void sync() const { cg::this_cluster().sync(); }
 };
 
+// Debug bounds checks (compute-sanitizer is closed on this pool): a build with
+// -DMPAP_DEBUG_CHECKS=1 counts every out-of-range store index of the search
+// kernels in g_dcheck_fail (read back after each search; a non-zero count is
+// reported as MPAP_ERR_CUDA).  Compiled out otherwise.
+#ifndef MPAP_DEBUG_CHECKS
+#define MPAP_DEBUG_CHECKS 0
+#endif
+__device__ unsigned long long g_dcheck_fail = 0;
+#define DCHECK(cond) do { if (MPAP_DEBUG_CHECKS && !(cond)) atomicAdd(&g_dcheck_fail, 1ull); } while (0)
+
 // control words are re-read after every team barrier
 template <typename T>
 __device__ __forceinline__ T vld(const T& x) { return *(const volatile T*)&x; }
@@ -210,8 +220,8 @@ __device__ void partition(const Team& team, const SearchArgs& A, Ctl* S, const i
     }
     bg = __shfl_sync(FULLM, bg, 0);
     bd = __shfl_sync(FULLM, bd, 0);
-    if (toG) G[bg + __popc(mg & lt)] = id;
-    if (toD) dst[bd + __popc(md & lt)] = id;
+    if (toG) { DCHECK(bg + __popc(mg & lt) < A.caps.L); G[bg + __popc(mg & lt)] = id; }
+    if (toD) { DCHECK(bd + __popc(md & lt) < A.caps.L); dst[bd + __popc(md & lt)] = id; }
   }
   if (mygoal) S->goal_in_g = 1;
   if (myminb != LLONG_MAX) atomicMin(&S->minb, myminb);
@@ -399,8 +409,13 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
             if (emit) {
               const int idx = base + __popc(em & lt);
               if (idx < C.C) {
+                DCHECK(x >= 0 && x < n);
                 cand[idx] = make_int4(x, __float_as_int(qc), __float_as_int(qh), p);
-                if (atomicAdd(&ccnt[x], 1) == 0) touched[atomicAdd(&S->ntouched, 1)] = x;
+                if (atomicAdd(&ccnt[x], 1) == 0) {
+                  const int tpos = atomicAdd(&S->ntouched, 1);
+                  DCHECK(tpos < n);
+                  touched[tpos] = x;
+                }
               } else {
                 atomicOr(&S->overflow, OVF_CAND);
               }
@@ -428,6 +443,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
     for (int k = tid; k < ncand; k += nthr) {
       const int4 cq = cand[k];
       const int pos = atomicAdd(&coff[cq.x], 1);
+      DCHECK(pos >= 0 && pos < C.C);
       cs[pos] = cq;
     }
     team.sync();
@@ -570,6 +586,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
             const int4 cq = sv[qq];
             const float qc = __int_as_float(cq.y), qh = __int_as_float(cq.z);
             const int id = lbase + lane;
+            DCHECK(id < C.L && pbase + lane < C.L && cq.w >= 0 && cq.w < C.L);
             labels[id] = make_int4(x, cq.w, cq.y, cq.z);
             lstate[id] = L_OPEN;
             pend[pbase + lane] = id;
@@ -1103,6 +1120,11 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
   }
   if (d_waves) CKS(cudaFreeAsync(d_waves, st));
   if (mem == MPAP_MEM_DEVICE) CKS(cudaStreamSynchronize(st));
+  if (MPAP_DEBUG_CHECKS) {
+    unsigned long long fails = 0;
+    CKS(cudaMemcpyFromSymbol(&fails, g_dcheck_fail, sizeof(fails)));
+    if (fails) return set_error(MPAP_ERR_CUDA, "MPAP_DEBUG_CHECKS: out-of-range store index in the search kernels");
+  }
   return status;
 }
 
