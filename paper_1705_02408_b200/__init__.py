@@ -117,9 +117,10 @@ _lib.mpap_search_ex.argtypes = [_vp, C.c_int32, C.c_int32, C.POINTER(mpap_goal),
                                 _i32p, C.c_int32, C.POINTER(mpap_result), C.POINTER(mpap_wave), C.c_int32, _vp]
 _lib.mpap_search_batch_ex.argtypes = [_vp, C.c_int32, _i32p, _i32p, C.POINTER(mpap_goal), C.POINTER(C.c_double),
                                       C.c_double, C.c_uint32, _vp, C.c_int32, _vp, C.c_int32, _vp]
-_lib.mpap_search_batch_trace.argtypes = [_vp, C.c_int32, _i32p, _i32p, C.POINTER(mpap_goal),
-                                         C.POINTER(C.c_double), C.c_double, C.c_uint32, _vp, C.c_int32, _vp,
-                                         C.c_int32, _vp, C.c_int32, _vp]
+if hasattr(_lib, "mpap_search_batch_trace"):   # (older tuning builds loaded via MPAP_LIB may lack it)
+    _lib.mpap_search_batch_trace.argtypes = [_vp, C.c_int32, _i32p, _i32p, C.POINTER(mpap_goal),
+                                             C.POINTER(C.c_double), C.c_double, C.c_uint32, _vp, C.c_int32, _vp,
+                                             C.c_int32, _vp, C.c_int32, _vp]
 _lib.mpap_mc_verify_batch.argtypes = [_vp, C.c_int32, _vp, _vp, C.c_int32, _vp, C.POINTER(mpap_mc_params),
                                       C.c_uint64, _vp, _vp, _vp, _vp]
 _lib.mpap_mc_verify.argtypes = [_vp, C.c_int32, _vp, C.c_int32, C.POINTER(mpap_mc_params), C.c_uint64, _vp, _vp,
@@ -151,10 +152,12 @@ _lib.mpap_prof_enable.restype = None
 _lib.mpap_prof_reset.restype = None
 _lib.mpap_prof_read.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
 _lib.mpap_prof_read.restype = C.c_int32
-_lib.mpap_prof_fp64_peak.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
-_lib.mpap_prof_fp64_peak.restype = C.c_int
-_lib.mpap_search_launches.argtypes = [C.c_int32]
-_lib.mpap_search_launches.restype = C.c_int64
+if hasattr(_lib, "mpap_prof_fp64_peak"):
+    _lib.mpap_prof_fp64_peak.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    _lib.mpap_prof_fp64_peak.restype = C.c_int
+if hasattr(_lib, "mpap_search_launches"):
+    _lib.mpap_search_launches.argtypes = [C.c_int32]
+    _lib.mpap_search_launches.restype = C.c_int64
 for _f in ("mpap_build_roadmap_batch", "mpap_build_roadmap", "mpap_search", "mpap_search_batch",
            "mpap_search_ex", "mpap_search_batch_ex", "mpap_roadmap_export_peaks", "mpap_roadmap_set_peaks",
            "mpap_roadmap_update", "mpap_roadmap_import", "mpap_roadmap_info", "mpap_roadmap_export"):
@@ -518,6 +521,8 @@ SEARCH_TEAMS = {"grid": 0, "cluster": 1, "cta": 2}
 
 def mpap_search_launches() -> Dict[str, int]:
     """Search launches so far per team kind (grid / cluster / cta)."""
+    if not hasattr(_lib, "mpap_search_launches"):
+        return {}
     return {k: int(_lib.mpap_search_launches(v)) for k, v in SEARCH_TEAMS.items()}
 
 

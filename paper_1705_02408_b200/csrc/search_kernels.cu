@@ -817,9 +817,13 @@ __global__ void __launch_bounds__(kST) k_search_cluster(SearchArgs A, Ctl* S_all
 }
 
 // A single query over the whole grid (cooperative launch; grid.sync between
-// the phases of each wave).  Control words live in global memory.
+// the phases of each wave).  Control words live in global memory.  One block
+// per SM is pinned in the launch bounds: left free, ptxas may squeeze the
+// kernel to 64 registers (two blocks per SM) with local-memory spills, which
+// measured 3x slower single queries (C1 8.1 -> 27.0 ms, C4 1.02 beta_min
+// 48 -> 136 ms; profiles/r02/search_regression_ab.jsonl).
 template <bool TRACE>
-__global__ void __launch_bounds__(kST) k_search_grid(SearchArgs A, Ctl* S) {
+__global__ void __launch_bounds__(kST, 1) k_search_grid(SearchArgs A, Ctl* S) {
   const GridTeam team;
   run_query<TRACE>(team, A, S, 0, 0);
 }

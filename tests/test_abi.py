@@ -163,3 +163,12 @@ def test_build_rejects_oversized_environment(mp, nfeat, nobst):
     assert s == mp.MPAP_ERR_INVALID_ARGUMENT
     assert out.value is None
     assert b"feature" in lib.mpap_last_error() or b"shared" in lib.mpap_last_error()
+
+
+def test_grid_search_kernel_keeps_its_registers(mp):
+    """k_search_grid is pinned to one block per SM (__launch_bounds__(512, 1)):
+    squeezed to 64 registers with local-memory spills it ran single queries
+    3x slower (profiles/r02/search_regression_ab.jsonl)."""
+    out = subprocess.run(["cuobjdump", "-res-usage", mp.LIB_PATH], capture_output=True, text=True).stdout
+    regs = re.findall(r"k_search_gridILb[01]E\S*:\s*\n\s*REG:(\d+)", out)
+    assert len(regs) == 2 and all(int(r) > 64 for r in regs), regs
