@@ -16,11 +16,15 @@
 //            appended with warp-aggregated atomics (ballot + popc).
 //   group    per-destination counts -> atomic range allocation -> scatter,
 //            so each touched node's candidates are contiguous.
-//   merge    warp per touched node: RemoveDominated (A3.15) as a set
-//            operation -- old staircase entries dominated by a candidate die
-//            (open ones are removed from P_open), candidates dominated by
-//            another candidate are dropped, survivors get label ids (warp-
-//            aggregated) and enter the staircase and the pending open list.
+//   merge    RemoveDominated (A3.15) as a set operation per touched
+//            node -- old staircase entries dominated by a candidate die (open
+//            ones are removed from P_open), candidates dominated by another
+//            candidate are dropped, survivors get label ids and enter the
+//            staircase and the pending open list.  Small nodes (<= 48
+//            candidates and entries): one warp each, all-pairs in shared
+//            memory, pulled from a work counter.  Large nodes: one whole CTA
+//            each, O(k log k): bitonic sort, prefix-min scan for the
+//            survivors, binary searches for the kills and the merged order.
 //   advance  G_i is retired (A3.16), i <- i+1 (A3.17), and the pending list
 //            is partitioned into G_{i+1} = {cost <= (i+1) lambda r_n} (A3.18)
 //            with ballot compaction; empty groups are skipped exactly (R24).
@@ -33,6 +37,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -53,6 +58,8 @@ constexpr int kSeqLargeMaxQ = 32;    //     of at most this many queries (C4 ref
                                      //     measured; larger batches fill the SMs with clusters / CTAs)
 constexpr int kMaxTies = 32;           // (cost, h) ties listed for the R16 tie-break; more -> leader scan
 constexpr int kMrgCap = 48;           // merge: a node's candidates / staircase staged in shared memory up to this size
+constexpr int kBigC = 2048;           // CTA merge of a large node: candidates (power of two, 4 per thread)
+constexpr int kBigM = 1024;           // ... and staircase entries (2 per thread); larger nodes take the warp path
 enum : uint8_t { L_OPEN = 0, L_CLOSED = 1, L_DEAD = 2 };
 enum { OVF_LABELS = 1, OVF_CAND = 2, OVF_STAIR = 4 };
 constexpr int kRetryBase = 100;       // result.status = kRetryBase + OVF_* mask
@@ -91,6 +98,8 @@ struct SearchArgs {
   int4* cand;
   int4* cand_sorted;
   int32_t* touched;
+  int32_t* tsmall;     // touched nodes merged by one warp each
+  int32_t* tbig;       // touched nodes merged by one CTA each
   int32_t* G;
   int32_t* pend;
   int32_t* pend2;
@@ -113,6 +122,7 @@ struct SearchArgs {
 
 struct Ctl {
   int q, gsize, psize, nsize, ncand, ntouched, nlabels, goal_in_g, overflow, any_goal, calloc;
+  int nsmall, nbig, snext;   // merge work lists (small: warp per node, pulled from snext; big: CTA per node)
   long long i, minb;
   unsigned long long relax, bpass, tcount, ssum, inserted, killed;
   unsigned long long relax_total, inserted_total;
@@ -127,6 +137,8 @@ struct Ctl {
 // A team runs one query: a CTA (batched queries, __syncthreads) or the whole
 // grid of a cooperative launch (a single latency-bound query, grid.sync).
 struct CtaTeam {
+  __device__ __forceinline__ int cta() const { return 0; }
+  __device__ __forceinline__ int ncta() const { return 1; }
   __device__ __forceinline__ int rank() const { return threadIdx.x; }
   __device__ __forceinline__ int size() const { return blockDim.x; }
   __device__ __forceinline__ int warp() const { return threadIdx.x >> 5; }
@@ -134,6 +146,8 @@ struct CtaTeam {
   __device__ __forceinline__ void sync() const { __syncthreads(); }
 };
 struct GridTeam {
+  __device__ __forceinline__ int cta() const { return blockIdx.x; }
+  __device__ __forceinline__ int ncta() const { return gridDim.x; }
   __device__ __forceinline__ int rank() const { return blockIdx.x * blockDim.x + threadIdx.x; }
   __device__ __forceinline__ int size() const { return gridDim.x * blockDim.x; }
   __device__ __forceinline__ int warp() const { return rank() >> 5; }
@@ -144,6 +158,8 @@ struct GridTeam {
 // A thread-block cluster (hardware barrier across its CTAs, which run on
 // different SMs); used for batches with fewer queries than resident CTAs.
 struct ClusterTeam {
+  __device__ __forceinline__ int cta() const { return (int)cg::this_cluster().block_rank(); }
+  __device__ __forceinline__ int ncta() const { return (int)cg::this_cluster().num_blocks(); }
   __device__ __forceinline__ int rank() const {
     return (int)cg::this_cluster().block_rank() * blockDim.x + threadIdx.x;
   }
@@ -239,6 +255,290 @@ __device__ __forceinline__ bool key_less(float ac, float ah, float bc, float bh)
   return ac < bc || (ac == bc && ah > bh);
 }
 
+// ---------------------------------------------------------------------------
+// CTA-cooperative merge of one large node (RemoveDominated + insert, A3.15,
+// P:193) -- the same set result as the warp path, in O(k log k):
+//   1. the node's candidates are bitonic-sorted by (cost asc, h desc, parent);
+//   2. candidate q survives iff min{h_r : cost_r < cost_q} > h_q (prefix-min
+//      scan of h, read at the start of q's equal-cost group);
+//   3. survivors form a staircase, so the cheapest-h survivor of cost < c is
+//      the last one of cost < c: an old entry o dies iff that survivor has
+//      h <= o.h (binary search);
+//   4. merged order: old alive entry j goes to (alive entries before j) +
+//      (survivors with key < o); survivor q to q + (alive entries with key <=
+//      q) -- both by binary search, alive counts from a prefix sum.
+// ---------------------------------------------------------------------------
+struct BigSmem {
+  int4 c[kBigC];          // candidates (x, cost, h, parent); survivors compacted in place
+  float pm[kBigC];        // inclusive prefix minimum of h over the sorted candidates
+  int gs[kBigC];          // start index of each candidate's equal-cost group
+  float2 st[kBigM];       // the node's old staircase
+  int32_t si[kBigM];
+  int ap[kBigM + 1];      // alive old entries before j
+  float fscr[32];
+  int iscr[32];
+  int bc[2];
+};
+constexpr size_t kBigSmem = sizeof(BigSmem);
+
+__device__ __forceinline__ bool cand_less(const int4& a, const int4& b) {
+  const float ac = __int_as_float(a.y), bc = __int_as_float(b.y);
+  const float ah = __int_as_float(a.z), bh = __int_as_float(b.z);
+  return ac < bc || (ac == bc && (ah > bh || (ah == bh && a.w < b.w)));
+}
+
+// Block-wide exclusive scans (blockDim.x threads, a multiple of 32).
+__device__ __forceinline__ int block_excl_sum(int v, int* scr, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  int x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULLM, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) scr[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < nwb ? scr[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULLM, t, o);
+      if (lane >= o) t += y;
+    }
+    scr[lane] = t;
+  }
+  __syncthreads();
+  const int r = (w > 0 ? scr[w - 1] : 0) + x - v;
+  *total = scr[nwb - 1];
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ float block_excl_min(float v, float* scr) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  float x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const float y = __shfl_up_sync(FULLM, x, o);
+    if (lane >= o) x = fminf(x, y);
+  }
+  const float ex = __shfl_up_sync(FULLM, x, 1);
+  if (lane == 31) scr[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    float t = lane < nwb ? scr[lane] : __int_as_float(0x7f800000);
+    for (int o = 1; o < 32; o <<= 1) {
+      const float y = __shfl_up_sync(FULLM, t, o);
+      if (lane >= o) t = fminf(t, y);
+    }
+    scr[lane] = t;
+  }
+  __syncthreads();
+  float r = (lane > 0) ? ex : __int_as_float(0x7f800000);
+  if (w > 0) r = fminf(r, scr[w - 1]);
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ int block_excl_max(int v, int* scr) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  int x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULLM, x, o);
+    if (lane >= o) x = max(x, y);
+  }
+  const int ex = __shfl_up_sync(FULLM, x, 1);
+  if (lane == 31) scr[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < nwb ? scr[lane] : INT_MIN;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULLM, t, o);
+      if (lane >= o) t = max(t, y);
+    }
+    scr[lane] = t;
+  }
+  __syncthreads();
+  int r = (lane > 0) ? ex : INT_MIN;
+  if (w > 0) r = max(r, scr[w - 1]);
+  __syncthreads();
+  return r;
+}
+
+__device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* cs, const int32_t* coff,
+                          const int32_t* ccnt, float2* sch, int32_t* sid, int32_t* sn, int4* labels,
+                          uint8_t* lstate, int32_t* pend, unsigned long long& my_ins, unsigned long long& my_kill) {
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  BigSmem& B = *reinterpret_cast<BigSmem*>(s_dyn);
+  const int tid = threadIdx.x, bd = blockDim.x;
+  constexpr int EC = kBigC / kST, EM = kBigM / kST;   // elements per thread
+  const int kc = ccnt[x];
+  const int beg = coff[x] - kc;
+  const int snx = sn[x];
+  const int m = snx & kStairCountMask;
+  const int par = snx >> 30;
+  const float2* st = sch + stair_base(snx, x, n, C.K);
+  const int32_t* si = sid + stair_base(snx, x, n, C.K);
+  float2* nst = sch + ((size_t)(par ^ 1) * n + x) * (size_t)C.K;
+  int32_t* nsi = sid + ((size_t)(par ^ 1) * n + x) * (size_t)C.K;
+  int p2 = 2;
+  while (p2 < kc) p2 <<= 1;
+  for (int i = tid; i < p2; i += bd)
+    B.c[i] = (i < kc) ? cs[beg + i] : make_int4(x, 0x7f800000, (int)0xff800000, INT_MAX);   // +inf cost: last
+  for (int j = tid; j < m; j += bd) {
+    B.st[j] = st[j];
+    B.si[j] = si[j];
+  }
+  __syncthreads();
+  // 1. bitonic sort ascending by (cost, -h, parent)
+  for (int k = 2; k <= p2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < p2; i += bd) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const int4 a = B.c[i], b = B.c[ixj];
+          if (cand_less(b, a) == ((i & k) == 0)) {
+            B.c[i] = b;
+            B.c[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // 2. survivors: prefix min of h and equal-cost group starts
+  int4 cq[EC];
+  float lmin = __int_as_float(0x7f800000);
+  int lmax = 0;
+#pragma unroll
+  for (int r = 0; r < EC; ++r) {
+    const int i = tid * EC + r;
+    cq[r] = B.c[i];
+    if (i < kc) {
+      lmin = fminf(lmin, __int_as_float(cq[r].z));
+      if (i == 0 || __int_as_float(B.c[i - 1].y) != __int_as_float(cq[r].y)) lmax = i;
+    }
+  }
+  float run = block_excl_min(lmin, B.fscr);
+  int gstart = block_excl_max(lmax, B.iscr);
+  if (gstart < 0) gstart = 0;
+#pragma unroll
+  for (int r = 0; r < EC; ++r) {
+    const int i = tid * EC + r;
+    if (i < kc) {
+      run = fminf(run, __int_as_float(cq[r].z));
+      if (i == 0 || __int_as_float(B.c[i - 1].y) != __int_as_float(cq[r].y)) gstart = i;
+      B.pm[i] = run;
+      B.gs[i] = gstart;
+    }
+  }
+  __syncthreads();
+  bool surv[EC];
+  int nloc = 0;
+#pragma unroll
+  for (int r = 0; r < EC; ++r) {
+    const int i = tid * EC + r;
+    surv[r] = false;
+    if (i < kc) {
+      const int g = B.gs[i];
+      surv[r] = (g == 0) || (B.pm[g - 1] > __int_as_float(cq[r].z));
+      nloc += surv[r] ? 1 : 0;
+    }
+  }
+  int ns = 0;
+  int spos = block_excl_sum(nloc, B.iscr, &ns);   // (its barriers also order the reads of B.c above)
+#pragma unroll
+  for (int r = 0; r < EC; ++r)
+    if (surv[r]) B.c[spos++] = cq[r];
+  __syncthreads();
+  // 3. kills of old entries
+  bool alive[EM];
+  int aloc = 0;
+#pragma unroll
+  for (int r = 0; r < EM; ++r) {
+    const int j = tid * EM + r;
+    alive[r] = false;
+    if (j < m) {
+      const float2 o = B.st[j];
+      int lo = 0, hi = ns;   // first survivor with cost >= o.x
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__int_as_float(B.c[mid].y) < o.x) lo = mid + 1; else hi = mid;
+      }
+      const bool dead = lo > 0 && __int_as_float(B.c[lo - 1].z) <= o.y;
+      alive[r] = !dead;
+      aloc += alive[r] ? 1 : 0;
+      if (dead) {
+        const int oid = B.si[j];
+        if (lstate[oid] == L_OPEN) {
+          lstate[oid] = L_DEAD;
+          ++my_kill;
+        }
+      }
+    }
+  }
+  int na = 0;
+  int apos = block_excl_sum(aloc, B.iscr, &na);
+#pragma unroll
+  for (int r = 0; r < EM; ++r) {
+    const int j = tid * EM + r;
+    if (j < m) {
+      B.ap[j] = apos;
+      apos += alive[r] ? 1 : 0;
+    }
+  }
+  if (tid == 0) {
+    B.ap[m] = na;
+    B.bc[0] = atomicAdd(&S->nlabels, ns);
+    B.bc[1] = atomicAdd(&S->psize, ns);
+  }
+  __syncthreads();
+  // 4. merged staircase in the other buffer; survivors get labels
+#pragma unroll
+  for (int r = 0; r < EM; ++r) {
+    const int j = tid * EM + r;
+    if (j < m && alive[r]) {
+      const float2 o = B.st[j];
+      int lo = 0, hi = ns;   // survivors with key < o
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (key_less(__int_as_float(B.c[mid].y), __int_as_float(B.c[mid].z), o.x, o.y)) lo = mid + 1; else hi = mid;
+      }
+      const int pos = B.ap[j] + lo;
+      if (pos < C.K) {
+        nst[pos] = o;
+        nsi[pos] = B.si[j];
+      }
+    }
+  }
+  const int lbase = B.bc[0], pbase = B.bc[1];
+  if (lbase + ns > C.L) {
+    if (tid == 0) atomicOr(&S->overflow, OVF_LABELS);
+  } else {
+    for (int q = tid; q < ns; q += bd) {
+      const int4 c = B.c[q];
+      const float qc = __int_as_float(c.y), qh = __int_as_float(c.z);
+      const int id = lbase + q;
+      DCHECK(id < C.L && pbase + q < C.L && c.w >= 0 && c.w < C.L);
+      labels[id] = make_int4(x, c.w, c.y, c.z);
+      lstate[id] = L_OPEN;
+      pend[pbase + q] = id;
+      int lo = 0, hi = m;   // first old entry with key > q
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (key_less(qc, qh, B.st[mid].x, B.st[mid].y)) hi = mid; else lo = mid + 1;
+      }
+      const int pos = q + B.ap[lo];
+      if (pos < C.K) {
+        nst[pos] = make_float2(qc, qh);
+        nsi[pos] = id;
+      }
+    }
+  }
+  if (tid == 0) {
+    const int newm = na + ns;
+    if (newm > C.K) atomicOr(&S->overflow, OVF_STAIR);
+    sn[x] = min(newm, C.K) | ((par ^ 1) << 30);
+    my_ins += (unsigned long long)ns;
+  }
+  __syncthreads();   // B is reused by the CTA's next large node
+}
+
 template <bool TRACE, typename Team>
 __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slot, int qpos) {
   const int q = A.qidx[qpos];
@@ -263,6 +563,8 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
   int4* cand = A.cand + (size_t)slot * C.C;
   int4* cs = A.cand_sorted + (size_t)slot * C.C;
   int32_t* touched = A.touched + (size_t)slot * C.n;
+  int32_t* tsmall = A.tsmall + (size_t)slot * C.n;
+  int32_t* tbig = A.tbig + (size_t)slot * C.n;
   int32_t* G = A.G + (size_t)slot * C.L;
   int32_t* pend = A.pend + (size_t)slot * C.L;
   int32_t* pend2 = A.pend2 + (size_t)slot * C.L;
@@ -347,7 +649,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
     if (leader) {
       S->need = 0;
       S->relax = 0; S->bpass = 0; S->tcount = 0; S->ssum = 0; S->inserted = 0; S->killed = 0;
-      S->ncand = 0; S->ntouched = 0; S->calloc = 0;
+      S->ncand = 0; S->ntouched = 0; S->calloc = 0; S->nsmall = 0; S->nbig = 0; S->snext = 0;
     }
     team.sync();
     // ---- a7 expand (A3.6-A3.11): warp per plan of G_i, 32 edges per step ----
@@ -437,7 +739,11 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
     // ---- group candidates by destination: contiguous range per touched node ----
     for (int t = tid; t < nt; t += nthr) {
       const int x = touched[t];
-      coff[x] = atomicAdd(&S->calloc, ccnt[x]);
+      const int kc = ccnt[x];
+      coff[x] = atomicAdd(&S->calloc, kc);
+      const int m = sn[x] & kStairCountMask;
+      if ((kc > kMrgCap || m > kMrgCap) && kc <= kBigC && m <= kBigM) tbig[atomicAdd(&S->nbig, 1)] = x;
+      else tsmall[atomicAdd(&S->nsmall, 1)] = x;
     }
     team.sync();
     for (int k = tid; k < ncand; k += nthr) {
@@ -458,8 +764,18 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
       __shared__ int32_t s_sid[kST / 32][kMrgCap];
       const int wl = threadIdx.x >> 5;
       unsigned long long my_ins = 0, my_kill = 0;
-      for (int t = warp; t < nt; t += nw) {
-        const int x = touched[t];
+      // large nodes: one CTA each (uniform per CTA: __syncthreads inside)
+      const int nbig = vld(S->nbig), nsmall = vld(S->nsmall);
+      for (int b = team.cta(); b < nbig; b += team.ncta())
+        cta_merge(S, C, tbig[b], n, cs, coff, ccnt, sch, sid, sn, labels, lstate, pend, my_ins, my_kill);
+      // small nodes: one warp each, pulled from a counter (warps of CTAs busy
+      // with large nodes join late)
+      for (;;) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(&S->snext, 1);
+        t = __shfl_sync(FULLM, t, 0);
+        if (t >= nsmall) break;
+        const int x = tsmall[t];
         const int kc = ccnt[x];
         const int beg = coff[x] - kc;
         const int snx = sn[x];
@@ -857,6 +1173,8 @@ size_t carve(SearchArgs* A, const SlotCaps& c, int nslots, char* base) {
   p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->cand_cnt = (int32_t*)p;
   p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->cand_off = (int32_t*)p;
   p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->touched = (int32_t*)p;
+  p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->tsmall = (int32_t*)p;
+  p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->tbig = (int32_t*)p;
   p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->stamp = (int32_t*)p;
   p = take((size_t)c.n);                                if (A) A->goal = (uint8_t*)p;
   p = take(sizeof(int4) * (size_t)c.C);                 if (A) A->cand = (int4*)p;
@@ -869,6 +1187,24 @@ size_t carve(SearchArgs* A, const SlotCaps& c, int nslots, char* base) {
 }  // namespace
 
 
+// The CTA merge of large nodes uses kBigSmem bytes of dynamic shared memory
+// (above the 48 KB default): opt every search kernel in, once per device.
+cudaError_t set_search_smem() {
+  static int done_dev = -1;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || dev == done_dev) return e;
+  const void* fns[] = {(const void*)k_search<false>, (const void*)k_search<true>, (const void*)k_search_cluster<false>,
+                       (const void*)k_search_cluster<true>, (const void*)k_search_grid<false>,
+                       (const void*)k_search_grid<true>};
+  for (const void* f : fns) {
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBigSmem);
+    if (e != cudaSuccess) return e;
+  }
+  done_dev = dev;
+  return cudaSuccess;
+}
+
 mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryDesc* h_queries, double lambda,
                                 int32_t* paths, int32_t path_cap, mpap_result* results, mpap_wave* h_waves,
                                 int32_t waves_cap, int32_t mem, cudaStream_t st) {
@@ -879,13 +1215,14 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
   CKS(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   const bool trace = (h_waves != nullptr && waves_cap > 0);
   int occ = 1;
-  if (trace) CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_search<true>, kST, 0));
-  else CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_search<false>, kST, 0));
+  CKS(set_search_smem());
+  if (trace) CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_search<true>, kST, kBigSmem));
+  else CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_search<false>, kST, kBigSmem));
   occ = std::max(occ, 1);
   int occ_grid = 1, coop = 0;
   CKS(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-  if (trace) CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_grid, k_search_grid<true>, kST, 0));
-  else CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_grid, k_search_grid<false>, kST, 0));
+  if (trace) CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_grid, k_search_grid<true>, kST, kBigSmem));
+  else CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_grid, k_search_grid<false>, kST, kBigSmem));
   const bool use_grid = coop && occ_grid > 0 && getenv("MPAP_SEARCH_CTA") == nullptr && getenv("MPAP_SEARCH_NO_GRID") == nullptr;
   const bool use_cluster = getenv("MPAP_SEARCH_CTA") == nullptr && getenv("MPAP_SEARCH_NO_CLUSTER") == nullptr;
   // A handful of queries (a perception-bound sweep) runs one after the other
@@ -1016,11 +1353,12 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
           if (grid_mode) {
             void* args[] = {&A, &d_ctl};
             const void* fn = trace ? (const void*)k_search_grid<true> : (const void*)k_search_grid<false>;
-            CKS(cudaLaunchCooperativeKernel(fn, dim3(nsm * occ_grid), dim3(kST), args, 0, st));
+            CKS(cudaLaunchCooperativeKernel(fn, dim3(nsm * occ_grid), dim3(kST), args, kBigSmem, st));
           } else {
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(nslots * csize);
             cfg.blockDim = dim3(kST);
+            cfg.dynamicSmemBytes = kBigSmem;
             cfg.stream = st;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1051,12 +1389,12 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
       if (grid_mode) {
         void* args[] = {&A, &d_ctl};
         const void* fn = trace ? (const void*)k_search_grid<true> : (const void*)k_search_grid<false>;
-        CKS(cudaLaunchCooperativeKernel(fn, dim3(nsm * occ_grid), dim3(kST), args, 0, st));
+        CKS(cudaLaunchCooperativeKernel(fn, dim3(nsm * occ_grid), dim3(kST), args, kBigSmem, st));
       } else if (cluster_mode) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(nslots * csize);
         cfg.blockDim = dim3(kST);
-        cfg.dynamicSmemBytes = 0;
+        cfg.dynamicSmemBytes = kBigSmem;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1068,9 +1406,9 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
         if (trace) CKS(cudaLaunchKernelEx(&cfg, k_search_cluster<true>, A, d_ctl));
         else CKS(cudaLaunchKernelEx(&cfg, k_search_cluster<false>, A, d_ctl));
       } else if (trace) {
-        k_search<true><<<nslots, kST, 0, st>>>(A);
+        k_search<true><<<nslots, kST, kBigSmem, st>>>(A);
       } else {
-        k_search<false><<<nslots, kST, 0, st>>>(A);
+        k_search<false><<<nslots, kST, kBigSmem, st>>>(A);
       }
       note_launch();
       note_team(grid_mode ? 0 : cluster_mode ? 1 : 2);
