@@ -59,7 +59,7 @@ constexpr int kSeqLargeMaxQ = 32;    //     of at most this many queries (C4 ref
 constexpr int kMaxTies = 32;           // (cost, h) ties listed for the R16 tie-break; more -> leader scan
 constexpr int kMrgCap = 48;           // merge: a node's candidates / staircase staged in shared memory up to this size
 constexpr int kBigC = 2048;           // CTA merge of a large node: candidates (power of two, 4 per thread)
-constexpr int kBigM = 1024;           // ... and staircase entries (2 per thread); larger nodes take the warp path
+constexpr int kBigM = 4096;           // ... and staircase entries (8 per thread); larger nodes take the warp path
 enum : uint8_t { L_OPEN = 0, L_CLOSED = 1, L_DEAD = 2 };
 enum { OVF_LABELS = 1, OVF_CAND = 2, OVF_STAIR = 4 };
 constexpr int kRetryBase = 100;       // result.status = kRetryBase + OVF_* mask
@@ -100,6 +100,7 @@ struct SearchArgs {
   int32_t* touched;
   int32_t* tsmall;     // touched nodes merged by one warp each
   int32_t* tbig;       // touched nodes merged by one CTA each
+  int32_t* tmid;       // touched nodes with <= 32 candidates but a large staircase: one warp each
   int32_t* G;
   int32_t* pend;
   int32_t* pend2;
@@ -122,7 +123,9 @@ struct SearchArgs {
 
 struct Ctl {
   int q, gsize, psize, nsize, ncand, ntouched, nlabels, goal_in_g, overflow, any_goal, calloc;
-  int nsmall, nbig, snext;   // merge work lists (small: warp per node, pulled from snext; big: CTA per node)
+  int nsmall, nbig, snext, bnext;   // merge work lists (small: warp per node, pulled from snext; big: CTA per
+                                    // node, pulled from bnext)
+  int nmid, mnext;                  // mid: warp per node (binary searches), pulled from mnext
   long long i, minb;
   unsigned long long relax, bpass, tcount, ssum, inserted, killed;
   unsigned long long relax_total, inserted_total;
@@ -178,6 +181,18 @@ struct ClusterTeam {
 #endif
 __device__ unsigned long long g_dcheck_fail = 0;
 #define DCHECK(cond) do { if (MPAP_DEBUG_CHECKS && !(cond)) atomicAdd(&g_dcheck_fail, 1ull); } while (0)
+// Per-wave phase timestamps of a single (whole-grid) query, debug builds
+// only (printed by the host when MPAP_PHASE_LOG is set): globaltimer after
+// each phase barrier, and the merge work split.
+constexpr int kPhaseWaves = 256;
+__device__ unsigned long long g_phase[kPhaseWaves][8];
+__device__ int g_phase_stat[kPhaseWaves][4];   // nbig, nsmall, max candidates, max staircase of a big node
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PHASE_MARK(k) do { if (MPAP_DEBUG_CHECKS && leader && A.nq == 1 && wave < kPhaseWaves) g_phase[wave][k] = gtimer(); } while (0)
 
 // control words are re-read after every team barrier
 template <typename T>
@@ -272,9 +287,7 @@ struct BigSmem {
   int4 c[kBigC];          // candidates (x, cost, h, parent); survivors compacted in place
   float pm[kBigC];        // inclusive prefix minimum of h over the sorted candidates
   int gs[kBigC];          // start index of each candidate's equal-cost group
-  float2 st[kBigM];       // the node's old staircase
-  int32_t si[kBigM];
-  int ap[kBigM + 1];      // alive old entries before j
+  int ap[kBigM + 1];      // alive old entries before j (the old staircase itself is read from global memory)
   float fscr[32];
   int iscr[32];
   int bc[2];
@@ -380,10 +393,6 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
   while (p2 < kc) p2 <<= 1;
   for (int i = tid; i < p2; i += bd)
     B.c[i] = (i < kc) ? cs[beg + i] : make_int4(x, 0x7f800000, (int)0xff800000, INT_MAX);   // +inf cost: last
-  for (int j = tid; j < m; j += bd) {
-    B.st[j] = st[j];
-    B.si[j] = si[j];
-  }
   __syncthreads();
   // 1. bitonic sort ascending by (cost, -h, parent)
   for (int k = 2; k <= p2; k <<= 1) {
@@ -454,7 +463,7 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
     const int j = tid * EM + r;
     alive[r] = false;
     if (j < m) {
-      const float2 o = B.st[j];
+      const float2 o = st[j];
       int lo = 0, hi = ns;   // first survivor with cost >= o.x
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
@@ -464,7 +473,7 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
       alive[r] = !dead;
       aloc += alive[r] ? 1 : 0;
       if (dead) {
-        const int oid = B.si[j];
+        const int oid = si[j];
         if (lstate[oid] == L_OPEN) {
           lstate[oid] = L_DEAD;
           ++my_kill;
@@ -493,7 +502,7 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
   for (int r = 0; r < EM; ++r) {
     const int j = tid * EM + r;
     if (j < m && alive[r]) {
-      const float2 o = B.st[j];
+      const float2 o = st[j];
       int lo = 0, hi = ns;   // survivors with key < o
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
@@ -502,7 +511,7 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
       const int pos = B.ap[j] + lo;
       if (pos < C.K) {
         nst[pos] = o;
-        nsi[pos] = B.si[j];
+        nsi[pos] = si[j];
       }
     }
   }
@@ -521,7 +530,8 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
       int lo = 0, hi = m;   // first old entry with key > q
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (key_less(qc, qh, B.st[mid].x, B.st[mid].y)) hi = mid; else lo = mid + 1;
+        const float2 om = st[mid];
+        if (key_less(qc, qh, om.x, om.y)) hi = mid; else lo = mid + 1;
       }
       const int pos = q + B.ap[lo];
       if (pos < C.K) {
@@ -537,6 +547,153 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
     my_ins += (unsigned long long)ns;
   }
   __syncthreads();   // B is reused by the CTA's next large node
+}
+
+// Warp merge of a node with <= 32 candidates and a staircase of up to kBigM
+// entries (left in global memory): the set semantics of cta_merge with one
+// candidate per lane -- a shuffle bitonic sort, shuffle scans for the
+// survivors, a binary search over the survivors per old entry, and a binary
+// search over the old staircase per survivor, with the alive counts kept per
+// 32-entry chunk in the warp's slice of the dynamic shared memory.
+struct MidSmem {
+  int4 sv[32];
+  int pre[kBigM / 32 + 1];
+  unsigned mask[kBigM / 32];
+};
+static_assert(sizeof(MidSmem) * (kST / 32) <= sizeof(BigSmem), "mid-merge slices must fit the CTA merge buffer");
+
+__device__ __forceinline__ int4 shfl_xor4(const int4& v, int j) {
+  return make_int4(__shfl_xor_sync(FULLM, v.x, j), __shfl_xor_sync(FULLM, v.y, j), __shfl_xor_sync(FULLM, v.z, j),
+                   __shfl_xor_sync(FULLM, v.w, j));
+}
+
+__device__ void warp_mid_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* cs, const int32_t* coff,
+                               const int32_t* ccnt, float2* sch, int32_t* sid, int32_t* sn, int4* labels,
+                               uint8_t* lstate, int32_t* pend, unsigned long long& my_ins,
+                               unsigned long long& my_kill) {
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  MidSmem& W = reinterpret_cast<MidSmem*>(s_dyn)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lane_lt();
+  const int kc = ccnt[x];
+  const int beg = coff[x] - kc;
+  const int snx = sn[x];
+  const int m = snx & kStairCountMask;
+  const int par = snx >> 30;
+  const float2* st = sch + stair_base(snx, x, n, C.K);
+  const int32_t* si = sid + stair_base(snx, x, n, C.K);
+  float2* nst = sch + ((size_t)(par ^ 1) * n + x) * (size_t)C.K;
+  int32_t* nsi = sid + ((size_t)(par ^ 1) * n + x) * (size_t)C.K;
+  int4 c = lane < kc ? cs[beg + lane] : make_int4(x, 0x7f800000, (int)0xff800000, INT_MAX);
+  // 1. bitonic sort across the warp, ascending by (cost, -h, parent)
+  for (int k = 2; k <= 32; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int4 o = shfl_xor4(c, j);
+      const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+      if (lower ? (cand_less(o, c) == up) : (cand_less(c, o) == up)) c = o;
+    }
+  }
+  // 2. survivors: min h over strictly cheaper candidates > own h
+  const bool valid = lane < kc;
+  const float cost = __int_as_float(c.y), h = __int_as_float(c.z);
+  float pm = valid ? h : __int_as_float(0x7f800000);
+  for (int o = 1; o < 32; o <<= 1) {
+    const float y = __shfl_up_sync(FULLM, pm, o);
+    if (lane >= o) pm = fminf(pm, y);
+  }
+  const float pc = __shfl_up_sync(FULLM, cost, 1);
+  int g = (lane == 0 || pc != cost) ? lane : 0;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULLM, g, o);
+    if (lane >= o) g = max(g, y);
+  }
+  const float pmg = __shfl_sync(FULLM, pm, g > 0 ? g - 1 : 0);
+  const bool surv = valid && (g == 0 || pmg > h);
+  const unsigned sm = __ballot_sync(FULLM, surv);
+  const int ns = __popc(sm);
+  if (surv) W.sv[__popc(sm & lt)] = c;
+  __syncwarp();
+  // 3. old entries: killed by a survivor? old alive ones to their merged slot
+  int na = 0;
+  for (int j0 = 0; j0 < m; j0 += 32) {
+    const int j = j0 + lane;
+    bool alive = false;
+    float2 o = make_float2(0.0f, 0.0f);
+    if (j < m) {
+      o = st[j];
+      int lo = 0, hi = ns;   // first survivor with cost >= o.x
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__int_as_float(W.sv[mid].y) < o.x) lo = mid + 1; else hi = mid;
+      }
+      const bool dead = lo > 0 && __int_as_float(W.sv[lo - 1].z) <= o.y;
+      alive = !dead;
+      if (dead) {
+        const int oid = si[j];
+        if (lstate[oid] == L_OPEN) {
+          lstate[oid] = L_DEAD;
+          ++my_kill;
+        }
+      }
+    }
+    const unsigned am = __ballot_sync(FULLM, alive);
+    if (lane == 0) {
+      W.pre[j0 >> 5] = na;
+      W.mask[j0 >> 5] = am;
+    }
+    if (alive) {
+      int lo = 0, hi = ns;   // survivors with key < o
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (key_less(__int_as_float(W.sv[mid].y), __int_as_float(W.sv[mid].z), o.x, o.y)) lo = mid + 1; else hi = mid;
+      }
+      const int pos = na + __popc(am & lt) + lo;
+      if (pos < C.K) {
+        nst[pos] = o;
+        nsi[pos] = si[j];
+      }
+    }
+    na += __popc(am);
+  }
+  __syncwarp();
+  // 4. survivors: labels, pending list, merged slot
+  int lbase = 0, pbase = 0;
+  if (lane == 0 && ns > 0) {
+    lbase = atomicAdd(&S->nlabels, ns);
+    pbase = atomicAdd(&S->psize, ns);
+  }
+  lbase = __shfl_sync(FULLM, lbase, 0);
+  pbase = __shfl_sync(FULLM, pbase, 0);
+  if (lbase + ns > C.L) {
+    if (lane == 0) atomicOr(&S->overflow, OVF_LABELS);
+  } else if (lane < ns) {
+    const int4 q = W.sv[lane];
+    const float qc = __int_as_float(q.y), qh = __int_as_float(q.z);
+    const int id = lbase + lane;
+    DCHECK(id < C.L && pbase + lane < C.L && q.w >= 0 && q.w < C.L);
+    labels[id] = make_int4(x, q.w, q.y, q.z);
+    lstate[id] = L_OPEN;
+    pend[pbase + lane] = id;
+    int lo = 0, hi = m;   // first old entry with key > q
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const float2 om = st[mid];
+      if (key_less(qc, qh, om.x, om.y)) hi = mid; else lo = mid + 1;
+    }
+    const int before = (lo == m) ? na : W.pre[lo >> 5] + __popc(W.mask[lo >> 5] & ((1u << (lo & 31)) - 1u));
+    const int pos = lane + before;
+    if (pos < C.K) {
+      nst[pos] = make_float2(qc, qh);
+      nsi[pos] = id;
+    }
+  }
+  if (lane == 0) {
+    const int newm = na + ns;
+    if (newm > C.K) atomicOr(&S->overflow, OVF_STAIR);
+    sn[x] = min(newm, C.K) | ((par ^ 1) << 30);
+    my_ins += (unsigned long long)ns;
+  }
+  __syncwarp();
 }
 
 template <bool TRACE, typename Team>
@@ -565,6 +722,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
   int32_t* touched = A.touched + (size_t)slot * C.n;
   int32_t* tsmall = A.tsmall + (size_t)slot * C.n;
   int32_t* tbig = A.tbig + (size_t)slot * C.n;
+  int32_t* tmid = A.tmid + (size_t)slot * C.n;
   int32_t* G = A.G + (size_t)slot * C.L;
   int32_t* pend = A.pend + (size_t)slot * C.L;
   int32_t* pend2 = A.pend2 + (size_t)slot * C.L;
@@ -649,9 +807,11 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
     if (leader) {
       S->need = 0;
       S->relax = 0; S->bpass = 0; S->tcount = 0; S->ssum = 0; S->inserted = 0; S->killed = 0;
-      S->ncand = 0; S->ntouched = 0; S->calloc = 0; S->nsmall = 0; S->nbig = 0; S->snext = 0;
+      S->ncand = 0; S->ntouched = 0; S->calloc = 0; S->nsmall = 0; S->nbig = 0; S->snext = 0; S->bnext = 0;
+      S->nmid = 0; S->mnext = 0;
     }
     team.sync();
+    PHASE_MARK(0);
     // ---- a7 expand (A3.6-A3.11): warp per plan of G_i, 32 edges per step ----
     {
       unsigned long long my_relax = 0, my_bpass = 0, my_t = 0, my_ss = 0;
@@ -692,12 +852,26 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
                 // candidate cannot survive RemoveDominated (transitivity).  With
                 // the staircase sorted, only the last entry of cost < qc matters.
                 const float2* st = sch + stair_base(snx, x, n, C.K);
-                int lo = 0, hi = m;   // first index with cost >= qc
+                // first index with cost >= qc; the wavefront's candidates are
+                // usually costlier than the whole staircase, so its last entry
+                // is checked first (one load instead of a log2(m)-deep search)
+                int lo = 0, hi = m;
+                float2 prev = make_float2(0.0f, __int_as_float(0x7f800000));
+                if (m > 0) {
+                  const float2 last = st[m - 1];
+                  if (last.x < qc) {
+                    lo = m;
+                    prev = last;
+                  } else {
+                    hi = m - 1;
+                  }
+                }
                 while (lo < hi) {
                   const int mid = (lo + hi) >> 1;
                   if (st[mid].x < qc) lo = mid + 1; else hi = mid;
                 }
-                const bool dom = lo > 0 && st[lo - 1].y <= qh;
+                if (lo > 0 && lo < m) prev = st[lo - 1];
+                const bool dom = lo > 0 && prev.y <= qh;
                 emit = !dom;
               }
             }
@@ -735,6 +909,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
     team.sync();
     if (vld(S->overflow)) break;
     const int nt = vld(S->ntouched);
+    PHASE_MARK(1);
     const int ncand = vld(S->ncand);
     // ---- group candidates by destination: contiguous range per touched node ----
     for (int t = tid; t < nt; t += nthr) {
@@ -742,10 +917,16 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
       const int kc = ccnt[x];
       coff[x] = atomicAdd(&S->calloc, kc);
       const int m = sn[x] & kStairCountMask;
-      if ((kc > kMrgCap || m > kMrgCap) && kc <= kBigC && m <= kBigM) tbig[atomicAdd(&S->nbig, 1)] = x;
+      if ((kc > kMrgCap || m > kMrgCap) && kc <= 32 && m <= kBigM) tmid[atomicAdd(&S->nmid, 1)] = x;
+      else if ((kc > kMrgCap || m > kMrgCap) && kc <= kBigC && m <= kBigM) tbig[atomicAdd(&S->nbig, 1)] = x;
       else tsmall[atomicAdd(&S->nsmall, 1)] = x;
+      if (MPAP_DEBUG_CHECKS && A.nq == 1 && wave < kPhaseWaves) {
+        atomicMax(&g_phase_stat[wave][2], kc);
+        atomicMax(&g_phase_stat[wave][3], m);
+      }
     }
     team.sync();
+    PHASE_MARK(2);
     for (int k = tid; k < ncand; k += nthr) {
       const int4 cq = cand[k];
       const int pos = atomicAdd(&coff[cq.x], 1);
@@ -753,6 +934,11 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
       cs[pos] = cq;
     }
     team.sync();
+    PHASE_MARK(3);
+    if (MPAP_DEBUG_CHECKS && leader && A.nq == 1 && wave < kPhaseWaves) {
+      g_phase_stat[wave][0] = vld(S->nbig);
+      g_phase_stat[wave][1] = vld(S->nsmall);
+    }
     // ---- a8 RemoveDominated + insert (A3.10-A3.15): warp per touched node ----
     {
       // per-warp shared-memory staging of the node's candidates (sorted copy,
@@ -766,8 +952,29 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
       unsigned long long my_ins = 0, my_kill = 0;
       // large nodes: one CTA each (uniform per CTA: __syncthreads inside)
       const int nbig = vld(S->nbig), nsmall = vld(S->nsmall);
-      for (int b = team.cta(); b < nbig; b += team.ncta())
-        cta_merge(S, C, tbig[b], n, cs, coff, ccnt, sch, sid, sn, labels, lstate, pend, my_ins, my_kill);
+      if (nbig > 0) {   // pulled from a counter by whole CTAs (large nodes vary a lot in size)
+        __shared__ int s_big;
+        for (;;) {
+          if (threadIdx.x == 0) s_big = atomicAdd(&S->bnext, 1);
+          __syncthreads();
+          const int b = s_big;
+          __syncthreads();
+          if (b >= nbig) break;
+          cta_merge(S, C, tbig[b], n, cs, coff, ccnt, sch, sid, sn, labels, lstate, pend, my_ins, my_kill);
+        }
+      }
+      // mid nodes (<= 32 candidates, large staircase): one warp each, with a
+      // slice of the CTA's (now free) dynamic shared memory
+      {
+        const int nmid = vld(S->nmid);
+        for (;;) {
+          int t = 0;
+          if (lane == 0) t = atomicAdd(&S->mnext, 1);
+          t = __shfl_sync(FULLM, t, 0);
+          if (t >= nmid) break;
+          warp_mid_merge(S, C, tmid[t], n, cs, coff, ccnt, sch, sid, sn, labels, lstate, pend, my_ins, my_kill);
+        }
+      }
       // small nodes: one warp each, pulled from a counter (warps of CTAs busy
       // with large nodes join late)
       for (;;) {
@@ -930,6 +1137,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
       if (my_ins) atomicAdd(&S->inserted, my_ins);
     }
     team.sync();
+    PHASE_MARK(4);
     if (vld(S->overflow)) break;
     // reset per-node candidate counters of touched nodes
     for (int t = tid; t < nt; t += nthr) ccnt[touched[t]] = 0;
@@ -953,11 +1161,13 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
       S->gsize = 0; S->nsize = 0; S->goal_in_g = 0; S->minb = LLONG_MAX;
     }
     team.sync();
+    PHASE_MARK(5);
     // ---- a6 G_{i+1} (A3.18), with the exact empty-group skip (R24) ----
     const int np = vld(S->psize);
     long long inext = i_cur + 1;
     partition(team, A, S, pend, np, G, pend2, inext, labels, lstate, goal);
     team.sync();
+    PHASE_MARK(6);
     if (vld(S->gsize) == 0 && vld(S->nsize) > 0) {
       inext = vld(S->minb);
       const int n2 = vld(S->nsize);
@@ -1175,6 +1385,7 @@ size_t carve(SearchArgs* A, const SlotCaps& c, int nslots, char* base) {
   p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->touched = (int32_t*)p;
   p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->tsmall = (int32_t*)p;
   p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->tbig = (int32_t*)p;
+  p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->tmid = (int32_t*)p;
   p = take(sizeof(int32_t) * (size_t)c.n);              if (A) A->stamp = (int32_t*)p;
   p = take((size_t)c.n);                                if (A) A->goal = (uint8_t*)p;
   p = take(sizeof(int4) * (size_t)c.C);                 if (A) A->cand = (int4*)p;
@@ -1462,6 +1673,20 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
   }
   if (d_waves) CKS(cudaFreeAsync(d_waves, st));
   if (mem == MPAP_MEM_DEVICE) CKS(cudaStreamSynchronize(st));
+  if (MPAP_DEBUG_CHECKS && nq == 1 && getenv("MPAP_PHASE_LOG")) {
+    static unsigned long long ph[kPhaseWaves][8];
+    static int pst[kPhaseWaves][4];
+    CKS(cudaMemcpyFromSymbol(ph, g_phase, sizeof(ph)));
+    CKS(cudaMemcpyFromSymbol(pst, g_phase_stat, sizeof(pst)));
+    const int nw = std::min(kPhaseWaves, (int)results[0].waves);
+    for (int w = 0; w < nw; ++w)
+      fprintf(stderr, "[phase] wave %d us expand %.1f group %.1f scatter %.1f merge %.1f retire %.1f partition %.1f "
+              "| nbig %d nsmall %d max_kc %d max_m %d\n", w, (ph[w][1] - ph[w][0]) * 1e-3, (ph[w][2] - ph[w][1]) * 1e-3,
+              (ph[w][3] - ph[w][2]) * 1e-3, (ph[w][4] - ph[w][3]) * 1e-3, (ph[w][5] - ph[w][4]) * 1e-3,
+              (ph[w][6] - ph[w][5]) * 1e-3, pst[w][0], pst[w][1], pst[w][2], pst[w][3]);
+    std::memset(pst, 0, sizeof(pst));
+    CKS(cudaMemcpyToSymbol(g_phase_stat, pst, sizeof(pst)));
+  }
   if (MPAP_DEBUG_CHECKS) {
     unsigned long long fails = 0;
     CKS(cudaMemcpyFromSymbol(&fails, g_dcheck_fail, sizeof(fails)));
