@@ -61,7 +61,8 @@ constexpr int kMrgCap = 48;           // merge: a node's candidates / staircase 
 constexpr int kBigC = 2048;           // CTA merge of a large node: candidates (power of two, 4 per thread)
 constexpr int kBigM = 4096;           // ... and staircase entries (8 per thread); larger nodes take the warp path
 enum : uint8_t { L_OPEN = 0, L_CLOSED = 1, L_DEAD = 2 };
-enum { OVF_LABELS = 1, OVF_CAND = 2, OVF_STAIR = 4 };
+enum { OVF_LABELS = 1, OVF_CAND = 2, OVF_STAIR = 4, OVF_RING = 8 };
+constexpr int kRingMax = 8;           // bucket ring of ceil(1/lambda) + 3 lists; more -> pending-list scan
 constexpr int kRetryBase = 100;       // result.status = kRetryBase + OVF_* mask
 
 struct SlotCaps {
@@ -69,6 +70,7 @@ struct SlotCaps {
   int K;     // staircase slots per node
   int L;     // label pool capacity
   int C;     // candidates per wave
+  int R;     // bucket ring size (0: one pending list re-partitioned every wave)
 };
 
 struct SearchArgs {
@@ -104,6 +106,7 @@ struct SearchArgs {
   int32_t* G;
   int32_t* pend;
   int32_t* pend2;
+  int32_t* ring;       // [R][L] open labels by cost bucket (caps.R > 0)
   int32_t* stamp;
   uint8_t* goal;
   // outputs
@@ -126,6 +129,7 @@ struct Ctl {
   int nsmall, nbig, snext, bnext;   // merge work lists (small: warp per node, pulled from snext; big: CTA per
                                     // node, pulled from bnext)
   int nmid, mnext;                  // mid: warp per node (binary searches), pulled from mnext
+  int rcount[kRingMax];             // bucket ring list lengths
   long long i, minb;
   unsigned long long relax, bpass, tcount, ssum, inserted, killed;
   unsigned long long relax_total, inserted_total;
@@ -270,6 +274,59 @@ __device__ __forceinline__ bool key_less(float ac, float ah, float bc, float bh)
   return ac < bc || (ac == bc && ah > bh);
 }
 
+// Where a new open plan goes (A3.11 "P_open <- P_open + q"): the pending list
+// re-partitioned every wave, or -- the paper's cost-thresholded buckets
+// -- the ring list of its group index b = max(b(cost), i + 1), so the
+// next group is one list (A3.18, reading R3).  b <= i + ceil(1/lambda) + 1
+// since an edge costs less than r_n (f32 rounding included); a plan beyond
+// the ring (not expected) flags OVF_RING and the query reruns on the list.
+struct Pusher {
+  int32_t* pend;
+  int32_t* ring;
+  int R, L;
+  double T;
+  long long i;
+};
+
+// Full warp; the lanes with v push plan `id` of cost c.
+__device__ void push_open(Ctl* S, const Pusher& P, bool v, int id, float c) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lane_lt();
+  if (P.R == 0) {
+    const unsigned m = __ballot_sync(FULLM, v);
+    if (!m) return;
+    const int lead = __ffs(m) - 1;
+    int base = 0;
+    if (lane == lead) base = atomicAdd(&S->psize, __popc(m));
+    base = __shfl_sync(FULLM, base, lead);
+    if (v) P.pend[base + __popc(m & lt)] = id;
+    return;
+  }
+  int slot = -1;
+  if (v) {
+    long long b = bucket_of(c, P.T);
+    if (b < P.i + 1) b = P.i + 1;
+    if (b > P.i + P.R) {
+      atomicOr(&S->overflow, OVF_RING);
+      v = false;
+    } else {
+      slot = (int)(b % P.R);
+    }
+  }
+  unsigned pending = __ballot_sync(FULLM, v);
+  while (pending) {   // warp-aggregated append per ring list
+    const int lead = __ffs(pending) - 1;
+    const int ls = __shfl_sync(FULLM, slot, lead);
+    const bool mine = v && slot == ls;
+    const unsigned m = __ballot_sync(FULLM, mine);
+    int base = 0;
+    if (lane == lead) base = atomicAdd(&S->rcount[ls], __popc(m));
+    base = __shfl_sync(FULLM, base, lead);
+    if (mine) P.ring[(size_t)ls * P.L + base + __popc(m & lt)] = id;
+    pending &= ~m;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // CTA-cooperative merge of one large node (RemoveDominated + insert, A3.15,
 // P:193) -- the same set result as the warp path, in O(k log k):
@@ -375,7 +432,8 @@ __device__ __forceinline__ int block_excl_max(int v, int* scr) {
 
 __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* cs, const int32_t* coff,
                           const int32_t* ccnt, float2* sch, int32_t* sid, int32_t* sn, int4* labels,
-                          uint8_t* lstate, int32_t* pend, unsigned long long& my_ins, unsigned long long& my_kill) {
+                          uint8_t* lstate, const Pusher& PU, unsigned long long& my_ins,
+                          unsigned long long& my_kill) {
   extern __shared__ __align__(16) unsigned char s_dyn[];
   BigSmem& B = *reinterpret_cast<BigSmem*>(s_dyn);
   const int tid = threadIdx.x, bd = blockDim.x;
@@ -494,7 +552,6 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
   if (tid == 0) {
     B.ap[m] = na;
     B.bc[0] = atomicAdd(&S->nlabels, ns);
-    B.bc[1] = atomicAdd(&S->psize, ns);
   }
   __syncthreads();
   // 4. merged staircase in the other buffer; survivors get labels
@@ -515,18 +572,21 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
       }
     }
   }
-  const int lbase = B.bc[0], pbase = B.bc[1];
+  const int lbase = B.bc[0];
   if (lbase + ns > C.L) {
     if (tid == 0) atomicOr(&S->overflow, OVF_LABELS);
   } else {
-    for (int q = tid; q < ns; q += bd) {
-      const int4 c = B.c[q];
+    for (int q0 = 0; q0 < ns; q0 += bd) {   // whole warps (push_open is warp-collective)
+      const int q = q0 + tid;
+      const bool v = q < ns;
+      const int4 c = v ? B.c[q] : make_int4(0, 0, 0, 0);
       const float qc = __int_as_float(c.y), qh = __int_as_float(c.z);
       const int id = lbase + q;
-      DCHECK(id < C.L && pbase + q < C.L && c.w >= 0 && c.w < C.L);
+      push_open(S, PU, v, id, qc);
+      if (!v) continue;
+      DCHECK(id < C.L && c.w >= 0 && c.w < C.L);
       labels[id] = make_int4(x, c.w, c.y, c.z);
       lstate[id] = L_OPEN;
-      pend[pbase + q] = id;
       int lo = 0, hi = m;   // first old entry with key > q
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
@@ -569,7 +629,7 @@ __device__ __forceinline__ int4 shfl_xor4(const int4& v, int j) {
 
 __device__ void warp_mid_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* cs, const int32_t* coff,
                                const int32_t* ccnt, float2* sch, int32_t* sid, int32_t* sn, int4* labels,
-                               uint8_t* lstate, int32_t* pend, unsigned long long& my_ins,
+                               uint8_t* lstate, const Pusher& PU, unsigned long long& my_ins,
                                unsigned long long& my_kill) {
   extern __shared__ __align__(16) unsigned char s_dyn[];
   MidSmem& W = reinterpret_cast<MidSmem*>(s_dyn)[threadIdx.x >> 5];
@@ -657,23 +717,24 @@ __device__ void warp_mid_merge(Ctl* S, const SlotCaps& C, int x, int n, const in
   }
   __syncwarp();
   // 4. survivors: labels, pending list, merged slot
-  int lbase = 0, pbase = 0;
-  if (lane == 0 && ns > 0) {
-    lbase = atomicAdd(&S->nlabels, ns);
-    pbase = atomicAdd(&S->psize, ns);
-  }
+  int lbase = 0;
+  if (lane == 0 && ns > 0) lbase = atomicAdd(&S->nlabels, ns);
   lbase = __shfl_sync(FULLM, lbase, 0);
-  pbase = __shfl_sync(FULLM, pbase, 0);
   if (lbase + ns > C.L) {
     if (lane == 0) atomicOr(&S->overflow, OVF_LABELS);
-  } else if (lane < ns) {
+  } else {
     const int4 q = W.sv[lane];
     const float qc = __int_as_float(q.y), qh = __int_as_float(q.z);
     const int id = lbase + lane;
-    DCHECK(id < C.L && pbase + lane < C.L && q.w >= 0 && q.w < C.L);
+    push_open(S, PU, lane < ns, id, qc);
+  }
+  if (lbase + ns <= C.L && lane < ns) {
+    const int4 q = W.sv[lane];
+    const float qc = __int_as_float(q.y), qh = __int_as_float(q.z);
+    const int id = lbase + lane;
+    DCHECK(id < C.L && q.w >= 0 && q.w < C.L);
     labels[id] = make_int4(x, q.w, q.y, q.z);
     lstate[id] = L_OPEN;
-    pend[pbase + lane] = id;
     int lo = 0, hi = m;   // first old entry with key > q
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
@@ -726,6 +787,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
   int32_t* G = A.G + (size_t)slot * C.L;
   int32_t* pend = A.pend + (size_t)slot * C.L;
   int32_t* pend2 = A.pend2 + (size_t)slot * C.L;
+  int32_t* ring = C.R ? A.ring + (size_t)slot * C.R * C.L : nullptr;
   int32_t* stamp = A.stamp + (size_t)slot * C.n;
   uint8_t* goal = A.goal + (size_t)slot * C.n;
   const double beta = Q.beta;
@@ -739,6 +801,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
       S->gsize = 1; S->psize = 0; S->nsize = 0; S->ncand = 0; S->ntouched = 0; S->nlabels = 1; S->calloc = 0;
       S->goal_in_g = 0; S->overflow = 0; S->any_goal = 0; S->i = 0; S->minb = LLONG_MAX;
       S->relax_total = 0; S->inserted_total = 0; S->waves = 0; S->suspended = 0; S->pswap = 0; S->need = 0;
+      for (int r = 0; r < kRingMax; ++r) S->rcount[r] = 0;
     }
     team.sync();
     bool mygoal = false;
@@ -950,6 +1013,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
       __shared__ int32_t s_sid[kST / 32][kMrgCap];
       const int wl = threadIdx.x >> 5;
       unsigned long long my_ins = 0, my_kill = 0;
+      const Pusher PU{pend, ring, C.R, C.L, A.T, i_cur};
       // large nodes: one CTA each (uniform per CTA: __syncthreads inside)
       const int nbig = vld(S->nbig), nsmall = vld(S->nsmall);
       if (nbig > 0) {   // pulled from a counter by whole CTAs (large nodes vary a lot in size)
@@ -960,7 +1024,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
           const int b = s_big;
           __syncthreads();
           if (b >= nbig) break;
-          cta_merge(S, C, tbig[b], n, cs, coff, ccnt, sch, sid, sn, labels, lstate, pend, my_ins, my_kill);
+          cta_merge(S, C, tbig[b], n, cs, coff, ccnt, sch, sid, sn, labels, lstate, PU, my_ins, my_kill);
         }
       }
       // mid nodes (<= 32 candidates, large staircase): one warp each, with a
@@ -972,7 +1036,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
           if (lane == 0) t = atomicAdd(&S->mnext, 1);
           t = __shfl_sync(FULLM, t, 0);
           if (t >= nmid) break;
-          warp_mid_merge(S, C, tmid[t], n, cs, coff, ccnt, sch, sid, sn, labels, lstate, pend, my_ins, my_kill);
+          warp_mid_merge(S, C, tmid[t], n, cs, coff, ccnt, sch, sid, sn, labels, lstate, PU, my_ins, my_kill);
         }
       }
       // small nodes: one warp each, pulled from a counter (warps of CTAs busy
@@ -1096,23 +1160,21 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
           const int qq = q0 + lane;
           const bool v = qq < ns;
           const unsigned vm = __ballot_sync(FULLM, v);
-          int lbase = 0, pbase = 0;
-          if (lane == 0) {
-            lbase = atomicAdd(&S->nlabels, __popc(vm));
-            pbase = atomicAdd(&S->psize, __popc(vm));
-          }
+          int lbase = 0;
+          if (lane == 0) lbase = atomicAdd(&S->nlabels, __popc(vm));
           lbase = __shfl_sync(FULLM, lbase, 0);
-          pbase = __shfl_sync(FULLM, pbase, 0);
           if (lbase + __popc(vm) > C.L) {
             if (lane == 0) atomicOr(&S->overflow, OVF_LABELS);
-          } else if (v) {
+          } else {
+            push_open(S, PU, v, lbase + lane, v ? __int_as_float(sv[qq].y) : 0.0f);
+          }
+          if (lbase + __popc(vm) <= C.L && v) {
             const int4 cq = sv[qq];
             const float qc = __int_as_float(cq.y), qh = __int_as_float(cq.z);
             const int id = lbase + lane;
-            DCHECK(id < C.L && pbase + lane < C.L && cq.w >= 0 && cq.w < C.L);
+            DCHECK(id < C.L && cq.w >= 0 && cq.w < C.L);
             labels[id] = make_int4(x, cq.w, cq.y, cq.z);
             lstate[id] = L_OPEN;
-            pend[pbase + lane] = id;
             int before = 0;   // alive old entries with key <= (qc, qh)
             for (int j = 0; j < m; ++j) {
               const float2 o = st[j];
@@ -1163,6 +1225,27 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
     team.sync();
     PHASE_MARK(5);
     // ---- a6 G_{i+1} (A3.18), with the exact empty-group skip (R24) ----
+    if (C.R) {
+      // bucket ring: G_j = the live plans of list j (every plan of list j has
+      // cost <= j T, every later plan more); empty lists are skipped
+      long long j = i_cur + 1;
+      for (;;) {
+        const int r = (int)(j % C.R);
+        const int cnt = vld(S->rcount[r]);
+        partition(team, A, S, ring + (size_t)r * C.L, cnt, G, G, LLONG_MAX / 4, labels, lstate, goal);
+        team.sync();
+        const bool done = vld(S->gsize) > 0 || j >= i_cur + C.R;
+        team.sync();
+        if (leader) S->rcount[r] = 0;
+        if (done) break;
+        ++j;
+      }
+      if (leader) S->i = j;
+      team.sync();
+      PHASE_MARK(6);
+      ++wave;
+      continue;
+    }
     const int np = vld(S->psize);
     long long inext = i_cur + 1;
     partition(team, A, S, pend, np, G, pend2, inext, labels, lstate, goal);
@@ -1304,7 +1387,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
 
 // Batched queries: one CTA per query at a time, queries pulled from a counter.
 template <bool TRACE>
-__global__ void __launch_bounds__(kST) k_search(SearchArgs A) {
+__global__ void __launch_bounds__(kST, 2) k_search(SearchArgs A) {   // two CTAs (queries) per SM
   __shared__ Ctl S;
   __shared__ int s_q;
   const CtaTeam team;
@@ -1393,6 +1476,7 @@ size_t carve(SearchArgs* A, const SlotCaps& c, int nslots, char* base) {
   p = take(sizeof(int32_t) * (size_t)c.L);              if (A) A->G = (int32_t*)p;
   p = take(sizeof(int32_t) * (size_t)c.L);              if (A) A->pend = (int32_t*)p;
   p = take(sizeof(int32_t) * (size_t)c.L);              if (A) A->pend2 = (int32_t*)p;
+  p = take(sizeof(int32_t) * (size_t)c.L * c.R);        if (A) A->ring = (int32_t*)p;
   return off;
 }
 }  // namespace
@@ -1461,6 +1545,11 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
   caps.K = std::max(64, rm->hint_K);
   caps.L = std::max(std::max(1 << 17, 64 * rm->n_max), rm->hint_L);
   caps.C = std::max(caps.L, rm->hint_C);
+  {  // bucket ring: ceil(1/lambda) + 3 lists cover every new plan's group index
+    const double inv = std::ceil(1.0 / lambda);
+    caps.R = (!rm->lazy && inv + 3.0 <= (double)kRingMax && getenv("MPAP_SEARCH_NO_RING") == nullptr)
+                 ? (int)inv + 3 : 0;
+  }
 
   // device copies of the queries and outputs
   QueryDesc* d_q = nullptr;
@@ -1641,6 +1730,7 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
       }
     }
     if (mask & OVF_STAIR) caps.K *= 2;
+    if (mask & OVF_RING) caps.R = 0;   // a plan beyond the ring: rerun on the pending list
     if (mask & OVF_LABELS) caps.L *= 2;
     if (mask & OVF_CAND) caps.C *= 2;
     rm->hint_K = std::max(rm->hint_K, caps.K);   // later searches on this roadmap start there

@@ -4,7 +4,7 @@ Calls only oracle/ (and the synth/ input generators); nothing here touches
 the CUDA path.  The GPU parity tests compare libmpap.so against these stored
 oracle outputs, because the full-size oracle build takes minutes of CPU.
 
-    python tests/golden/make_golden.py [c3] [c5] [c4] [c5_bench] [c5_all]
+    python tests/golden/make_golden.py [c3] [c5] [c4] [c5_bench] [c5_all] [c4_tight]
 
 c5_bench: the bench's rank-0 shard (C5 environments 0..63) at four bounds
 each -- the 64-query batch the bench times (beta = configs/c5.json betas[1])
@@ -105,6 +105,14 @@ def main(argv):
             if k % 16 == 15:   # checkpoint (the full run takes over an hour on 8 cores)
                 json.dump({"beta": beta, "envs": envs}, open(os.path.join(HERE, "c5_all.json"), "w"))
         json.dump({"beta": beta, "envs": envs}, open(os.path.join(HERE, "c5_all.json"), "w"))
+    if "c4_tight" in which:
+        # C4 at the tightest bound of its sweep (1.02 beta_min): 105 waves, 2e8
+        # relaxations, staircases of thousands of plans -- the large-node merge
+        # paths of the search.  The literal oracle search takes ~35 min.
+        cfg = load_config("c4")
+        prob = make_problem(cfg)
+        res = run_one(prob, [float(cfg["betas"][-1])], procs)
+        json.dump(res, open(os.path.join(HERE, "c4_tight.json"), "w"), indent=1)
     if "c4" in which:
         cfg = load_config("c4")
         prob = make_problem(cfg)

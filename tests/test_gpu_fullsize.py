@@ -186,3 +186,25 @@ def test_full_csr_digests_c5_golden_envs(mp):
     for e, gd in enumerate(gold):
         assert _digests(mp, rm, e) == gd["digests"], e
     rm.free()
+
+
+def test_c4_tightest_bound_single_query(mp):
+    """C4 at 1.02 beta_min (the tightest bound of BASELINE.json configs[3]'s
+    sweep): 105 waves, 2.1e8 relaxations, staircases of thousands of plans,
+    so the CTA-cooperative and warp binary-search merges of large nodes run;
+    whole result and every per-wave counter vs the oracle's stored run."""
+    path = os.path.join(GOLDEN, "c4_tight.json")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/c4_tight.json not generated")
+    gold = json.load(open(path))
+    prob = make_problem(load_config("c4"))
+    rm = mp.pb.build_problem(prob)
+    assert _digests(mp, rm, 0) == gold["digests"]
+    for s in gold["searches"]:
+        g = mp.pb.search_problem(rm, prob, float(s["beta"]), trace_waves=4096)
+        assert g["status"] == s["status"] and g["waves"] == s["waves"]
+        assert g["relaxations"] == s["relaxations"] and g["labels_inserted"] == s["labels_inserted"]
+        assert g["wave_counters"].tolist() == s["wave_counters"]
+        assert g["path"].tolist() == s["path"]
+        assert _hex(g["cost"]) == s["cost"] and _hex(g["h"]) == s["h"] and _hex(g["h_peak"]) == s["h_peak"]
+    rm.free()
