@@ -329,8 +329,8 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_near(const double* __restri
           // sixteenths of each quarter that is still possible.
           auto possible_on = [&](int lvl, int jj) -> bool {
             const double ta = s_near[lvl][jj][0], tb = s_near[lvl][jj][1];
-            const double tq = fmin(fmax(tv, ta), tb);
-            const double g2 = fmax(dp2 - tq * as + tq * tq * ss * 0.25, 0.0);
+            const double tq = dmin(dmax(tv, ta), tb);   // finite operands: no NaN handling needed
+            const double g2 = dmax(dp2 - tq * as + tq * tq * ss * 0.25, 0.0);
             const double L = ta + ru * (12.0 * g2 * s_near[lvl][jj][3] + dv2 * s_near[lvl][jj][2]);
             return L * (1.0 - 1e-9) < r;
           };
