@@ -17,7 +17,7 @@ PKG = os.path.join(ROOT, "paper_1705_02408_b200")
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libmpap.so")
-SOURCES = ["capi.cu", "build_kernels.cu", "search_kernels.cu", "mc_kernels.cu", "peak_kernels.cu"]
+SOURCES = ["capi.cu", "build_kernels.cu", "search_kernels.cu", "mc_kernels.cu", "peak_kernels.cu", "rowshard.cu"]
 HEADERS = [os.path.join(CSRC, "mpap_internal.cuh"), os.path.join(CSRC, "traj.cuh"), os.path.join(INCLUDE, "mpap.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

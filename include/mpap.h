@@ -262,6 +262,46 @@ mpap_status mpap_search_batch_trace(const mpap_roadmap *rm, int32_t n_queries, c
                                     mpap_wave *waves, int32_t waves_capacity, void *cuda_stream);
 
 /*
+ * Device-resident row blocks of a row-sharded build:
+ * rank g builds rows [row_begin, row_end) with mpap_build_roadmap_rows, hands
+ * its block to one NCCL all-gather as device arrays, and every rank assembles
+ * the gathered blocks into a search roadmap on the device -- no host round
+ * trip of the CSR.
+ *
+ * mpap_roadmap_block_device -- the block of `rm` (built by
+ * mpap_build_roadmap_rows, one environment, not lazy):
+ *   counts    device, [row_end - row_begin] int32: entries per row, in row order.
+ *   edges     device, [capacity] 16-byte records {dst | coll << 31, f32 w, s, c}
+ *             (the roadmap's own layout), the block's rows in order.
+ *   capacity  records `edges` can hold (>= 0).
+ *   nnz       out (host): the block's record count.
+ * Errors: INVALID_ARGUMENT (NULL, not a one-environment eager build, another
+ * device), BUFFER_TOO_SMALL (nnz > capacity: nothing written, *nnz set),
+ * CUDA.  Synchronises `cuda_stream`.
+ *
+ * mpap_roadmap_assemble_device -- the device counterpart of
+ * mpap_roadmap_import for n_blocks gathered blocks:
+ *   n, pos_dim, positions  as mpap_roadmap_import (host positions).
+ *   row_begin     host, [n_blocks + 1]: block b holds rows [row_begin[b],
+ *                 row_begin[b + 1]); row_begin[0] = 0, row_begin[n_blocks] = n.
+ *   counts        device, [n_blocks][counts_stride] int32 (block b's row
+ *                 counts first in its slot; counts_stride >= every block's rows).
+ *   edges         device, [n_blocks][edges_stride] 16-byte records (block b's
+ *                 records first in its slot).
+ *   r             r_n (> 0, finite).
+ * The CSR is the concatenation of the blocks in row order (one scan of the
+ * counts, one copy kernel).  Errors: INVALID_ARGUMENT (blocks not tiling [0,
+ * n), a block wider than its slot, a dst out of range, bad positions / r),
+ * OUT_OF_MEMORY, CUDA.  Synchronises `cuda_stream`; the inputs stay owned by
+ * the caller. */
+mpap_status mpap_roadmap_block_device(const mpap_roadmap *rm, int32_t *counts, void *edges, int64_t capacity,
+                                      int64_t *nnz, void *cuda_stream);
+mpap_status mpap_roadmap_assemble_device(int32_t n, int32_t pos_dim, const double *positions, int32_t n_blocks,
+                                         const int32_t *row_begin, const int32_t *counts, int32_t counts_stride,
+                                         const void *edges, int64_t edges_stride, double r, void *cuda_stream,
+                                         mpap_roadmap **out);
+
+/*
  * mpap_roadmap_import -- wrap a precomputed single-environment CSR (P:337:
  * neighbours and edge data "precomputed offline") so mpap_search can run on it.
  *   n, pos_dim      node count (>= 1) and position dimension (2 or 3).

@@ -47,7 +47,8 @@ EXPORTED_SYMBOLS = [
     "mpap_roadmap_work", "mpap_search_ex", "mpap_search_batch_ex", "mpap_roadmap_export_peaks",
     "mpap_roadmap_set_peaks", "mpap_roadmap_update", "mpap_mc_verify", "mpap_mc_verify_batch",
     "mpap_roadmap_rows_evaluated", "mpap_build_roadmap_rows", "mpap_prof_fp64_peak",
-    "mpap_search_batch_trace", "mpap_search_launches",
+    "mpap_search_batch_trace", "mpap_search_launches", "mpap_roadmap_block_device",
+    "mpap_roadmap_assemble_device",
 ]
 
 
@@ -152,6 +153,10 @@ _lib.mpap_prof_enable.restype = None
 _lib.mpap_prof_reset.restype = None
 _lib.mpap_prof_read.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
 _lib.mpap_prof_read.restype = C.c_int32
+if hasattr(_lib, "mpap_roadmap_block_device"):
+    _lib.mpap_roadmap_block_device.argtypes = [_vp, _vp, _vp, C.c_int64, C.POINTER(C.c_int64), _vp]
+    _lib.mpap_roadmap_assemble_device.argtypes = [C.c_int32, C.c_int32, _vp, C.c_int32, _i32p, _vp, C.c_int32, _vp,
+                                                  C.c_int64, C.c_double, _vp, C.POINTER(_vp)]
 if hasattr(_lib, "mpap_prof_fp64_peak"):
     _lib.mpap_prof_fp64_peak.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     _lib.mpap_prof_fp64_peak.restype = C.c_int
@@ -514,6 +519,36 @@ def mpap_prof_read(kernel: str) -> tuple:
     n = C.c_int64()
     _lib.mpap_prof_read(kernel.encode(), C.byref(ms), C.byref(n))
     return float(ms.value), int(n.value)
+
+
+def mpap_roadmap_block_device(rm: Roadmap, counts, edges, stream=None) -> int:
+    """Write rm's row block into CUDA tensors: counts int32 [rows], edges
+    int32 [capacity, 4] (16-byte records).  Returns the record count."""
+    nnz = C.c_int64()
+    st = _stream(stream)
+    s = _lib.mpap_roadmap_block_device(rm.handle, C.c_void_p(int(counts.data_ptr())),
+                                       C.c_void_p(int(edges.data_ptr())), int(edges.shape[0]), C.byref(nnz),
+                                       C.c_void_p(st) if st else None)
+    if s != MPAP_OK:
+        raise MpapError(s, "mpap_roadmap_block_device")
+    return int(nnz.value)
+
+
+def mpap_roadmap_assemble_device(positions, row_begin, counts, edges, r: float, stream=None) -> Roadmap:
+    """Assemble gathered row blocks (CUDA tensors counts int32 [B, rows_max],
+    edges int32 [B, nnz_max, 4]) into a search roadmap on the device."""
+    pos = np.ascontiguousarray(positions, dtype=np.float64)
+    rb = np.ascontiguousarray(row_begin, dtype=np.int32)
+    out = C.c_void_p()
+    st = _stream(stream)
+    s = _lib.mpap_roadmap_assemble_device(pos.shape[0], pos.shape[1], pos.ctypes.data, len(rb) - 1,
+                                          rb.ctypes.data_as(_i32p), C.c_void_p(int(counts.data_ptr())),
+                                          int(counts.shape[1]), C.c_void_p(int(edges.data_ptr())),
+                                          int(edges.shape[1]), float(r), C.c_void_p(st) if st else None,
+                                          C.byref(out))
+    if s != MPAP_OK:
+        raise MpapError(s, "mpap_roadmap_assemble_device")
+    return Roadmap(out.value)
 
 
 SEARCH_TEAMS = {"grid": 0, "cluster": 1, "cta": 2}

@@ -1472,6 +1472,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_affected(const double* __restri
     if (_e != cudaSuccess) return cuda_error(_e, #x);  \
   } while (0)
 
+// exclusive scan of int32 row counts -> int64 row offsets (k_scan), for the
+// other translation units (device-side row-block assembly)
+cudaError_t scan_row_counts(const int32_t* cnt, int64_t n, int64_t* row_ptr, cudaStream_t st) {
+  k_scan<<<1, 1024, 0, st>>>(cnt, n, row_ptr);
+  note_launch();
+  return cudaGetLastError();
+}
+
 namespace {
 template <int D, int DYN>
 cudaError_t launch_near(dim3 grid, cudaStream_t st, const mpap_roadmap* rm, const int32_t* d_n, int cap,

@@ -98,6 +98,9 @@ struct HostTimer {
   }
 };
 
+// exclusive scan of int32 row counts -> int64 row offsets (k_scan)
+cudaError_t scan_row_counts(const int32_t* cnt, int64_t n, int64_t* row_ptr, cudaStream_t st);
+
 // launch bookkeeping shared by the translation units (host side)
 void note_launch(int k = 1);
 // search launches per team kind (mpap_search_launches): 0 grid, 1 cluster, 2 CTA

@@ -131,3 +131,35 @@ def gather_csr_blocks(block: dict, world: int):
                     "w": r_[:, 1].copy().view(np.float32), "s": r_[:, 2].copy().view(np.float32),
                     "c": r_[:, 3].copy().view(np.float32)})
     return out
+
+
+def gather_csr_blocks_device(part, b: int, e: int, world: int, n: int, positions, r: float, stream=None):
+    """Device-resident row-sharded assembly: this rank's
+    block of rows [b, e) of `part` (a mpap_build_roadmap_rows roadmap) is
+    written into CUDA tensors (mpap_roadmap_block_device), all-gathered with
+    two NCCL all_gather_into_tensor calls (row counts, 16-byte records; slots
+    padded to the largest block, sizes agreed by one all-reduce MAX), and
+    assembled on the device (mpap_roadmap_assemble_device).  Returns the
+    search roadmap; the CSR never visits the host."""
+    import torch
+    import torch.distributed as dist
+    from . import mpap_roadmap_assemble_device, mpap_roadmap_block_device, mpap_roadmap_info
+    dev = torch.device("cuda", torch.cuda.current_device())
+    nnz = mpap_roadmap_info(part)["nnz"]
+    size = torch.tensor([e - b, nnz], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(size, op=dist.ReduceOp.MAX)
+    rows_max, nnz_max = int(size[0].item()), max(int(size[1].item()), 1)
+    counts = torch.zeros(rows_max, dtype=torch.int32, device=dev)
+    edges = torch.zeros((nnz_max, 4), dtype=torch.int32, device=dev)
+    mpap_roadmap_block_device(part, counts, edges, stream=stream)
+    if world > 1:
+        gc = torch.empty(world * rows_max, dtype=torch.int32, device=dev)
+        ge = torch.empty((world * nnz_max, 4), dtype=torch.int32, device=dev)
+        dist.all_gather_into_tensor(gc, counts)
+        dist.all_gather_into_tensor(ge, edges)
+    else:
+        gc, ge = counts, edges
+    row_begin = [row_block(g, world, n)[0] for g in range(world)] + [n]
+    return mpap_roadmap_assemble_device(positions, row_begin, gc.view(world, rows_max),
+                                        ge.view(world, nnz_max, 4), r, stream=stream)

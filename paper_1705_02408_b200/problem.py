@@ -48,6 +48,20 @@ def build_problem_sharded(prob, rank: int, world: int, stream=None) -> Roadmap:
                                full["s"], full["c"], prob.r, stream=stream)
 
 
+def build_problem_sharded_device(prob, rank: int, world: int, stream=None) -> Roadmap:
+    """SURVEY.md §8(e) with the CSR blocks kept on the device: build rows
+    [g n/G, (g+1) n/G), one NCCL all-gather of the device blocks, device-side
+    assembly (dist.gather_csr_blocks_device)."""
+    from .dist import gather_csr_blocks_device, row_block
+    b, e = row_block(rank, world, prob.n)
+    part = build_problem_rows(prob, b, e, stream=stream)
+    try:
+        return gather_csr_blocks_device(part, b, e, world, prob.n, prob.samples[:, : prob.pos_dim], prob.r,
+                                        stream=stream)
+    finally:
+        part.free()
+
+
 def search_problem(rm: Roadmap, prob, beta: float, env: int = 0, lam=None, trace_waves: int = 0,
                    path_capacity: int = 65536, stream=None, forall_t: bool = False) -> Dict[str, Any]:
     return mpap_search(rm, env, prob.start, prob.goal_lo, prob.goal_hi, beta, prob.lam if lam is None else lam,

@@ -70,3 +70,57 @@ def test_row_range_validation(mp):
     empty = mp.pb.build_problem_rows(prob, 7, 7)
     assert mp.mpap_roadmap_info(empty)["nnz"] == 0
     empty.free()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+def test_device_blocks_assemble_to_full_c4(mp, world):
+    """The device path (mpap_roadmap_block_device per rank, the slots stacked
+    as NCCL's all_gather_into_tensor lays them out, mpap_roadmap_assemble_device)
+    gives the full C4 CSR bit for bit (digests of tests/golden/c4_full.json,
+    oracle only) and the same search."""
+    import json
+    import os
+    import sys
+    import torch
+    golden = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    sys.path.insert(0, golden)
+    from digest import csr_digests
+    gold = json.load(open(os.path.join(golden, "c4_full.json")))
+    prob = make_problem(load_config("c4"))
+    dev = torch.device("cuda")
+    parts, sizes = [], []
+    for rank in range(world):
+        b, e = mp.dist.row_block(rank, world, prob.n)
+        part = mp.pb.build_problem_rows(prob, b, e)
+        sizes.append((e - b, mp.mpap_roadmap_info(part)["nnz"]))
+        parts.append(part)
+    rows_max = max(s[0] for s in sizes)
+    nnz_max = max(max(s[1] for s in sizes), 1)
+    gc = torch.zeros((world, rows_max), dtype=torch.int32, device=dev)
+    ge = torch.zeros((world, nnz_max, 4), dtype=torch.int32, device=dev)
+    for rank, part in enumerate(parts):
+        assert mp.mpap_roadmap_block_device(part, gc[rank], ge[rank]) == sizes[rank][1]
+        part.free()
+    row_begin = [mp.dist.row_block(g, world, prob.n)[0] for g in range(world)] + [prob.n]
+    rm = mp.mpap_roadmap_assemble_device(prob.samples[:, :3], row_begin, gc, ge, prob.r)
+    assert csr_digests(mp.mpap_roadmap_export(rm)) == gold["digests"]
+    assert mp.mpap_roadmap_info(rm)["nnz_free"] == gold["nnz_free"]
+    s = gold["searches"][1]
+    g = mp.pb.search_problem(rm, prob, float(s["beta"]), trace_waves=4096)
+    assert g["path"].tolist() == s["path"] and g["wave_counters"].tolist() == s["wave_counters"]
+    rm.free()
+
+
+def test_device_assemble_rejects_bad_blocks(mp):
+    import torch
+    dev = torch.device("cuda")
+    pos = np.zeros((4, 2))
+    gc = torch.tensor([[1, 1], [1, 0]], dtype=torch.int32, device=dev)
+    ge = torch.zeros((2, 2, 4), dtype=torch.int32, device=dev)
+    ge[0, 0, 0] = 1
+    ge[0, 1, 0] = 9      # dst out of range
+    ge[1, 0, 0] = 0
+    with pytest.raises(mp.MpapError):
+        mp.mpap_roadmap_assemble_device(pos, [0, 2, 4], gc, ge, 1.0)
+    with pytest.raises(mp.MpapError):   # blocks do not tile [0, n)
+        mp.mpap_roadmap_assemble_device(pos, [0, 2, 3], gc, ge, 1.0)
