@@ -1472,6 +1472,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_affected(const double* __restri
     if (_e != cudaSuccess) return cuda_error(_e, #x);  \
   } while (0)
 
+// SM count of the current device (grid sizes: multiples of it)
+int device_sms() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 1;
+}
+
 // exclusive scan of int32 row counts -> int64 row offsets (k_scan), for the
 // other translation units (device-side row-block assembly)
 cudaError_t scan_row_counts(const int32_t* cnt, int64_t n, int64_t* row_ptr, cudaStream_t st) {
@@ -1743,7 +1751,7 @@ mpap_status build_roadmap_device(mpap_roadmap* rm, cudaStream_t st) {
     CK(cudaMemsetAsync(rm->d_ready, 0, sizeof(int32_t) * N, st));
     if (rm->nnz_total > 0) {
       ProfScope ps("k_lazy_init", st);
-      k_lazy_init<<<(unsigned)std::min<int64_t>((N + 7) / 8, 148 * 16), 256, 0, st>>>(
+      k_lazy_init<<<(unsigned)std::min<int64_t>((N + 7) / 8, (int64_t)device_sms() * 16), 256, 0, st>>>(
           d_scr, cap, rm->d_row_ptr, N, rm->d_edges, rm->d_tau, rm->d_esrc, rm->d_peak);
       CK(cudaGetLastError());
       note_launch();
@@ -1869,7 +1877,7 @@ mpap_status evaluate_rows_device(mpap_roadmap* rm, const int32_t* d_rows, int64_
   {
     ProfScope ps("k_row_items", st);
     const int64_t n = d_rows ? n_req : N;
-    k_row_items<<<(unsigned)std::min<int64_t>((n + 7) / 8, 148 * 16), 256, 0, st>>>(d_rows, n_req, N, rm->d_row_ptr,
+    k_row_items<<<(unsigned)std::min<int64_t>((n + 7) / 8, (int64_t)device_sms() * 16), 256, 0, st>>>(d_rows, n_req, N, rm->d_row_ptr,
                                                                                     rm->d_ready, d_items, d_ctr);
     CK(cudaGetLastError());
   }

@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "mpap_internal.cuh"
 
 namespace mpap {
@@ -189,7 +191,10 @@ void prof_drain_locked() {
 }
 }  // namespace
 
+// NVTX: every kernel launch of the library is a named host range (visible to
+// nsys / ncu --nvtx when a tool is attached; a no-op otherwise).
 ProfScope::ProfScope(const char* kernel, cudaStream_t stream) : name(kernel), st(stream), rec(nullptr) {
+  nvtxRangePushA(kernel);
   if (!g_prof_on.load()) return;
   PendingRec* r = new PendingRec{kernel, nullptr, nullptr};
   cudaEventCreate(&r->a);
@@ -199,6 +204,7 @@ ProfScope::ProfScope(const char* kernel, cudaStream_t stream) : name(kernel), st
 }
 
 ProfScope::~ProfScope() {
+  nvtxRangePop();
   if (!rec) return;
   PendingRec* r = static_cast<PendingRec*>(rec);
   cudaEventRecord(r->b, st);

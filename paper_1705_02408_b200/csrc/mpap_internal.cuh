@@ -98,6 +98,8 @@ struct HostTimer {
   }
 };
 
+// SM count of the current device
+int device_sms();
 // exclusive scan of int32 row counts -> int64 row offsets (k_scan)
 cudaError_t scan_row_counts(const int32_t* cnt, int64_t n, int64_t* row_ptr, cudaStream_t st);
 
