@@ -429,6 +429,9 @@ struct WarpLists {
 #ifndef MPAP_CULL_FENV
 #define MPAP_CULL_FENV 1     // feature cull from per-environment float copies staged in shared memory
 #endif
+#ifndef MPAP_CULL_BRANCHFREE
+#define MPAP_CULL_BRANCHFREE 1   // bearing cull evaluated by every lane (no divergent branches)
+#endif
 #ifndef MPAP_FMASK_F32
 #define MPAP_FMASK_F32 0     // occluder masks in single precision, lanes over boxes (measured slower: 177.4 -> 196.3 ms)
 #endif
@@ -894,6 +897,19 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
         const float ey = fmaxf(fmaxf(fly - fy, fy - fhy), 0.0f);
         const float ez = (D == 3) ? fmaxf(fmaxf(flz - fz, fz - fhz), 0.0f) : 0.0f;
         keep = ex * ex + ey * ey + ez * ez <= mf2;
+#if MPAP_CULL_BRANCHFREE
+        {   // the same decision as the nested form below, without divergent branches
+          const float dx = fx - ccx, dy = fy - ccy;
+          const float dc2 = dx * dx + dy * dy;
+          const float inv = rsqrtf(fmaxf(dc2, 1e-30f));
+          const float sw = rho * inv;
+          const float cw = sqrtf(fmaxf(1.0f - sw * sw, 0.0f));
+          const float cosb = c1 * cw - s1 * sw;            // cos(beta0 + omega)
+          const float dotv = (ux * dx + uy * dy) * inv;      // cos(angle to the centre direction)
+          const bool out = ang && dc2 > rho2 && sw < smax && dotv < cosb - 2e-4f;
+          keep = keep && !out;
+        }
+#else
         if (keep && ang) {
           const float dx = fx - ccx, dy = fy - ccy;
           const float dc2 = dx * dx + dy * dy;
@@ -908,6 +924,7 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
             }
           }
         }
+#endif
       }
       const unsigned msk = __ballot_sync(FULL, keep);
       if (keep) {
