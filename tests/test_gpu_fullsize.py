@@ -208,3 +208,24 @@ def test_c4_tightest_bound_single_query(mp):
         assert g["path"].tolist() == s["path"]
         assert _hex(g["cost"]) == s["cost"] and _hex(g["h"]) == s["h"] and _hex(g["h_peak"]) == s["h_peak"]
     rm.free()
+
+
+def test_all_512_c5_queries_on_one_gpu(mp):
+    """BASELINE.json configs[4] whole: the 512 C5 environments built as one
+    batch and searched as one 512-query batch (one CTA per query) on one GPU
+    -- the strong-scaling base of bench.py --queries-per-gpu 512 -- every
+    result vs the oracle's stored run (c5_all.json), CSR digests of 16
+    sampled environments."""
+    gold = json.load(open(os.path.join(GOLDEN, "c5_all.json")))
+    cfg = load_config("c5")
+    assert len(gold["envs"]) == int(cfg["n_queries"]) and gold["beta"] == float(cfg["betas"][1])
+    B = mp.pb.Batch([make_problem(cfg, env_index=k) for k in range(len(gold["envs"]))])
+    rm = B.build()
+    before = mp.mpap_search_launches()
+    paths, res = B.search(rm, [gold["beta"]] * len(gold["envs"]), path_capacity=512)
+    assert mp.mpap_search_launches()["cta"] > before["cta"]
+    for q, gd in enumerate(gold["envs"]):
+        _check(res, paths, q, gd["searches"][0])
+    for e in range(0, len(gold["envs"]), 32):
+        assert _digests(mp, rm, e) == gold["envs"][e]["digests"], e
+    rm.free()
