@@ -423,6 +423,14 @@ def main():
     dom_ms, dom_n = kern[dom]
     roof = roofline(dom, dom_ms, dom_n, last_work, B, res, peaks, peak_src, fp64)
     roof["share_of_step"] = dom_ms / tot_ms if tot_ms > 0 else None
+    if dom == "k_heuristic" and last_work:
+        # context: SURVEY 8(d) writes the heuristic's work as K x F (step, feature)
+        # pairs per edge; the exact chunk culls leave the executed
+        # range tests -- the counted work above counts only executed tests
+        pairs = float(last_work["steps"]) * float(np.mean(B.n_feat))
+        roof["cull"] = {"step_feature_pairs_in_definition": pairs,
+                        "range_tests_executed": int(last_work["range_tests"]),
+                        "skipped_fraction": 1.0 - float(last_work["range_tests"]) / pairs if pairs else None}
     roof["traffic"] = committed_traffic(dom, Q)
 
     # ---- parity gate (hard): timed results, per-wave counters, CSR digests ----
