@@ -54,6 +54,14 @@ constexpr double kCullMargin = 1e-6;      // absolute; >> rounding of O(100) coo
 __device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
 
+// Approximate single-precision sqrt / division (MUFU, ~1e-7 relative error)
+// for the conservative culls and heading arcs only: their margins (1e-4 m,
+// 2e-3 rad, 2e-4 in a cosine) exceed the error by three orders of magnitude.
+// (The build compiles with -prec-sqrt/-prec-div: sqrtf and / are the
+// correctly rounded multi-instruction sequences.)
+__device__ __forceinline__ float sqrt_cull(float x) { return x > 0.0f ? x * rsqrtf(x) : 0.0f; }
+__device__ __forceinline__ float div_cull(float a, float b) { return __fdividef(a, b); }
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -425,6 +433,7 @@ struct WarpLists {
   float4* fenv;                 // [F_max] the current environment's features (float x, y, z), staged per env
   float* boxf;                  // [O_max][2D] the chunk's culled boxes (float), for the occluder masks
   int* fidx;                    // [F_max] the chunk's kept features' indices into fenv
+  const float* arc;             // [2] cos, sin of the bearing cull's half angle (block-shared)
 };
 #ifndef MPAP_CULL_FENV
 #define MPAP_CULL_FENV 1     // feature cull from per-environment float copies staged in shared memory
@@ -817,13 +826,10 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
   const double cos2 = P.fov_cos_half * P.fov_cos_half;
   constexpr int heur = HEUR;
   const unsigned lt = lanemask_lt();
-  // bearing cull half angle: FOV half angle + 2e-3 rad margin (cos, sin)
-  float chf = 0.0f, shf = 0.0f;
-  if (heur >= 2) {
-    const float hf = acosf((float)P.fov_cos_half) + 2e-3f;
-    chf = cosf(hf);
-    shf = sinf(hf);
-  }
+  // bearing cull half angle: FOV half angle + 2e-3 rad margin (cos, sin),
+  // computed once per block (k_edges)
+  const float chf = (heur >= 2) ? L.arc[0] : 0.0f, shf = (heur >= 2) ? L.arc[1] : 0.0f;
+  const float invT = 1.0f / (float)T;   // heading-arc parameters only (culling)
   for (int k0 = 0; k0 < K; k0 += 32) {
     const int nk = min(32, K - k0);
     const double ta = (double)k0 * Dl, tb = (double)(k0 + nk - 1) * Dl;
@@ -838,26 +844,26 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
     bool ang = false;
     float ux = 0.0f, uy = 0.0f, c1 = 0.0f, s1 = 0.0f, smax = -1.0f;
     if (heur >= 2) {
-      const float sa = (float)(ta / T), sb = (float)(tb / T);
+      const float sa = (float)ta * invT, sb = (float)tb * invT;
       const float hx0 = (float)hu0, hy0 = (float)hu1, gx = (float)hv0 - hx0, gy = (float)hv1 - hy0;
       const float ax = fmaf(sa, gx, hx0), ay = fmaf(sa, gy, hy0);
       const float bx = fmaf(sb, gx, hx0), by = fmaf(sb, gy, hy0);
       const float ex = bx - ax, ey = by - ay;
       const float ee = ex * ex + ey * ey;
-      float tq = (ee > 0.0f) ? -(ax * ex + ay * ey) / ee : 0.0f;
+      float tq = (ee > 0.0f) ? -div_cull(ax * ex + ay * ey, ee) : 0.0f;
       tq = fminf(fmaxf(tq, 0.0f), 1.0f);
       const float qx = ax + tq * ex, qy = ay + tq * ey;
       if (qx * qx + qy * qy > 1e-4f) {
         const float na = rsqrtf(ax * ax + ay * ay), nb2 = rsqrtf(bx * bx + by * by);
         const float dax = ax * na, day = ay * na, dbx = bx * nb2, dby = by * nb2;
         const float mx = dax + dbx, my = day + dby;
-        const float mn = sqrtf(mx * mx + my * my);
+        const float mn = sqrt_cull(mx * mx + my * my);
         if (mn > 1e-2f) {
-          ux = mx / mn;
-          uy = my / mn;
+          ux = div_cull(mx, mn);
+          uy = div_cull(my, mn);
           // |da + db| = 2 cos(dev), |da - db| = 2 sin(dev)
           const float cd = 0.5f * mn;
-          const float sd = 0.5f * sqrtf((dax - dbx) * (dax - dbx) + (day - dby) * (day - dby));
+          const float sd = 0.5f * sqrt_cull((dax - dbx) * (dax - dbx) + (day - dby) * (day - dby));
           c1 = chf * cd - shf * sd;   // cos(beta0)
           s1 = shf * cd + chf * sd;   // sin(beta0)
           if (c1 > -0.99995f) {       // beta0 < pi - 0.01
@@ -876,7 +882,7 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
     const float flx = (float)lo[0], fhx = (float)hi[0], fly = (float)lo[1], fhy = (float)hi[1];
     const float flz = (D == 3) ? (float)lo[D - 1] : 0.0f, fhz = (D == 3) ? (float)hi[D - 1] : 0.0f;
     const float ccx = 0.5f * (flx + fhx), ccy = 0.5f * (fly + fhy);
-    const float rho = 0.5f * sqrtf((fhx - flx) * (fhx - flx) + (fhy - fly) * (fhy - fly)) + 1e-4f;
+    const float rho = 0.5f * sqrt_cull((fhx - flx) * (fhx - flx) + (fhy - fly) * (fhy - fly)) + 1e-4f;
     const float rho2 = rho * rho;
     const float mf = (float)R + 1e-3f;
     const float mf2 = mf * mf;
@@ -903,7 +909,7 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
           const float dc2 = dx * dx + dy * dy;
           const float inv = rsqrtf(fmaxf(dc2, 1e-30f));
           const float sw = rho * inv;
-          const float cw = sqrtf(fmaxf(1.0f - sw * sw, 0.0f));
+          const float cw = sqrt_cull(1.0f - sw * sw);
           const float cosb = c1 * cw - s1 * sw;            // cos(beta0 + omega)
           const float dotv = (ux * dx + uy * dy) * inv;      // cos(angle to the centre direction)
           const bool out = ang && dc2 > rho2 && sw < smax && dotv < cosb - 2e-4f;
@@ -943,7 +949,32 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
     // single precision with a 1e-4 m margin (>> the float rounding of
     // coordinates below 1e3 m): a superset of the exact overlaps.
     const bool use_mask = nb > 0 && nb <= 64;
-#if !MPAP_FMASK_F32
+#if MPAP_FMASK_F32 == 2
+    if (use_mask) {   // one kept feature per lane, boxes in single precision (1e-4 m margin)
+      constexpr float mg = 1e-4f;
+      const float clo[3] = {flx, fly, flz}, chi[3] = {fhx, fhy, fhz};
+      for (int i = lane; i < nf; i += 32) {
+        float fl[D], fh[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+          const float fq = (float)L.f[q][i];
+          fl[q] = fminf(clo[q], fq) - mg;
+          fh[q] = fmaxf(chi[q], fq) + mg;
+        }
+        unsigned long long msk = 0ull;
+        for (int bb = 0; bb < nb; ++bb) {
+          const float* bx = L.boxf + (size_t)bb * 2 * D;
+          bool sep = false;
+#pragma unroll
+          for (int q = 0; q < D; ++q) sep |= bx[q] > fh[q] || bx[D + q] < fl[q];
+          if (!sep) msk |= 1ull << bb;
+        }
+        L.fmask[i] = msk;
+      }
+      W.add(lane, W_CULL_TESTS, nf * nb);
+      __syncwarp();
+    }
+#elif !MPAP_FMASK_F32
     if (use_mask) {
       for (int i = lane; i < nf; i += 32) {
         double fl[D], fh[D];
@@ -1110,7 +1141,13 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
   __shared__ unsigned s_work[kWarps][W_NUM];
   __shared__ double s_mlp[kMlpSize];
   __shared__ double s_ec[kWarps][12];
+  __shared__ float s_arc[2];
   for (int i = threadIdx.x; i < kMlpSize; i += blockDim.x) s_mlp[i] = P.mlp[i];
+  if (threadIdx.x == 0) {
+    const float hf = acosf((float)P.fov_cos_half) + 2e-3f;
+    s_arc[0] = cosf(hf);
+    s_arc[1] = sinf(hf);
+  }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpLists<D> L;
@@ -1128,6 +1165,7 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
     if (MPAP_FMASK_F32) nxt += os * D;
     L.fidx = reinterpret_cast<int*>(nxt);
     L.mlp = s_mlp;
+    L.arc = s_arc;
   }
   int staged_env = -1;   // environment whose features L.fenv holds (PHASE 1)
   const int64_t NI = items ? n_items : node_base[B];
