@@ -1326,8 +1326,14 @@ __global__ void __launch_bounds__(kFoldThreads, MPAP_FOLD_MIN_BLOCKS) k_fold(con
                                                       EdgeRec* __restrict__ edges, float2* __restrict__ peak,
                                                       const longlong2* __restrict__ items, int64_t n) {
   __shared__ double s_mlp[kMlpSize];
-  if (HEUR == 3)
+  // MLP input k_v / n_f for the small counts, each entry the same correctly
+  // rounded division the step would do (a lookup instead of a DDIV per step)
+  constexpr int kZ2 = 256;
+  __shared__ double s_z2[kZ2];
+  if (HEUR == 3) {
     for (int i = threadIdx.x; i < kMlpSize; i += blockDim.x) s_mlp[i] = P.mlp[i];
+    for (int i = threadIdx.x; i < kZ2; i += blockDim.x) s_z2[i] = (double)i / P.n_f;
+  }
   __syncthreads();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n) return;
@@ -1363,6 +1369,7 @@ __global__ void __launch_bounds__(kFoldThreads, MPAP_FOLD_MIN_BLOCKS) k_fold(con
 #pragma unroll
   for (int j = 0; j < D; ++j) { c2[j] = 0.0; c3[j] = 0.0; }
   if (HEUR == 3 && DYN == 1) di_traj<D>(su_l, sv_l, T, c2, c3);
+  const bool unit_vref = P.v_ref == 1.0;
   const uint16_t* kvp = kvbuf + koff[e];
   const double q = Dl / P.n_f;
   double s = 0.0, c = 0.0, Sp = 0.0, Cp = 0.0;
@@ -1393,12 +1400,14 @@ __global__ void __launch_bounds__(kFoldThreads, MPAP_FOLD_MIN_BLOCKS) k_fold(con
             for (int j = 0; j < D; ++j) ss = fma(vel[j], vel[j], ss);
             speed = sqrt(ss);
           }
-          z0[u] = speed / P.v_ref;
+          z0[u] = unit_vref ? speed : speed / P.v_ref;   // x / 1.0 == x exactly (IEEE)
         }
       }
       if (HEUR == 3) {
         const double z1 = omega / P.w_ref;
-        const double2 o = mlp_out0_x2(s_mlp, z0[0], z0[1], z1, (double)kv2[0] / P.n_f, (double)kv2[1] / P.n_f);
+        const double za = kv2[0] < kZ2 ? s_z2[kv2[0]] : (double)kv2[0] / P.n_f;
+        const double zb = kv2[1] < kZ2 ? s_z2[kv2[1]] : (double)kv2[1] / P.n_f;
+        const double2 o = mlp_out0_x2(s_mlp, z0[0], z0[1], z1, za, zb);
         inc2[0] = inc2[0] + Dl * (P.mlp_gain * o.x);
         inc2[1] = inc2[1] + Dl * (P.mlp_gain * o.y);
       }
