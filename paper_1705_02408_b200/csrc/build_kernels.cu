@@ -1370,6 +1370,7 @@ __global__ void __launch_bounds__(kFoldThreads, MPAP_FOLD_MIN_BLOCKS) k_fold(con
   for (int j = 0; j < D; ++j) { c2[j] = 0.0; c3[j] = 0.0; }
   if (HEUR == 3 && DYN == 1) di_traj<D>(su_l, sv_l, T, c2, c3);
   const bool unit_vref = P.v_ref == 1.0;
+  const double z1 = omega / P.w_ref;   // per-edge MLP input (one division per edge)
   const uint16_t* kvp = kvbuf + koff[e];
   const double q = Dl / P.n_f;
   double s = 0.0, c = 0.0, Sp = 0.0, Cp = 0.0;
@@ -1404,7 +1405,6 @@ __global__ void __launch_bounds__(kFoldThreads, MPAP_FOLD_MIN_BLOCKS) k_fold(con
         }
       }
       if (HEUR == 3) {
-        const double z1 = omega / P.w_ref;
         const double za = kv2[0] < kZ2 ? s_z2[kv2[0]] : (double)kv2[0] / P.n_f;
         const double zb = kv2[1] < kZ2 ? s_z2[kv2[1]] : (double)kv2[1] / P.n_f;
         const double2 o = mlp_out0_x2(s_mlp, z0[0], z0[1], z1, za, zb);
