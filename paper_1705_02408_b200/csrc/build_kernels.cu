@@ -438,6 +438,9 @@ struct WarpLists {
 #ifndef MPAP_CULL_FENV
 #define MPAP_CULL_FENV 1     // feature cull from per-environment float copies staged in shared memory
 #endif
+#ifndef MPAP_CULL_TWOSTAGE
+#define MPAP_CULL_TWOSTAGE 1   // feature cull: range over all features, bearing over the compacted survivors
+#endif
 #ifndef MPAP_CULL_BRANCHFREE
 #define MPAP_CULL_BRANCHFREE 1   // bearing cull evaluated by every lane (no divergent branches)
 #endif
@@ -888,6 +891,58 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
     const float mf2 = mf * mf;
     int nf = 0;
     __syncwarp();
+#if MPAP_CULL_TWOSTAGE && MPAP_CULL_FENV
+    {
+      // stage 1: range only, survivors' indices compacted into the (not yet
+      // used) occluder-mask array; stage 2: bearing over the survivors only,
+      // every lane busy
+      int* rsel = reinterpret_cast<int*>(L.fmask);
+      int nr = 0;
+      for (int f0 = 0; f0 < F; f0 += 32) {
+        const int f = f0 + lane;
+        bool keep = false;
+        if (f < F) {
+          const float4 fv = L.fenv[f];
+          const float ex = fmaxf(fmaxf(flx - fv.x, fv.x - fhx), 0.0f);
+          const float ey = fmaxf(fmaxf(fly - fv.y, fv.y - fhy), 0.0f);
+          const float ez = (D == 3) ? fmaxf(fmaxf(flz - fv.z, fv.z - fhz), 0.0f) : 0.0f;
+          keep = ex * ex + ey * ey + ez * ez <= mf2;
+        }
+        const unsigned msk = __ballot_sync(FULL, keep);
+        if (keep) rsel[nr + __popc(msk & lt)] = f;
+        nr += __popc(msk);
+      }
+      __syncwarp();
+      for (int i0 = 0; i0 < nr; i0 += 32) {
+        const int i = i0 + lane;
+        bool keep = false;
+        int f = 0;
+        if (i < nr) {
+          f = rsel[i];
+          keep = true;
+          if (ang) {
+            const float4 fv = L.fenv[f];
+            const float dx = fv.x - ccx, dy = fv.y - ccy;
+            const float dc2 = dx * dx + dy * dy;
+            const float inv = rsqrtf(fmaxf(dc2, 1e-30f));
+            const float sw = rho * inv;
+            const float cw = sqrt_cull(1.0f - sw * sw);
+            const float cosb = c1 * cw - s1 * sw;            // cos(beta0 + omega)
+            const float dotv = (ux * dx + uy * dy) * inv;      // cos(angle to the centre direction)
+            keep = !(dc2 > rho2 && sw < smax && dotv < cosb - 2e-4f);
+          }
+        }
+        const unsigned msk = __ballot_sync(FULL, keep);
+        if (keep) {
+          const int pos = nf + __popc(msk & lt);
+#pragma unroll
+          for (int q = 0; q < D; ++q) L.f[q][pos] = __ldg(feat + (size_t)f * D + q);   // exact coordinates
+        }
+        nf += __popc(msk);
+      }
+      __syncwarp();
+    }
+#else
     for (int f0 = 0; f0 < F; f0 += 32) {
       const int f = f0 + lane;
       bool keep = false;
@@ -941,6 +996,7 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
       }
       nf += __popc(msk);
     }
+#endif
     const int nb = (nf > 0) ? cull_boxes<D>(box, O, lo, hi, m, L.box, lane, MPAP_FMASK_F32 ? L.boxf : nullptr) : 0;
     W.add(lane, W_CULL_TESTS, F + (nf > 0 ? O : 0));
     // per kept feature: which of the chunk's boxes meet the box spanned by the
