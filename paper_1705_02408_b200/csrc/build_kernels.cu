@@ -438,6 +438,9 @@ struct WarpLists {
 #ifndef MPAP_CULL_FENV
 #define MPAP_CULL_FENV 1     // feature cull from per-environment float copies staged in shared memory
 #endif
+#ifndef MPAP_FMASK_PAIRS
+#define MPAP_FMASK_PAIRS 1   // occluder masks of <= 16 kept features: lanes over (feature, box) pairs
+#endif
 #ifndef MPAP_CULL_TWOSTAGE
 #define MPAP_CULL_TWOSTAGE 1   // feature cull: range over all features, bearing over the compacted survivors
 #endif
@@ -1031,7 +1034,36 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
       __syncwarp();
     }
 #elif !MPAP_FMASK_F32
-    if (use_mask) {
+    if (use_mask && MPAP_FMASK_PAIRS && nf <= 16) {
+      // few kept features: lanes over (feature, box) pairs -- feature i =
+      // lane mod nfp, boxes sub, sub + g, ... (g = 32 / nfp lane groups); the
+      // groups' partial masks are OR-ed with shuffles
+      int nfp = 1;
+      while (nfp < nf) nfp <<= 1;
+      const int g = 32 / nfp, i = lane & (nfp - 1), sub = lane / nfp;
+      unsigned long long msk = 0ull;
+      if (i < nf) {
+        double fl[D], fh[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+          const double fq = L.f[q][i];
+          fl[q] = dmin(lo[q], fq) - kCullMargin;
+          fh[q] = dmax(hi[q], fq) + kCullMargin;
+        }
+        for (int bb = sub; bb < nb; bb += g) {
+          const double* bx = L.box + (size_t)bb * 2 * D;
+          bool sep = false;
+#pragma unroll
+          for (int q = 0; q < D; ++q)
+            if (bx[q] > fh[q] || bx[D + q] < fl[q]) sep = true;
+          if (!sep) msk |= 1ull << bb;
+        }
+      }
+      for (int o = nfp; o < 32; o <<= 1) msk |= __shfl_xor_sync(FULL, msk, o);
+      if (sub == 0 && i < nf) L.fmask[i] = msk;
+      W.add(lane, W_CULL_TESTS, nf * nb);
+      __syncwarp();
+    } else if (use_mask) {
       for (int i = lane; i < nf; i += 32) {
         double fl[D], fh[D];
 #pragma unroll
