@@ -426,7 +426,8 @@ __global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ cnt, 
 // Per-warp shared scratch: culled feature coordinates (SoA) and culled boxes.
 template <int D>
 struct WarpLists {
-  double* f[D];                 // [F_max] each
+  double* f[D];                 // [F_max] each; f[0], f[1] interleaved as (x, y) pairs (fxy), f[D-1] = z
+  double2* fxy;                 // [F_max] (x, y) of the kept features: one LDS.128 per feature in the step loop
   double* box;                  // [O_max][2D]
   unsigned long long* fmask;    // [F_max] per-feature box masks
   const double* mlp;            // [122] block-shared MLP weights
@@ -463,6 +464,9 @@ __host__ __device__ constexpr size_t round4(int x) { return (size_t)((x + 3) & ~
 // Work counters: warp-uniform counts go to the warp's shared-memory slots
 // (written by lane 0 only); per-lane counts live in four registers and are
 // folded into the slots once per edge.
+// kept feature i, axis q: x and y interleaved in fxy, z in its own array
+#define FREF(L, q, i) ((q) < 2 ? (L).f[q][2 * (i)] : (L).f[q][i])
+
 struct Work {
   unsigned* sm;   // [W_NUM] per warp
   unsigned occl_segs, occl_tests, coll_segs, coll_tests;
@@ -939,7 +943,7 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
         if (keep) {
           const int pos = nf + __popc(msk & lt);
 #pragma unroll
-          for (int q = 0; q < D; ++q) L.f[q][pos] = __ldg(feat + (size_t)f * D + q);   // exact coordinates
+          for (int q = 0; q < D; ++q) FREF(L, q, pos) = __ldg(feat + (size_t)f * D + q);   // exact coordinates
         }
         nf += __popc(msk);
       }
@@ -994,7 +998,7 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
       if (keep) {
         const int pos = nf + __popc(msk & lt);
 #pragma unroll
-        for (int q = 0; q < D; ++q) L.f[q][pos] = __ldg(feat + (size_t)f * D + q);   // exact coordinates
+        for (int q = 0; q < D; ++q) FREF(L, q, pos) = __ldg(feat + (size_t)f * D + q);   // exact coordinates
         if (MPAP_CULL_FENV && MPAP_FMASK_F32) L.fidx[pos] = f;
       }
       nf += __popc(msk);
@@ -1016,7 +1020,7 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
         float fl[D], fh[D];
 #pragma unroll
         for (int q = 0; q < D; ++q) {
-          const float fq = (float)L.f[q][i];
+          const float fq = (float)FREF(L, q, i);
           fl[q] = fminf(clo[q], fq) - mg;
           fh[q] = fmaxf(chi[q], fq) + mg;
         }
@@ -1046,7 +1050,7 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
         double fl[D], fh[D];
 #pragma unroll
         for (int q = 0; q < D; ++q) {
-          const double fq = L.f[q][i];
+          const double fq = FREF(L, q, i);
           fl[q] = dmin(lo[q], fq) - kCullMargin;
           fh[q] = dmax(hi[q], fq) + kCullMargin;
         }
@@ -1068,7 +1072,7 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
         double fl[D], fh[D];
 #pragma unroll
         for (int q = 0; q < D; ++q) {
-          const double fq = L.f[q][i];
+          const double fq = FREF(L, q, i);
           fl[q] = dmin(lo[q], fq) - kCullMargin;
           fh[q] = dmax(hi[q], fq) + kCullMargin;
         }
@@ -1101,7 +1105,7 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
 #if MPAP_CULL_FENV
         const float4 fk = L.fenv[L.fidx[i]];
 #else
-        const float4 fk = make_float4((float)L.f[0][i], (float)L.f[1][i], (D == 3) ? (float)L.f[D - 1][i] : 0.0f, 0.0f);
+        const float4 fk = make_float4((float)FREF(L, 0, i), (float)FREF(L, 1, i), (D == 3) ? (float)FREF(L, D - 1, i) : 0.0f, 0.0f);
 #endif
         const float fq[3] = {fk.x, fk.y, fk.z};
         bool s0 = !h0, s1 = !h1;
@@ -1153,8 +1157,15 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
       for (int i = 0; i < nf; ++i) {
         double dl[D];
         double dd = 0.0;
+        double fc[D];
+        {
+          const double2 xy = L.fxy[i];   // one 16-byte load for (x, y)
+          fc[0] = xy.x;
+          fc[1] = xy.y;
+          if (D == 3) fc[D - 1] = L.f[D - 1][i];
+        }
 #pragma unroll
-        for (int j = 0; j < D; ++j) { dl[j] = L.f[j][i] - x[j]; dd = fma(dl[j], dl[j], dd); }
+        for (int j = 0; j < D; ++j) { dl[j] = fc[j] - x[j]; dd = fma(dl[j], dl[j], dd); }
         if (dd > R2) continue;
         if (heur != 0) {
           double dot = 0.0;
@@ -1172,7 +1183,7 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
         }
         double fp[D];
 #pragma unroll
-        for (int j = 0; j < D; ++j) fp[j] = L.f[j][i];
+        for (int j = 0; j < D; ++j) fp[j] = fc[j];
         const unsigned rr = use_mask ? seg_hits_boxes<D, true>(x, fp, dl, L.box, nb, fm)
                                      : seg_hits_boxes<D, false>(x, fp, dl, L.box, nb, 0ull);
         W.occl_tests += rr >> 1;
@@ -1242,8 +1253,10 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
   {
     const size_t fs = round4(f_max), os = round4(o_max);
     double* base = smem + (size_t)warp * warp_scratch_doubles(D, fs, os);
-#pragma unroll
-    for (int q = 0; q < D; ++q) L.f[q] = base + (size_t)q * fs;
+    L.fxy = reinterpret_cast<double2*>(base);   // (x, y) pairs
+    L.f[0] = base;                               // (x, y) strided: accessed through FREF
+    L.f[1] = base + 1;
+    if (D == 3) L.f[D - 1] = base + 2 * fs;      // z
     L.box = base + (size_t)D * fs;
     L.fmask = reinterpret_cast<unsigned long long*>(L.box + os * 2 * D);
     double* nxt = reinterpret_cast<double*>(L.fmask + fs);
