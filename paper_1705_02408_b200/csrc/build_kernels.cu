@@ -467,6 +467,19 @@ __host__ __device__ constexpr size_t round4(int x) { return (size_t)((x + 3) & ~
 // kept feature i, axis q: x and y interleaved in fxy, z in its own array
 #define FREF(L, q, i) ((q) < 2 ? (L).f[q][2 * (i)] : (L).f[q][i])
 
+// One staged box (lo[D], hi[D] contiguous, 16-byte aligned) with 16-byte
+// shared loads.
+template <int D>
+__device__ __forceinline__ void load_box(const double* bx, double* b) {
+  const double2* p = reinterpret_cast<const double2*>(bx);
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const double2 v = p[k];
+    b[2 * k] = v.x;
+    b[2 * k + 1] = v.y;
+  }
+}
+
 struct Work {
   unsigned* sm;   // [W_NUM] per warp
   unsigned occl_segs, occl_tests, coll_segs, coll_tests;
@@ -560,7 +573,8 @@ __device__ __forceinline__ unsigned seg_hits_boxes(const double* A, const double
     } else {
       if (++i >= nl) break;
     }
-    const double* bx = bl + (size_t)i * 2 * D;
+    double bx[2 * D];
+    load_box<D>(bl + (size_t)i * 2 * D, bx);
     bool sep = false;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
@@ -1055,7 +1069,8 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
           fh[q] = dmax(hi[q], fq) + kCullMargin;
         }
         for (int bb = sub; bb < nb; bb += g) {
-          const double* bx = L.box + (size_t)bb * 2 * D;
+          double bx[2 * D];
+          load_box<D>(L.box + (size_t)bb * 2 * D, bx);
           bool sep = false;
 #pragma unroll
           for (int q = 0; q < D; ++q)
@@ -1078,7 +1093,8 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
         }
         unsigned long long msk = 0ull;
         for (int bb = 0; bb < nb; ++bb) {
-          const double* bx = L.box + (size_t)bb * 2 * D;
+          double bx[2 * D];
+          load_box<D>(L.box + (size_t)bb * 2 * D, bx);
           bool sep = false;
 #pragma unroll
           for (int q = 0; q < D; ++q)
