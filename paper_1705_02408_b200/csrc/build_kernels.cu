@@ -523,8 +523,13 @@ __device__ int cull_boxes(const double* __restrict__ box, int O, const double* l
     double bl[2 * D];
     if (o < O) {
       keep = true;
+      const double2* src = reinterpret_cast<const double2*>(box + (size_t)o * 2 * D);   // 16-byte aligned records
 #pragma unroll
-      for (int k = 0; k < 2 * D; ++k) bl[k] = __ldg(box + (size_t)o * 2 * D + k);
+      for (int k = 0; k < D; ++k) {
+        const double2 v = __ldg(src + k);
+        bl[2 * k] = v.x;
+        bl[2 * k + 1] = v.y;
+      }
 #pragma unroll
       for (int k = 0; k < D; ++k)
         if (bl[k] > hi[k] + m || bl[D + k] < lo[k] - m) keep = false;
@@ -532,9 +537,9 @@ __device__ int cull_boxes(const double* __restrict__ box, int O, const double* l
     const unsigned msk = __ballot_sync(FULL, keep);
     if (keep) {
       const int pos = nc + __popc(msk & lt);
-      double* dst = out + (size_t)pos * 2 * D;
+      double2* dst = reinterpret_cast<double2*>(out + (size_t)pos * 2 * D);
 #pragma unroll
-      for (int k = 0; k < 2 * D; ++k) dst[k] = bl[k];
+      for (int k = 0; k < D; ++k) dst[k] = make_double2(bl[2 * k], bl[2 * k + 1]);
       if (outf) {
 #pragma unroll
         for (int k = 0; k < 2 * D; ++k) outf[(size_t)pos * 2 * D + k] = (float)bl[k];
@@ -956,8 +961,11 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
         const unsigned msk = __ballot_sync(FULL, keep);
         if (keep) {
           const int pos = nf + __popc(msk & lt);
-#pragma unroll
-          for (int q = 0; q < D; ++q) FREF(L, q, pos) = __ldg(feat + (size_t)f * D + q);   // exact coordinates
+          {   // exact coordinates: (x, y) with one 16-byte store, z
+            const double* fp = feat + (size_t)f * D;
+            L.fxy[pos] = make_double2(__ldg(fp), __ldg(fp + 1));
+            if (D == 3) L.f[D - 1][pos] = __ldg(fp + D - 1);
+          }
         }
         nf += __popc(msk);
       }
