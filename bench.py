@@ -844,11 +844,14 @@ def fp64_ops(kernel: str, w: dict, D: int = 3) -> float:
     if kernel == "k_collide":
         return (12 * D + 2 * D + 4) * w["coll_segs"] + 4 * D * w["coll_box_tests"] + 27 * w["edges"]
     if kernel == "k_heuristic":
-        # per step: t, position (3 per axis), heading interpolation (2 x 3 + 1), |h|^2 (D);
-        # range test 2D + 1, FOV test 2D + 3, occlusion segment 6D (dl, 1/dl, segment box),
-        # slab box test 4D; per free edge 40 (trajectory, stationary points, arc)
-        per_step = 1 + 3 * D + 7 + D
-        return (per_step * w["steps"] + (2 * D + 1) * w["range_tests"] + (2 * D + 3) * w["fov_tests"]
+        # per step: t, position (3 per axis), heading interpolation (2 x 3 + 1), |h|^2 (DH);
+        # range test 2D + 1, FOV test 2 DH + 3, occlusion segment 6D (dl, 1/dl, segment box),
+        # slab box test 4D; per free edge 40 (trajectory, stationary points, arc).  The
+        # heading heuristics' view vector is horizontal: DH = 2 terms in |h|^2 and the FOV
+        # dot product (the kernels skip the z term, an exact zero)
+        DH = 2
+        per_step = 1 + 3 * D + 7 + DH
+        return (per_step * w["steps"] + (2 * D + 1) * w["range_tests"] + (2 * DH + 3) * w["fov_tests"]
                 + 6 * D * w["occl_segs"] + 4 * D * w["occl_box_tests"] + 40 * w["free_edges"])
     if kernel == "k_fold":
         # per step: increment 2, MLP 3-8-8-1 with ReLUs 128, speed (t, velocity 3D, |v|^2 D, sqrt) 14,

@@ -1066,7 +1066,8 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
       // groups' partial masks are OR-ed with shuffles
       int nfp = 1;
       while (nfp < nf) nfp <<= 1;
-      const int g = 32 / nfp, i = lane & (nfp - 1), sub = lane / nfp;
+      const int lg = __ffs(nfp) - 1;   // nfp is a power of two
+      const int g = 32 >> lg, i = lane & (nfp - 1), sub = lane >> lg;
       unsigned long long msk = 0ull;
       if (i < nf) {
         double fl[D], fh[D];
@@ -1174,9 +1175,13 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
         hv[0] = fma(sp, hv0, (1.0 - sp) * hu0);
         hv[1] = fma(sp, hv1, (1.0 - sp) * hu1);
       }
+      // heading heuristics: hv is horizontal (hv_z = 0), so the z terms of hh
+      // and of the FOV dot product add exact zeros -- skipped (a zero's sign
+      // can differ, which no comparison below sees)
+      constexpr int DH = (HEUR >= 2) ? 2 : D;
       double hh = 0.0;
 #pragma unroll
-      for (int j = 0; j < D; ++j) hh = fma(hv[j], hv[j], hh);
+      for (int j = 0; j < DH; ++j) hh = fma(hv[j], hv[j], hh);
       int kv = 0;
       for (int i = 0; i < nf; ++i) {
         double dl[D];
@@ -1194,7 +1199,7 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
         if (heur != 0) {
           double dot = 0.0;
 #pragma unroll
-          for (int j = 0; j < D; ++j) dot = fma(hv[j], dl[j], dot);
+          for (int j = 0; j < DH; ++j) dot = fma(hv[j], dl[j], dot);
           if (!(hh > 0.0)) continue;
           if (dot < 0.0) continue;
           if (dot * dot < cos2 * (hh * dd)) continue;
