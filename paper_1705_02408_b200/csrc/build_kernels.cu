@@ -430,7 +430,6 @@ struct WarpLists {
   double2* fxy;                 // [F_max] (x, y) of the kept features: one LDS.128 per feature in the step loop
   double* box;                  // [O_max][2D]
   unsigned long long* fmask;    // [F_max] per-feature box masks
-  const double* mlp;            // [122] block-shared MLP weights
   float4* fenv;                 // [F_max] the current environment's features (float x, y, z), staged per env
   float* boxf;                  // [O_max][2D] the chunk's culled boxes (float), for the occluder masks
   int* fidx;                    // [F_max] the chunk's kept features' indices into fenv
@@ -672,76 +671,38 @@ __device__ __forceinline__ bool edge_collision(const DevParams& P, const double*
   return false;
 }
 
-// The weights are read from shared memory on every call (staged once per
-// block) so the compiler cannot hoist all 122 of them into registers.
-__device__ __noinline__ double mlp_out0(const double* w, double z0, double z1, double z2) {
-  const double* W1 = w;
-  const double* b1 = w + 24;
-  const double* W2 = w + 32;
-  const double* b2 = w + 96;
-  const double* W3 = w + 104;
-  const double* b3 = w + 120;
-  double h1[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    double a = b1[i];
-    a = fma(W1[i * 3 + 0], z0, a);
-    a = fma(W1[i * 3 + 1], z1, a);
-    a = fma(W1[i * 3 + 2], z2, a);
-    h1[i] = (a > 0.0) ? a : 0.0;
-  }
-  // output sum o = b3[0] + sum_i W3[i] h2[i] accumulated in index order as
-  // each hidden-2 unit is produced (same operation sequence as the contract)
-  double o = b3[0];
-#pragma unroll 1
-  for (int i = 0; i < 8; ++i) {
-    double a = b2[i];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) a = fma(W2[i * 8 + j], h1[j], a);
-    const double h2 = (a > 0.0) ? a : 0.0;
-    o = fma(W3[i], h2, o);
-  }
-  return o;
-}
-
-
-// mlp_out0 for two inputs that share z1 (two steps of one edge): every weight
-// read from shared memory feeds two DFMAs (k_fold is bound by the shared-
-// memory load issue rate at one load per DFMA).  Same operation order per
-// input as mlp_out0.
-__device__ __noinline__ double2 mlp_out0_x2(const double* w, double z0a, double z0b, double z1, double z2a,
-                                            double z2b) {
-  const double* W1 = w;
-  const double* b1 = w + 24;
-  const double* W2 = w + 32;
-  const double* b2 = w + 96;
-  const double* W3 = w + 104;
-  const double* b3 = w + 120;
+// Output 0 of the 3-8-8-1 MLP (reading R12) for two inputs that share z1
+// (two steps of one edge), each in the contract's operation order: hidden-1
+// units b1 + W1 z by fma in input order, ReLU; o = b3 then, as each hidden-2
+// unit (b2 + W2 h1 in index order, ReLU) is produced, o = fma(W3_i, h2_i, o).
+// The weights are read straight from the kernel's parameter bank (a
+// __grid_constant__ DevParams) at compile-time indices, so they reach the
+// DFMAs through uniform registers -- no shared-memory load per weight (that
+// load issue rate had capped k_fold's FP64 pipe at ~45 %).
+__device__ __forceinline__ double2 mlp_out0_x2(const double (&w)[kMlpSize], double z0a, double z0b, double z1,
+                                                 double z2a, double z2b) {
   double ha[8], hb[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const double w0 = W1[i * 3 + 0], w1 = W1[i * 3 + 1], w2 = W1[i * 3 + 2], bb = b1[i];
-    double a = fma(w0, z0a, bb), b = fma(w0, z0b, bb);
-    a = fma(w1, z1, a);
-    b = fma(w1, z1, b);
-    a = fma(w2, z2a, a);
-    b = fma(w2, z2b, b);
+    double a = fma(w[i * 3 + 0], z0a, w[24 + i]), b = fma(w[i * 3 + 0], z0b, w[24 + i]);
+    a = fma(w[i * 3 + 1], z1, a);
+    b = fma(w[i * 3 + 1], z1, b);
+    a = fma(w[i * 3 + 2], z2a, a);
+    b = fma(w[i * 3 + 2], z2b, b);
     ha[i] = (a > 0.0) ? a : 0.0;
     hb[i] = (b > 0.0) ? b : 0.0;
   }
-  double oa = b3[0], ob = b3[0];
-#pragma unroll 1
+  double oa = w[120], ob = w[120];
+#pragma unroll
   for (int i = 0; i < 8; ++i) {
-    double a = b2[i], b = b2[i];
+    double a = w[96 + i], b = w[96 + i];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const double wij = W2[i * 8 + j];
-      a = fma(wij, ha[j], a);
-      b = fma(wij, hb[j], b);
+      a = fma(w[32 + i * 8 + j], ha[j], a);
+      b = fma(w[32 + i * 8 + j], hb[j], b);
     }
-    const double w3 = W3[i];
-    oa = fma(w3, (a > 0.0) ? a : 0.0, oa);
-    ob = fma(w3, (b > 0.0) ? b : 0.0, ob);
+    oa = fma(w[104 + i], (a > 0.0) ? a : 0.0, oa);
+    ob = fma(w[104 + i], (b > 0.0) ? b : 0.0, ob);
   }
   return make_double2(oa, ob);
 }
@@ -1267,10 +1228,8 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
   extern __shared__ __align__(16) double smem[];
   __shared__ double s_state[kWarps][2][NS];
   __shared__ unsigned s_work[kWarps][W_NUM];
-  __shared__ double s_mlp[kMlpSize];
   __shared__ double s_ec[kWarps][12];
   __shared__ float s_arc[2];
-  for (int i = threadIdx.x; i < kMlpSize; i += blockDim.x) s_mlp[i] = P.mlp[i];
   if (threadIdx.x == 0) {
     const float hf = acosf((float)P.fov_cos_half) + 2e-3f;
     s_arc[0] = cosf(hf);
@@ -1294,7 +1253,6 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
     L.boxf = reinterpret_cast<float*>(nxt);
     if (MPAP_FMASK_F32) nxt += os * D;
     L.fidx = reinterpret_cast<int*>(nxt);
-    L.mlp = s_mlp;
     L.arc = s_arc;
   }
   int staged_env = -1;   // environment whose features L.fenv holds (PHASE 1)
@@ -1448,20 +1406,19 @@ constexpr int kFoldThreads = 256;
 
 template <int D, int DYN, int HEUR>
 __global__ void __launch_bounds__(kFoldThreads, MPAP_FOLD_MIN_BLOCKS) k_fold(const double* __restrict__ samples,
-                                                      const int64_t* __restrict__ node_base, int B, DevParams P,
+                                                      const int64_t* __restrict__ node_base, int B,
+                                                      const __grid_constant__ DevParams P,
                                                       const int32_t* __restrict__ esrc,
                                                       const double* __restrict__ tau_arr,
                                                       const long long* __restrict__ koff,
                                                       const uint16_t* __restrict__ kvbuf,
                                                       EdgeRec* __restrict__ edges, float2* __restrict__ peak,
                                                       const longlong2* __restrict__ items, int64_t n) {
-  __shared__ double s_mlp[kMlpSize];
   // MLP input k_v / n_f for the small counts, each entry the same correctly
   // rounded division the step would do (a lookup instead of a DDIV per step)
   constexpr int kZ2 = 256;
   __shared__ double s_z2[kZ2];
   if (HEUR == 3) {
-    for (int i = threadIdx.x; i < kMlpSize; i += blockDim.x) s_mlp[i] = P.mlp[i];
     for (int i = threadIdx.x; i < kZ2; i += blockDim.x) s_z2[i] = (double)i / P.n_f;
   }
   __syncthreads();
@@ -1537,7 +1494,7 @@ __global__ void __launch_bounds__(kFoldThreads, MPAP_FOLD_MIN_BLOCKS) k_fold(con
       if (HEUR == 3) {
         const double za = kv2[0] < kZ2 ? s_z2[kv2[0]] : (double)kv2[0] / P.n_f;
         const double zb = kv2[1] < kZ2 ? s_z2[kv2[1]] : (double)kv2[1] / P.n_f;
-        const double2 o = mlp_out0_x2(s_mlp, z0[0], z0[1], z1, za, zb);
+        const double2 o = mlp_out0_x2(P.mlp, z0[0], z0[1], z1, za, zb);
         inc2[0] = inc2[0] + Dl * (P.mlp_gain * o.x);
         inc2[1] = inc2[1] + Dl * (P.mlp_gain * o.y);
       }
