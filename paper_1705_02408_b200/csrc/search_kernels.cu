@@ -125,7 +125,8 @@ struct SearchArgs {
 };
 
 struct Ctl {
-  int q, gsize, psize, nsize, ncand, ntouched, nlabels, goal_in_g, overflow, any_goal, calloc;
+  int q, psize, nsize, ncand, ntouched, nlabels, overflow, any_goal, calloc;
+  int gs[2], gig[2];                // |G| and goal-in-G of the group of wave w: index w & 1
   int nsmall, nbig, snext, bnext;   // merge work lists (small: warp per node, pulled from snext; big: CTA per
                                     // node, pulled from bnext)
   int nmid, mnext;                  // mid: warp per node (binary searches), pulled from mnext
@@ -222,7 +223,7 @@ __device__ __forceinline__ long long bucket_of(float cost, double T) {
 template <typename Team>
 __device__ void partition(const Team& team, const SearchArgs& A, Ctl* S, const int32_t* src, int nsrc, int32_t* G,
                           int32_t* dst, long long inext, const int4* labels, const uint8_t* lstate,
-                          const uint8_t* goal) {
+                          const uint8_t* goal, int tp) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = lane_lt();
   const double thr = (double)inext * A.T;
@@ -250,7 +251,7 @@ __device__ void partition(const Team& team, const SearchArgs& A, Ctl* S, const i
     const unsigned md = __ballot_sync(FULLM, toD);
     int bg = 0, bd = 0;
     if (lane == 0) {
-      if (mg) bg = atomicAdd(&S->gsize, __popc(mg));
+      if (mg) bg = atomicAdd(&S->gs[tp], __popc(mg));
       if (md) bd = atomicAdd(&S->nsize, __popc(md));
     }
     bg = __shfl_sync(FULLM, bg, 0);
@@ -258,7 +259,7 @@ __device__ void partition(const Team& team, const SearchArgs& A, Ctl* S, const i
     if (toG) { DCHECK(bg + __popc(mg & lt) < A.caps.L); G[bg + __popc(mg & lt)] = id; }
     if (toD) { DCHECK(bd + __popc(md & lt) < A.caps.L); dst[bd + __popc(md & lt)] = id; }
   }
-  if (mygoal) S->goal_in_g = 1;
+  if (mygoal) S->gig[tp] = 1;
   if (myminb != LLONG_MAX) atomicMin(&S->minb, myminb);
 }
 
@@ -757,6 +758,13 @@ __device__ void warp_mid_merge(Ctl* S, const SlotCaps& C, int x, int n, const in
   __syncwarp();
 }
 
+// Per-wave counters and work-queue heads, zeroed by the leader once per wave.
+__device__ __forceinline__ void reset_wave_counters(Ctl* S) {
+  S->relax = 0; S->bpass = 0; S->tcount = 0; S->ssum = 0; S->inserted = 0; S->killed = 0;
+  S->ncand = 0; S->ntouched = 0; S->calloc = 0; S->nsmall = 0; S->nbig = 0; S->snext = 0; S->bnext = 0;
+  S->nmid = 0; S->mnext = 0;
+}
+
 template <bool TRACE, typename Team>
 __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slot, int qpos) {
   const int q = A.qidx[qpos];
@@ -787,6 +795,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
   int32_t* G = A.G + (size_t)slot * C.L;
   int32_t* pend = A.pend + (size_t)slot * C.L;
   int32_t* pend2 = A.pend2 + (size_t)slot * C.L;
+  int32_t* const Galt = A.pend2 + (size_t)slot * C.L;   // ring mode: the second group list (pend2 is unused there)
   int32_t* ring = C.R ? A.ring + (size_t)slot * C.R * C.L : nullptr;
   int32_t* stamp = A.stamp + (size_t)slot * C.n;
   uint8_t* goal = A.goal + (size_t)slot * C.n;
@@ -798,10 +807,11 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
   // ---- a5: init (A3.1-A3.4) ----
   if (!A.resume) {
     if (leader) {
-      S->gsize = 1; S->psize = 0; S->nsize = 0; S->ncand = 0; S->ntouched = 0; S->nlabels = 1; S->calloc = 0;
-      S->goal_in_g = 0; S->overflow = 0; S->any_goal = 0; S->i = 0; S->minb = LLONG_MAX;
+      S->gs[0] = 1; S->gs[1] = 0; S->psize = 0; S->nsize = 0; S->nlabels = 1;
+      S->gig[0] = 0; S->gig[1] = 0; S->overflow = 0; S->any_goal = 0; S->i = 0; S->minb = LLONG_MAX;
       S->relax_total = 0; S->inserted_total = 0; S->waves = 0; S->suspended = 0; S->pswap = 0; S->need = 0;
       for (int r = 0; r < kRingMax; ++r) S->rcount[r] = 0;
+      reset_wave_counters(S);
     }
     team.sync();
     bool mygoal = false;
@@ -825,7 +835,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
       sid[(size_t)Q.start * C.K] = 0;
       sn[Q.start] = 1;
       G[0] = 0;
-      S->goal_in_g = goal[Q.start];
+      S->gig[0] = goal[Q.start];
     }
     team.sync();
     if (!vld(S->any_goal)) {
@@ -846,14 +856,24 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
     if (leader) { S->suspended = 0; S->need = 0; }
     team.sync();
   }
+  // the group index i, kept by every thread (each computes the same value;
+  // S->i is its copy for a resumed launch and the host)
+  long long i_loc = vld(S->i);
   while (true) {
-    if (vld(S->goal_in_g) || vld(S->gsize) == 0) break;     // A3.5 (G = {} <=> P_open = {} here)
-    const int gsize = vld(S->gsize);
-    const long long i_cur = vld(S->i);
+    const int par = wave & 1;
+    if (vld(S->gig[par]) || vld(S->gs[par]) == 0) break;     // A3.5 (G = {} <=> P_open = {} here)
+    const int gsize = vld(S->gs[par]);
+    const long long i_cur = i_loc;
+    // ring mode: G_i and G_{i+1} in alternate lists, so retiring G_i and
+    // forming G_{i+1} share one phase; the next group's counters were last
+    // read at the top of the previous wave
+    int32_t* const Gc = (C.R && par) ? Galt : G;
+    int32_t* const Gn = (C.R && !par) ? Galt : G;
+    if (leader) { S->gs[par ^ 1] = 0; S->gig[par ^ 1] = 0; }
     if (A.ready) {   // lazy roadmap: every head of G_i must have its row evaluated
       bool my_need = false;
       for (int k = tid; k < gsize; k += nthr) {
-        const int64_t row = nbase + labels[G[k]].x;
+        const int64_t row = nbase + labels[Gc[k]].x;
         if (vld(A.ready[row]) != 1) {
           my_need = true;
           if (atomicCAS(&A.ready[row], 0, 2) == 0) A.req[atomicAdd(A.nreq, 1)] = (int32_t)row;
@@ -866,20 +886,14 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
         return;
       }
     }
-    team.sync();
-    if (leader) {
-      S->need = 0;
-      S->relax = 0; S->bpass = 0; S->tcount = 0; S->ssum = 0; S->inserted = 0; S->killed = 0;
-      S->ncand = 0; S->ntouched = 0; S->calloc = 0; S->nsmall = 0; S->nbig = 0; S->snext = 0; S->bnext = 0;
-      S->nmid = 0; S->mnext = 0;
-    }
-    team.sync();
+    // the per-wave counters were reset by the previous wave's retire step
+    // (or the init), two team barriers ago
     PHASE_MARK(0);
     // ---- a7 expand (A3.6-A3.11): warp per plan of G_i, 32 edges per step ----
     {
       unsigned long long my_relax = 0, my_bpass = 0, my_t = 0, my_ss = 0;
       for (int k = warp; k < gsize; k += nw) {
-        const int p = G[k];
+        const int p = Gc[k];
         const int4 lb = labels[p];
         const int u = lb.x;
         const float pc = __int_as_float(lb.z), ph = __int_as_float(lb.w);
@@ -1205,7 +1219,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
     for (int t = tid; t < nt; t += nthr) ccnt[touched[t]] = 0;
     // ---- a9 retire G_i (A3.16), i <- i+1 (A3.17) ----
     for (int k = tid; k < gsize; k += nthr) {
-      const int p = G[k];
+      const int p = Gc[k];
       if (lstate[p] == L_OPEN) lstate[p] = L_CLOSED;
     }
     if (leader) {
@@ -1220,9 +1234,12 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
       S->relax_total += vld(S->relax);
       S->inserted_total += vld(S->inserted);
       S->waves = wave + 1;
-      S->gsize = 0; S->nsize = 0; S->goal_in_g = 0; S->minb = LLONG_MAX;
+      S->nsize = 0; S->minb = LLONG_MAX;
+      reset_wave_counters(S);   // nothing reads them between the merge barrier and the next expand
     }
-    team.sync();
+    // ring mode: no barrier -- the partition below reads other plans' states
+    // (a plan is in exactly one ring list) and writes the other group list
+    if (!C.R) team.sync();
     PHASE_MARK(5);
     // ---- a6 G_{i+1} (A3.18), with the exact empty-group skip (R24) ----
     if (C.R) {
@@ -1232,32 +1249,36 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
       for (;;) {
         const int r = (int)(j % C.R);
         const int cnt = vld(S->rcount[r]);
-        partition(team, A, S, ring + (size_t)r * C.L, cnt, G, G, LLONG_MAX / 4, labels, lstate, goal);
+        partition(team, A, S, ring + (size_t)r * C.L, cnt, Gn, Gn, LLONG_MAX / 4, labels, lstate, goal, par ^ 1);
         team.sync();
-        const bool done = vld(S->gsize) > 0 || j >= i_cur + C.R;
-        team.sync();
+        const bool done = vld(S->gs[par ^ 1]) > 0 || j >= i_cur + C.R;   // the same for every thread
+        if (done) {
+          // list r is next written R - 1 groups later (new plans go to lists
+          // i + 1 .. i + R - 1), many barriers after this store
+          if (leader) { S->rcount[r] = 0; S->i = j; }
+          break;
+        }
+        team.sync();   // every thread has read gsize before the next list's partition adds to it
         if (leader) S->rcount[r] = 0;
-        if (done) break;
         ++j;
       }
-      if (leader) S->i = j;
-      team.sync();
+      i_loc = j;
       PHASE_MARK(6);
       ++wave;
       continue;
     }
     const int np = vld(S->psize);
     long long inext = i_cur + 1;
-    partition(team, A, S, pend, np, G, pend2, inext, labels, lstate, goal);
+    partition(team, A, S, pend, np, G, pend2, inext, labels, lstate, goal, par ^ 1);
     team.sync();
     PHASE_MARK(6);
-    if (vld(S->gsize) == 0 && vld(S->nsize) > 0) {
+    if (vld(S->gs[par ^ 1]) == 0 && vld(S->nsize) > 0) {
       inext = vld(S->minb);
       const int n2 = vld(S->nsize);
       team.sync();
       if (leader) { S->nsize = 0; S->minb = LLONG_MAX; }
       team.sync();
-      partition(team, A, S, pend2, n2, G, pend, inext, labels, lstate, goal);
+      partition(team, A, S, pend2, n2, G, pend, inext, labels, lstate, goal, par ^ 1);
       team.sync();
       if (leader) { S->psize = vld(S->nsize); S->i = inext; }
     } else {
@@ -1267,6 +1288,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
       pswap ^= 1;
     }
     team.sync();
+    i_loc = inext;
     ++wave;
   }
 
@@ -1279,7 +1301,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
     }
     return;
   }
-  if (!vld(S->goal_in_g)) {   // P_open emptied: no feasible plan
+  if (!vld(S->gig[wave & 1])) {   // P_open emptied: no feasible plan
     if (leader) {
       mpap_result r{};
       r.status = MPAP_ERR_NO_FEASIBLE_PLAN;
