@@ -431,6 +431,11 @@ __device__ __forceinline__ int block_excl_max(int v, int* scr) {
   return r;
 }
 
+__device__ __forceinline__ int4 shfl_xor4(const int4& v, int j) {
+  return make_int4(__shfl_xor_sync(FULLM, v.x, j), __shfl_xor_sync(FULLM, v.y, j), __shfl_xor_sync(FULLM, v.z, j),
+                   __shfl_xor_sync(FULLM, v.w, j));
+}
+
 __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* cs, const int32_t* coff,
                           const int32_t* ccnt, float2* sch, int32_t* sid, int32_t* sn, int4* labels,
                           uint8_t* lstate, const Pusher& PU, unsigned long long& my_ins,
@@ -450,10 +455,37 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
   int32_t* nsi = sid + ((size_t)(par ^ 1) * n + x) * (size_t)C.K;
   int p2 = 2;
   while (p2 < kc) p2 <<= 1;
-  for (int i = tid; i < p2; i += bd)
-    B.c[i] = (i < kc) ? cs[beg + i] : make_int4(x, 0x7f800000, (int)0xff800000, INT_MAX);   // +inf cost: last
-  __syncthreads();
+  const int4 pad = make_int4(x, 0x7f800000, (int)0xff800000, INT_MAX);   // +inf cost: sorts last
   // 1. bitonic sort ascending by (cost, -h, parent)
+  if (p2 <= bd) {
+    // one element per thread in registers: partners closer than 32 by
+    // shuffles, farther ones through two alternating shared-memory buffers
+    // (one barrier per such step); the same compare-exchange network
+    int4 v = (tid < kc) ? cs[beg + tid] : pad;
+    int boff = 0;   // alternating halves B.c[0, bd) and B.c[bd, 2 bd)
+    for (int k = 2; k <= p2; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        int4 o;
+        if (j >= 32) {
+          B.c[boff + tid] = v;
+          __syncthreads();
+          o = B.c[boff + (tid ^ j)];
+          boff ^= bd;
+        } else {
+          o = shfl_xor4(v, j);
+        }
+        // pair (i, i ^ j), i the lower index: swap iff cand_less(c[i ^ j], c[i]) == ((i & k) == 0)
+        const bool up = (tid & k) == 0;
+        const bool sw = ((tid & j) == 0) ? (cand_less(o, v) == up) : (cand_less(v, o) == up);
+        if (sw) v = o;
+      }
+    }
+    __syncthreads();   // the last exchange buffer's reads are done
+    if (tid < p2) B.c[tid] = v;
+    __syncthreads();
+  } else {
+  for (int i = tid; i < p2; i += bd) B.c[i] = (i < kc) ? cs[beg + i] : pad;
+  __syncthreads();
   for (int k = 2; k <= p2; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int i = tid; i < p2; i += bd) {
@@ -468,6 +500,7 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
       }
       __syncthreads();
     }
+  }
   }
   // 2. survivors: prefix min of h and equal-cost group starts
   int4 cq[EC];
@@ -623,10 +656,6 @@ struct MidSmem {
 };
 static_assert(sizeof(MidSmem) * (kST / 32) <= sizeof(BigSmem), "mid-merge slices must fit the CTA merge buffer");
 
-__device__ __forceinline__ int4 shfl_xor4(const int4& v, int j) {
-  return make_int4(__shfl_xor_sync(FULLM, v.x, j), __shfl_xor_sync(FULLM, v.y, j), __shfl_xor_sync(FULLM, v.z, j),
-                   __shfl_xor_sync(FULLM, v.w, j));
-}
 
 __device__ void warp_mid_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* cs, const int32_t* coff,
                                const int32_t* ccnt, float2* sch, int32_t* sid, int32_t* sn, int4* labels,
