@@ -36,8 +36,11 @@
 namespace mpap {
 
 #define FULL 0xffffffffu
+#ifndef MPAP_FOLD_SMEM_TRAJ
+#define MPAP_FOLD_SMEM_TRAJ 1
+#endif
 #ifndef MPAP_FOLD_MIN_BLOCKS
-#define MPAP_FOLD_MIN_BLOCKS 4
+#define MPAP_FOLD_MIN_BLOCKS 3
 #endif
 #ifndef MPAP_EDGES_MIN_BLOCKS
 #define MPAP_EDGES_MIN_BLOCKS 4
@@ -1418,6 +1421,11 @@ __global__ void __launch_bounds__(kFoldThreads, MPAP_FOLD_MIN_BLOCKS) k_fold(con
   // rounded division the step would do (a lookup instead of a DDIV per step)
   constexpr int kZ2 = 256;
   __shared__ double s_z2[kZ2];
+#if MPAP_FOLD_SMEM_TRAJ
+  // the thread's velocity polynomial v(t) = v0 + t (2 c2 + t 3 c3) per axis,
+  // kept in shared memory (its registers go to the two MLP evaluations)
+  __shared__ double s_tr[(HEUR == 3 && DYN == 1) ? 3 * D : 1][kFoldThreads];
+#endif
   if (HEUR == 3) {
     for (int i = threadIdx.x; i < kZ2; i += blockDim.x) s_z2[i] = (double)i / P.n_f;
   }
@@ -1456,6 +1464,16 @@ __global__ void __launch_bounds__(kFoldThreads, MPAP_FOLD_MIN_BLOCKS) k_fold(con
 #pragma unroll
   for (int j = 0; j < D; ++j) { c2[j] = 0.0; c3[j] = 0.0; }
   if (HEUR == 3 && DYN == 1) di_traj<D>(su_l, sv_l, T, c2, c3);
+#if MPAP_FOLD_SMEM_TRAJ
+  if (HEUR == 3 && DYN == 1) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {   // the factors di_vel forms per call (the same products)
+      s_tr[j][threadIdx.x] = 3.0 * c3[j];
+      s_tr[D + j][threadIdx.x] = 2.0 * c2[j];
+      s_tr[2 * D + j][threadIdx.x] = su_l[D + j];
+    }
+  }
+#endif
   const bool unit_vref = P.v_ref == 1.0;
   const double z1 = omega / P.w_ref;   // per-edge MLP input (one division per edge)
   const uint16_t* kvp = kvbuf + koff[e];
@@ -1482,7 +1500,13 @@ __global__ void __launch_bounds__(kFoldThreads, MPAP_FOLD_MIN_BLOCKS) k_fold(con
           if (DYN == 1) {
             const double t = (double)k * Dl;
             double vel[D];
+#if MPAP_FOLD_SMEM_TRAJ
+#pragma unroll
+            for (int j = 0; j < D; ++j)   // = di_vel: fma(t, fma(t, 3 c3, 2 c2), v0)
+              vel[j] = fma(t, fma(t, s_tr[j][threadIdx.x], s_tr[D + j][threadIdx.x]), s_tr[2 * D + j][threadIdx.x]);
+#else
             di_vel<D>(su_l, c2, c3, t, vel);
+#endif
             double ss = 0.0;
 #pragma unroll
             for (int j = 0; j < D; ++j) ss = fma(vel[j], vel[j], ss);
