@@ -36,6 +36,9 @@
 namespace mpap {
 
 #define FULL 0xffffffffu
+#ifndef MPAP_NEAR_F32
+#define MPAP_NEAR_F32 1      // k_near's level-2 interval filter in single precision with certified margins
+#endif
 #ifndef MPAP_FOLD_SMEM_TRAJ
 #define MPAP_FOLD_SMEM_TRAJ 1
 #endif
@@ -218,6 +221,9 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_near(const double* __restri
   // interval tables of the level-2 filter: [level][interval] = {ta, tb, 1/tb, 1/tb^3}
   // for the whole range (level 0), quarters (1) and sixteenths (2) of (0, r]
   __shared__ double s_near[3][16][4];
+#if MPAP_NEAR_F32
+  __shared__ float4 s_nearf[3][16];   // the same table in single precision (the FP32 filter)
+#endif
   if (DYN == 1 && threadIdx.x < 21) {
     const int t = threadIdx.x;
     const int lvl = (t == 0) ? 0 : (t < 5) ? 1 : 2;
@@ -229,6 +235,9 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_near(const double* __restri
     s_near[lvl][jj][1] = tb;
     s_near[lvl][jj][2] = 1.0 / tb;
     s_near[lvl][jj][3] = 1.0 / (tb * tb * tb);
+#if MPAP_NEAR_F32
+    s_nearf[lvl][jj] = make_float4((float)ta, (float)tb, (float)(1.0 / tb), (float)(1.0 / (tb * tb * tb)));
+#endif
   }
   __syncthreads();
   const int b = blockIdx.y;
@@ -285,6 +294,9 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_near(const double* __restri
     const double bp = (sqrt(v02) * r + r * r / sqrt(3.0 * ru)) * (1.0 + 1e-9);
     const double bv = (r / (2.0 * sqrt(ru))) * (1.0 + 1e-9);
     const double bp2 = bp * bp, bv2 = bv * bv;
+#if MPAP_NEAR_F32
+    const float ruf = (float)ru, rf = __double2float_ru(r);
+#endif
     int qn = 0;
     auto process = [&](int k) {
       bool ok = false;
@@ -334,10 +346,31 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_near(const double* __restri
             ss += e * e;
             as += a * e;
           }
-          const double tv = (ss > 0.0) ? 2.0 * as / ss : 0.0;   // vertex of the quadratic
           // Lower bound of c on [ta, tb] (reciprocals of tb from the block's
           // table): tested on [0, r], then on its 4 quarters, then on the 4
           // sixteenths of each quarter that is still possible.
+#if MPAP_NEAR_F32
+          // The same bound in single precision, made conservative (DESIGN.md
+          // §7): g2 is lowered by 1e-6 of the magnitude of its terms (> 16
+          // float roundings of the conversions and the 5 operations), L by a
+          // further 1e-6 relative (the table's and r_u's roundings), and r is
+          // rounded up.  The float clamped vertex moves g by O(ss eps^2 r^2),
+          // far inside the margin.  A pair with a tiny ss (float underflow)
+          // is kept.
+          const float dp2f = (float)dp2, asf = (float)as, ssf = (float)ss, dv2f = (float)dv2;
+          const bool ss_ok = ssf > 1e-30f || ss == 0.0;
+          const float tvf = (ssf > 1e-30f) ? 2.0f * asf / ssf : 0.0f;
+          auto possible_on = [&](int lvl, int jj) -> bool {
+            const float4 tt = s_nearf[lvl][jj];   // ta, tb, 1/tb, 1/tb^3
+            const float tq = fminf(fmaxf(tvf, tt.x), tt.y);
+            const float t1 = tq * asf, t2 = tq * tq * ssf * 0.25f;
+            const float g2 = dp2f - t1 + t2;
+            const float g2lo = fmaxf(g2 - 1e-6f * (dp2f + fabsf(t1) + t2), 0.0f);
+            const float L = tt.x + ruf * (12.0f * g2lo * tt.w + dv2f * tt.z);
+            return !ss_ok || L * (1.0f - 1e-6f) < rf;
+          };
+#else
+          const double tv = (ss > 0.0) ? 2.0 * as / ss : 0.0;   // vertex of the quadratic
           auto possible_on = [&](int lvl, int jj) -> bool {
             const double ta = s_near[lvl][jj][0], tb = s_near[lvl][jj][1];
             const double tq = dmin(dmax(tv, ta), tb);   // finite operands: no NaN handling needed
@@ -345,6 +378,7 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_near(const double* __restri
             const double L = ta + ru * (12.0 * g2 * s_near[lvl][jj][3] + dv2 * s_near[lvl][jj][2]);
             return L * (1.0 - 1e-9) < r;
           };
+#endif
           bool possible = false;
           if (possible_on(0, 0)) {
             for (int q = 0; q < 4 && !possible; ++q) {
