@@ -644,6 +644,26 @@ __device__ __forceinline__ unsigned seg_hits_boxes(const double* A, const double
   return tests << 1;
 }
 
+// di_traj (traj.cuh) for a whole warp: lane j < D forms c2[j], lane D + j
+// forms c3[j] -- the same expressions, one division per lane instead of 2 D
+// in sequence -- and every lane receives all of them.
+template <int D>
+__device__ __forceinline__ void di_traj_warp(const double* su, const double* sv, double tau, int lane, double* c2,
+                                             double* c3) {
+  const int j = (lane < D) ? lane : (lane < 2 * D) ? lane - D : 0;
+  const double tau2 = tau * tau;
+  const double tau3 = tau2 * tau;
+  const double dp = (sv[j] - su[j]) - su[D + j] * tau;
+  const double dl = sv[D + j] - su[D + j];
+  const double num = (lane < D) ? (3.0 * dp - dl * tau) : (dl * tau - 2.0 * dp);
+  const double q = num / ((lane < D) ? tau2 : tau3);
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    c2[i] = __shfl_sync(FULL, q, i);
+    c3[i] = __shfl_sync(FULL, q, D + i);
+  }
+}
+
 // Collision(u,v) of reading R8, warp-cooperative; every lane returns the result.
 template <int D, int DYN>
 __device__ __forceinline__ bool edge_collision(const DevParams& P, const double* su, const double* sv, double tau,
@@ -665,7 +685,7 @@ __device__ __forceinline__ bool edge_collision(const DevParams& P, const double*
     return false;
   }
   double c2[D], c3[D];
-  di_traj<D>(su, sv, tau, c2, c3);
+  di_traj_warp<D>(su, sv, tau, lane, c2, c3);
   const double kc = ceil(tau / P.collision_dt);
   const int Kc = (kc < 1.0) ? 1 : (int)kc;
   // bounding box of the polyline vertices P_0..P_Kc
@@ -687,6 +707,9 @@ __device__ __forceinline__ bool edge_collision(const DevParams& P, const double*
   const int nl = cull_boxes<D>(box, O, lo, hi, kCullMargin, L.box, lane);
   W.add(lane, W_CULL_TESTS, O);
   if (nl == 0) return false;
+  // segment k = [P_{k-1}, P_k]: each lane forms its end vertex P_k, the
+  // start vertex is the previous lane's (the previous chunk's last for lane
+  // 0, P_0 = p(0) first) -- the same values as forming both per lane
   for (int k0 = 1; k0 <= Kc; k0 += 32) {
     const int k = k0 + lane;
     bool hit = false;
@@ -828,7 +851,7 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
 #pragma unroll
     for (int j = 0; j < D; ++j) { t2[j] = 0.0; t3[j] = 0.0; q0[j] = -1.0; q1[j] = -1.0; }
     if (DYN == 1) {
-      di_traj<D>(su, sv, T, t2, t3);
+      di_traj_warp<D>(su, sv, T, lane, t2, t3);
       cubic_stationary<D>(su, t2, t3, q0, q1);
     }
     __syncwarp();
