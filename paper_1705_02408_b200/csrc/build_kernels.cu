@@ -36,6 +36,9 @@
 namespace mpap {
 
 #define FULL 0xffffffffu
+#ifndef MPAP_STAT_WARP
+#define MPAP_STAT_WARP 1
+#endif
 #ifndef MPAP_NEAR_F32
 #define MPAP_NEAR_F32 1      // k_near's level-2 interval filter in single precision with certified margins
 #endif
@@ -852,7 +855,33 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
     for (int j = 0; j < D; ++j) { t2[j] = 0.0; t3[j] = 0.0; q0[j] = -1.0; q1[j] = -1.0; }
     if (DYN == 1) {
       di_traj_warp<D>(su, sv, T, lane, t2, t3);
+#if MPAP_STAT_WARP
+      {   // stationary points: lane j < D solves axis j (cubic_stationary's expressions), then shuffles
+        double a2 = t2[0], a3 = t3[0];
+#pragma unroll
+        for (int i = 1; i < D; ++i)
+          if (lane == i) { a2 = t2[i]; a3 = t3[i]; }
+        const double A = 3.0 * a3, Bq = 2.0 * a2, Cq = su[D + ((lane < D) ? lane : 0)];
+        double x0 = -1.0, x1 = -1.0;
+        if (A != 0.0) {
+          const double disc = Bq * Bq - 4.0 * A * Cq;
+          if (disc >= 0.0) {
+            const double sq = sqrt(disc);
+            x0 = (-Bq - sq) / (2.0 * A);
+            x1 = (-Bq + sq) / (2.0 * A);
+          }
+        } else if (Bq != 0.0) {
+          x0 = -Cq / Bq;
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          q0[i] = __shfl_sync(FULL, x0, i);
+          q1[i] = __shfl_sync(FULL, x1, i);
+        }
+      }
+#else
       cubic_stationary<D>(su, t2, t3, q0, q1);
+#endif
     }
     __syncwarp();
     if (lane == 0) {
