@@ -36,6 +36,9 @@
 namespace mpap {
 
 #define FULL 0xffffffffu
+#ifndef MPAP_BBOX_WARP
+#define MPAP_BBOX_WARP 1
+#endif
 #ifndef MPAP_STAT_WARP
 #define MPAP_STAT_WARP 1
 #endif
@@ -832,6 +835,43 @@ __device__ __forceinline__ void chunk_bbox(const double* su, const double* sv, c
   }
 }
 
+// chunk_bbox with lane j < D forming axis j (the same expressions: di_pos's
+// component j, the stationary points' values), then shuffles.
+template <int D, int DYN>
+__device__ __forceinline__ void chunk_bbox_warp(const double* su, const double* sv, const double* c2,
+                                                const double* c3, const double* r0, const double* r1, double T,
+                                                double ta, double tb, int lane, double* lo, double* hi) {
+  const int j = (lane < D) ? lane : 0;
+  double xa, xb;
+  if (DYN == 0) {
+    const double sa = ta / T, sb = tb / T;
+    xa = fma(sa, sv[j] - su[j], su[j]);
+    xb = fma(sb, sv[j] - su[j], su[j]);
+  } else {
+    xa = fma(ta, fma(ta, fma(ta, c3[j], c2[j]), su[D + j]), su[j]);
+    xb = fma(tb, fma(tb, fma(tb, c3[j], c2[j]), su[D + j]), su[j]);
+  }
+  double l = dmin(xa, xb), h = dmax(xa, xb);
+  if (DYN == 1) {
+    const double a0 = r0[j], a1 = r1[j];
+    if (a0 > ta && a0 < tb) {
+      const double x = fma(a0, fma(a0, fma(a0, c3[j], c2[j]), su[D + j]), su[j]);
+      l = dmin(l, x);
+      h = dmax(h, x);
+    }
+    if (a1 > ta && a1 < tb) {
+      const double x = fma(a1, fma(a1, fma(a1, c3[j], c2[j]), su[D + j]), su[j]);
+      l = dmin(l, x);
+      h = dmax(h, x);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    lo[i] = __shfl_sync(FULL, l, i);
+    hi[i] = __shfl_sync(FULL, h, i);
+  }
+}
+
 // Visible-feature counts of a collision-free edge (the k_v of P:324-328, per
 // step of reading R9).  Steps are processed 32 at a time (one per lane).  Per
 // chunk every lane computes the chunk's bounding box and heading arc
@@ -913,7 +953,11 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
     const int nk = min(32, K - k0);
     const double ta = (double)k0 * Dl, tb = (double)(k0 + nk - 1) * Dl;
     double lo[D], hi[D];
+#if MPAP_BBOX_WARP
+    chunk_bbox_warp<D, DYN>(su, sv, c2, c3, r0, r1, T, ta, tb, lane, lo, hi);
+#else
     chunk_bbox<D, DYN>(su, sv, c2, c3, r0, r1, T, ta, tb, lo, hi);
+#endif
     // Heading arc of the chunk (heading heuristics): the step headings lie on
     // the chord between the interpolated headings at the chunk's first and
     // last step, so their directions are within dev of the chord's mid
