@@ -475,7 +475,8 @@ struct WarpLists {
   unsigned long long* fmask;    // [F_max] per-feature box masks
   float4* fenv;                 // [F_max] the current environment's features (float x, y, z), staged per env
   float* boxf;                  // [O_max][2D] the chunk's culled boxes (float), for the occluder masks
-  int* fidx;                    // [F_max] the chunk's kept features' indices into fenv
+  int* fidx;                    // [F_max] the chunk's kept features' indices into fenv (MPAP_FMASK_F32), or
+                                //         the edge's range candidates (MPAP_CULL_EDGE)
   const float* arc;             // [2] cos, sin of the bearing cull's half angle (block-shared)
 };
 #ifndef MPAP_CULL_FENV
@@ -490,6 +491,9 @@ struct WarpLists {
 #ifndef MPAP_CULL_BRANCHFREE
 #define MPAP_CULL_BRANCHFREE 1   // bearing cull evaluated by every lane (no divergent branches)
 #endif
+#ifndef MPAP_CULL_EDGE
+#define MPAP_CULL_EDGE 1     // feature range cull per edge first, each chunk's range cull over the edge's list
+#endif
 #ifndef MPAP_FMASK_F32
 #define MPAP_FMASK_F32 0     // occluder masks in single precision, lanes over boxes (measured slower: 177.4 -> 196.3 ms)
 #endif
@@ -499,7 +503,7 @@ struct WarpLists {
 //   boxf[os][2D] float (MPAP_FMASK_F32), fidx[fs] int (both).
 __host__ __device__ constexpr size_t warp_scratch_doubles(int D, size_t fs, size_t os) {
   return fs * (D + 1) + os * 2 * D + (MPAP_CULL_FENV ? fs * 2 : 0) + (MPAP_FMASK_F32 ? os * D : 0) +
-         ((MPAP_CULL_FENV && MPAP_FMASK_F32) ? fs / 2 : 0);
+         ((MPAP_CULL_FENV && (MPAP_FMASK_F32 || MPAP_CULL_EDGE)) ? fs / 2 : 0);
 }
 __host__ __device__ constexpr size_t round4(int x) { return (size_t)((x + 3) & ~3); }
 
@@ -949,6 +953,38 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
   // computed once per block (k_edges)
   const float chf = (heur >= 2) ? L.arc[0] : 0.0f, shf = (heur >= 2) ? L.arc[1] : 0.0f;
   const float invT = 1.0f / (float)T;   // heading-arc parameters only (culling)
+#if MPAP_CULL_EDGE && MPAP_CULL_TWOSTAGE && MPAP_CULL_FENV && !MPAP_FMASK_F32
+  // Edge-level range candidates: features within R + 2e-3 of the bounding
+  // box of all the edge's steps (float test).  Every chunk box lies inside
+  // it up to rounding (~1e-14 m, and one float ulp ~2e-6 m after conversion),
+  // so a feature passing a chunk's range test (margin R + 1e-3) is on this
+  // list: the chunks' kept sets, in index order, are unchanged.
+  int* elist = L.fidx;
+  int ne = 0;
+  {
+    double elo[D], ehi[D];
+    chunk_bbox_warp<D, DYN>(su, sv, c2, c3, r0, r1, T, 0.0, (double)(K - 1) * Dl, lane, elo, ehi);
+    const float ax = (float)elo[0], bx = (float)ehi[0], ay = (float)elo[1], by = (float)ehi[1];
+    const float az = (D == 3) ? (float)elo[D - 1] : 0.0f, bz = (D == 3) ? (float)ehi[D - 1] : 0.0f;
+    const float me = (float)R + 2e-3f, me2 = me * me;
+    __syncwarp();
+    for (int f0 = 0; f0 < F; f0 += 32) {
+      const int f = f0 + lane;
+      bool keep = false;
+      if (f < F) {
+        const float4 fv = L.fenv[f];
+        const float ex = fmaxf(fmaxf(ax - fv.x, fv.x - bx), 0.0f);
+        const float ey = fmaxf(fmaxf(ay - fv.y, fv.y - by), 0.0f);
+        const float ez = (D == 3) ? fmaxf(fmaxf(az - fv.z, fv.z - bz), 0.0f) : 0.0f;
+        keep = ex * ex + ey * ey + ez * ez <= me2;
+      }
+      const unsigned msk = __ballot_sync(FULL, keep);
+      if (keep) elist[ne + __popc(msk & lt)] = f;
+      ne += __popc(msk);
+    }
+    __syncwarp();
+  }
+#endif
   for (int k0 = 0; k0 < K; k0 += 32) {
     const int nk = min(32, K - k0);
     const double ta = (double)k0 * Dl, tb = (double)(k0 + nk - 1) * Dl;
@@ -1018,10 +1054,17 @@ __device__ void edge_visible(const DevParams& P, const double* su, const double*
       // every lane busy
       int* rsel = reinterpret_cast<int*>(L.fmask);
       int nr = 0;
+#if MPAP_CULL_EDGE && !MPAP_FMASK_F32
+      for (int i0 = 0; i0 < ne; i0 += 32) {
+        const int f = (i0 + lane < ne) ? elist[i0 + lane] : 0;
+        bool keep = false;
+        if (i0 + lane < ne) {
+#else
       for (int f0 = 0; f0 < F; f0 += 32) {
         const int f = f0 + lane;
         bool keep = false;
         if (f < F) {
+#endif
           const float4 fv = L.fenv[f];
           const float ex = fmaxf(fmaxf(flx - fv.x, fv.x - fhx), 0.0f);
           const float ey = fmaxf(fmaxf(fly - fv.y, fv.y - fhy), 0.0f);
@@ -1373,12 +1416,14 @@ __global__ void __launch_bounds__(kWarps * 32, EdgeBounds<PHASE>::kMin) k_edges(
   WarpLists<D> L;
   {
     const size_t fs = round4(f_max), os = round4(o_max);
-    double* base = smem + (size_t)warp * warp_scratch_doubles(D, fs, os);
+    // PHASE 0 (collision) stages only the culled boxes: its own, smaller
+    // per-warp slice (more of the SM's L1 stays cache)
+    double* base = smem + (size_t)warp * (PHASE == 0 ? os * 2 * D : warp_scratch_doubles(D, fs, os));
     L.fxy = reinterpret_cast<double2*>(base);   // (x, y) pairs
     L.f[0] = base;                               // (x, y) strided: accessed through FREF
     L.f[1] = base + 1;
     if (D == 3) L.f[D - 1] = base + 2 * fs;      // z
-    L.box = base + (size_t)D * fs;
+    L.box = (PHASE == 0) ? base : base + (size_t)D * fs;
     L.fmask = reinterpret_cast<unsigned long long*>(L.box + os * 2 * D);
     double* nxt = reinterpret_cast<double*>(L.fmask + fs);
     L.fenv = reinterpret_cast<float4*>(nxt);
@@ -1931,7 +1976,8 @@ size_t edges_smem(const mpap_roadmap* rm);
 cudaError_t edge_phases(size_t smem, cudaStream_t st, const mpap_roadmap* rm, EdgeWork ew) {
   {
     ProfScope ps("k_collide", st);
-    cudaError_t e = launch_edges_any(0, smem, st, rm, ew);
+    const size_t smem0 = sizeof(double) * (size_t)kWarps * round4(rm->o_max) * 2 * rm->prm.pos_dim;
+    cudaError_t e = launch_edges_any(0, smem0, st, rm, ew);
     if (e != cudaSuccess) return e;
   }
   note_launch();
