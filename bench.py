@@ -56,8 +56,8 @@ FP64_LANES_PER_SM = 64
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mpap", choices=["mpap", "reference"])
     ap.add_argument("--config", default="c5")
     ap.add_argument("--queries-per-gpu", type=int, default=0)
@@ -472,6 +472,7 @@ def main():
         "feasible_fraction": feasible_all / (world * Q), "all_status_ok": ok,
         "roofline": roof, "fp64_peak_measured": fp64, "gpu_launches": int(launches), "clocks": clocks,
         "wall_s": wall, "step_ms": [round(x, 3) for x in step_ms],
+        "step_ms_stats": step_stats(step_ms),
         "step_host_ms": [round(x, 3) for x in host_ms],
         "search_teams": mp.mpap_search_launches(),
         "parity_gate": gate,
@@ -838,6 +839,15 @@ def measure_mc(mp, B, betas, path_cap: int, trials: int, with_cpu: bool):
 # Algorithmic FP64 operations per counted unit (+, -, *, /, sqrt, min/max,
 # compare and FMA each = 1), read off the kernels' source.
 # D = 3, double integrator, heading + MLP heuristic (the C5 workload).
+def step_stats(ms: list) -> dict:
+    """Median, min and p90 (nearest rank) of this rank's timed steps (SURVEY 8(d) timing)."""
+    xs = sorted(ms)
+    if not xs:
+        return {}
+    p90 = xs[min(len(xs) - 1, max(0, math.ceil(0.9 * len(xs)) - 1))]
+    return {"median": round(statistics.median(xs), 3), "min": round(xs[0], 3), "p90": round(p90, 3)}
+
+
 def fp64_ops(kernel: str, w: dict, D: int = 3) -> float:
     if kernel == "k_near":
         return 18 * w["pairs"] + 101 * w["prefilter_pass"] + 9 * w["bisect_iters"]
