@@ -382,58 +382,44 @@ __device__ __forceinline__ int block_excl_sum(int v, int* scr, int* total) {
   __syncthreads();
   return r;
 }
-__device__ __forceinline__ float block_excl_min(float v, float* scr) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
-  float x = v;
-  for (int o = 1; o < 32; o <<= 1) {
-    const float y = __shfl_up_sync(FULLM, x, o);
-    if (lane >= o) x = fminf(x, y);
-  }
-  const float ex = __shfl_up_sync(FULLM, x, 1);
-  if (lane == 31) scr[w] = x;
-  __syncthreads();
-  if (w == 0) {
-    float t = lane < nwb ? scr[lane] : __int_as_float(0x7f800000);
-    for (int o = 1; o < 32; o <<= 1) {
-      const float y = __shfl_up_sync(FULLM, t, o);
-      if (lane >= o) t = fminf(t, y);
-    }
-    scr[lane] = t;
-  }
-  __syncthreads();
-  float r = (lane > 0) ? ex : __int_as_float(0x7f800000);
-  if (w > 0) r = fminf(r, scr[w - 1]);
-  __syncthreads();
-  return r;
-}
-__device__ __forceinline__ int block_excl_max(int v, int* scr) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
-  int x = v;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(FULLM, x, o);
-    if (lane >= o) x = max(x, y);
-  }
-  const int ex = __shfl_up_sync(FULLM, x, 1);
-  if (lane == 31) scr[w] = x;
-  __syncthreads();
-  if (w == 0) {
-    int t = lane < nwb ? scr[lane] : INT_MIN;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(FULLM, t, o);
-      if (lane >= o) t = max(t, y);
-    }
-    scr[lane] = t;
-  }
-  __syncthreads();
-  int r = (lane > 0) ? ex : INT_MIN;
-  if (w > 0) r = max(r, scr[w - 1]);
-  __syncthreads();
-  return r;
-}
-
 __device__ __forceinline__ int4 shfl_xor4(const int4& v, int j) {
   return make_int4(__shfl_xor_sync(FULLM, v.x, j), __shfl_xor_sync(FULLM, v.y, j), __shfl_xor_sync(FULLM, v.z, j),
                    __shfl_xor_sync(FULLM, v.w, j));
+}
+
+// Block-wide exclusive prefix minimum (float) and maximum (int) in one pass.
+__device__ __forceinline__ void block_excl_min_max(float vmin, int vmax, float* fscr, int* iscr, float& rmin,
+                                                   int& rmax) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  float x = vmin;
+  int y = vmax;
+  for (int o = 1; o < 32; o <<= 1) {
+    const float a = __shfl_up_sync(FULLM, x, o);
+    const int b = __shfl_up_sync(FULLM, y, o);
+    if (lane >= o) { x = fminf(x, a); y = max(y, b); }
+  }
+  const float ex = __shfl_up_sync(FULLM, x, 1);
+  const int ey = __shfl_up_sync(FULLM, y, 1);
+  if (lane == 31) { fscr[w] = x; iscr[w] = y; }
+  __syncthreads();
+  if (w == 0) {
+    float t = lane < nwb ? fscr[lane] : __int_as_float(0x7f800000);
+    int u = lane < nwb ? iscr[lane] : INT_MIN;
+    for (int o = 1; o < 32; o <<= 1) {
+      const float a = __shfl_up_sync(FULLM, t, o);
+      const int b = __shfl_up_sync(FULLM, u, o);
+      if (lane >= o) { t = fminf(t, a); u = max(u, b); }
+    }
+    fscr[lane] = t;
+    iscr[lane] = u;
+  }
+  __syncthreads();
+  float r = (lane > 0) ? ex : __int_as_float(0x7f800000);
+  int q = (lane > 0) ? ey : INT_MIN;
+  if (w > 0) { r = fminf(r, fscr[w - 1]); q = max(q, iscr[w - 1]); }
+  __syncthreads();
+  rmin = r;
+  rmax = q;
 }
 
 __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* cs, const int32_t* coff,
@@ -515,8 +501,9 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
       if (i == 0 || __int_as_float(B.c[i - 1].y) != __int_as_float(cq[r].y)) lmax = i;
     }
   }
-  float run = block_excl_min(lmin, B.fscr);
-  int gstart = block_excl_max(lmax, B.iscr);
+  float run;
+  int gstart;
+  block_excl_min_max(lmin, lmax, B.fscr, B.iscr, run, gstart);
   if (gstart < 0) gstart = 0;
 #pragma unroll
   for (int r = 0; r < EC; ++r) {
