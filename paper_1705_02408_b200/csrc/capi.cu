@@ -288,8 +288,8 @@ static mpap_status check_env_sizes(int d, int64_t n_obstacles, int64_t n_feature
   if (n_features > 65535) return set_error(MPAP_ERR_INVALID_ARGUMENT, "more than 65535 features in one environment");
   // per warp at most fs (d + 3.5) + 3 d os doubles with fs, os = F, O rounded
   // up to a multiple of 4 (warp_scratch_doubles in build_kernels.cu: kept
-  // features, boxes, masks, float feature copies, the edge's feature list;
-  // + 3 d os / 2 more with the optional float box copies)
+  // features, masks, float feature copies and the edge's feature list make
+  // fs (d + 3.5); boxes 2 d os, plus d os for the optional float box copies)
   const int64_t fs = (n_features + 3) & ~3, os = (n_obstacles + 3) & ~3;
   const int64_t bytes = 4 * kEdgeWarps * (fs * (2 * d + 7) + os * 6 * d) + kStaticBytes;
   if (bytes > kSmemMax)
