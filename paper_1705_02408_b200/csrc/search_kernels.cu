@@ -42,6 +42,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "mpap_internal.cuh"
@@ -1488,6 +1489,18 @@ namespace {
 // Carves the per-launch slot arena: every array holds nslots consecutive
 // per-slot views (slot s at element offset s * cap), each array 256-B aligned.
 // With base == nullptr it only returns the byte count.
+// Process-wide capacity hints per device: the staircase / label / candidate
+// capacities earlier searches needed.  A fresh roadmap starts there when the
+// slot arena stays within kHintArenaBytes (fewer overflow reruns, the same
+// results: capacities never change what a search computes).
+struct CapHint {
+  int K = 0, L = 0, C = 0;
+};
+constexpr int kMaxDevices = 64;
+constexpr size_t kHintArenaBytes = size_t(4) << 30;
+CapHint g_cap_hint[kMaxDevices];
+std::mutex g_cap_mu;
+
 size_t carve(SearchArgs* A, const SlotCaps& c, int nslots, char* base) {
   size_t off = 0;
   auto take = [&](size_t per_slot) -> void* {
@@ -1629,6 +1642,19 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     while (csize > 2 && nrun * csize > nsm * occ) csize >>= 1;
     const bool cluster_mode = !grid_mode && use_cluster && (nrun * csize <= nsm * occ || rm->lazy);
     const int nslots = grid_mode ? 1 : cluster_mode ? nrun : std::min(nrun, nsm * occ);
+    if (round == 0 && dev >= 0 && dev < kMaxDevices && getenv("MPAP_SEARCH_NO_HINT") == nullptr) {
+      CapHint h;
+      {
+        std::lock_guard<std::mutex> lk(g_cap_mu);
+        h = g_cap_hint[dev];
+      }
+      SlotCaps t = caps;
+      t.L = std::max(t.L, h.L);
+      t.C = std::max(t.C, h.C);
+      t.K = std::max(t.K, h.K);
+      while (t.K > caps.K && carve(nullptr, t, nslots, nullptr) > kHintArenaBytes) t.K = std::max(caps.K, t.K / 2);
+      if (carve(nullptr, t, nslots, nullptr) <= kHintArenaBytes) caps = t;
+    }
     const size_t sb_slots = carve(nullptr, caps, nslots, nullptr);
     const size_t sb = sb_slots + sizeof(Ctl) * (size_t)nslots + 256;
     HostTimer ta("slot arena");
@@ -1774,6 +1800,13 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     rm->hint_K = std::max(rm->hint_K, caps.K);   // later searches on this roadmap start there
     rm->hint_L = std::max(rm->hint_L, caps.L);
     rm->hint_C = std::max(rm->hint_C, caps.C);
+    if (dev >= 0 && dev < kMaxDevices) {   // ... and, within the arena budget, later roadmaps
+      std::lock_guard<std::mutex> lk(g_cap_mu);
+      CapHint& h = g_cap_hint[dev];
+      h.K = std::max(h.K, caps.K);
+      h.L = std::max(h.L, caps.L);
+      h.C = std::max(h.C, caps.C);
+    }
     todo.swap(again);
   }
   if (status == MPAP_OK && !todo.empty()) status = set_error(MPAP_ERR_OUT_OF_MEMORY, "search capacity regrow limit");

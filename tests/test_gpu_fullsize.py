@@ -188,11 +188,16 @@ def test_full_csr_digests_c5_golden_envs(mp):
     rm.free()
 
 
-def test_c4_tightest_bound_single_query(mp):
+@pytest.mark.parametrize("hints", ["process", "none"])
+def test_c4_tightest_bound_single_query(mp, monkeypatch, hints):
     """C4 at 1.02 beta_min (the tightest bound of BASELINE.json configs[3]'s
     sweep): 105 waves, 2.1e8 relaxations, staircases of thousands of plans,
     so the CTA-cooperative and warp binary-search merges of large nodes run;
-    whole result and every per-wave counter vs the oracle's stored run."""
+    whole result and every per-wave counter vs the oracle's stored run.
+    With hints="none" (MPAP_SEARCH_NO_HINT) the fresh roadmap starts at the
+    default capacities, so the overflow -> regrow -> rerun path runs too."""
+    if hints == "none":
+        monkeypatch.setenv("MPAP_SEARCH_NO_HINT", "1")
     path = os.path.join(GOLDEN, "c4_tight.json")
     if not os.path.exists(path):
         pytest.skip("tests/golden/c4_tight.json not generated")
@@ -207,6 +212,8 @@ def test_c4_tightest_bound_single_query(mp):
         assert g["wave_counters"].tolist() == s["wave_counters"]
         assert g["path"].tolist() == s["path"]
         assert _hex(g["cost"]) == s["cost"] and _hex(g["h"]) == s["h"] and _hex(g["h_peak"]) == s["h_peak"]
+        if hints == "none":
+            assert g["retries"] >= 1   # thousands of plans per node overflow the default staircase capacity
     rm.free()
 
 
