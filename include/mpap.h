@@ -160,7 +160,12 @@ typedef struct {
   int32_t status;     /* mpap_status of this query (OK or NO_FEASIBLE_PLAN ...)     */
   int32_t path_len;   /* nodes in the plan, start first (0 if no plan)              */
   int32_t waves;      /* non-empty groups expanded (reading R24)                    */
-  int32_t retries;    /* capacity regrow-and-rerun rounds used (exact)              */
+  int32_t retries;    /* capacity regrow-and-rerun rounds used (exact).  A search
+                         starts at the capacities earlier searches on the same
+                         roadmap needed, or, while its slot arena stays under 4
+                         GB, earlier searches on the device (env
+                         MPAP_SEARCH_NO_HINT=1 disables the latter); capacities
+                         never change a result, only this count and the time  */
   float cost;         /* plan cost p.cost (f32 sum along the path, N5)               */
   float h;            /* plan perception value p.h (A3.21; R25)                      */
   float h_peak;       /* max node-prefix h along the plan (<= beta) (R25)            */
