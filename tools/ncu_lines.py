@@ -17,7 +17,10 @@ for w in ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram
           "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
           "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
           "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
-          "smsp__thread_inst_executed_per_inst_executed.ratio", "sm__throughput.avg.pct_of_peak_sustained_elapsed"]:
+          "smsp__thread_inst_executed_per_inst_executed.ratio", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+          "FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram__bytes.sum.per_second",
+          "lts__t_sectors.sum", "lts__t_sector_hit_rate.pct",
+          "l1tex__t_sector_hit_rate.pct"]:
     if w in h:
         print(f"{w} = {v[h.index(w)]} {rows[1][h.index(w)]}".rstrip())
 src = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv", "--print-source", "cuda,sass"],
