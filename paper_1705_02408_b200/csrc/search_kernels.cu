@@ -47,6 +47,10 @@
 
 #include "mpap_internal.cuh"
 
+#ifndef MPAP_MERGE_RANKSORT
+#define MPAP_MERGE_RANKSORT 1   // CTA merge: warp sorts + rank merge (else one bitonic network)
+#endif
+
 namespace mpap {
 namespace cg = cooperative_groups;
 
@@ -192,6 +196,11 @@ __device__ unsigned long long g_dcheck_fail = 0;
 // each phase barrier, and the merge work split.
 constexpr int kPhaseWaves = 256;
 __device__ unsigned long long g_phase[kPhaseWaves][8];
+// debug builds: cycles of cta_merge's steps summed over large nodes (thread 0's
+// clock: load+sort, survivors, kills, merged order + labels, tail), and count
+__device__ unsigned long long g_merge_cyc[6];
+#define MERGE_MARK(i) do { if (MPAP_DEBUG_CHECKS && tid == 0) { const unsigned long long c_ = clock64(); \
+    atomicAdd(&g_merge_cyc[i], c_ - mk_); mk_ = c_; } } while (0)
 __device__ int g_phase_stat[kPhaseWaves][4];   // nbig, nsmall, max candidates, max staircase of a big node
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -431,6 +440,7 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
   BigSmem& B = *reinterpret_cast<BigSmem*>(s_dyn);
   const int tid = threadIdx.x, bd = blockDim.x;
   constexpr int EC = kBigC / kST, EM = kBigM / kST;   // elements per thread
+  unsigned long long mk_ = MPAP_DEBUG_CHECKS ? clock64() : 0ull;
   const int kc = ccnt[x];
   const int beg = coff[x] - kc;
   const int snx = sn[x];
@@ -444,6 +454,41 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
   while (p2 < kc) p2 <<= 1;
   const int4 pad = make_int4(x, 0x7f800000, (int)0xff800000, INT_MAX);   // +inf cost: sorts last
   // 1. bitonic sort ascending by (cost, -h, parent)
+#if MPAP_MERGE_RANKSORT
+  if (p2 <= bd) {
+    // one element per thread: each warp sorts its 32 by shuffles (bitonic),
+    // then every element's rank = its place in its run + how many elements
+    // of each other run precede it (binary searches in shared memory; the
+    // order is strict on candidates, pads sort last and rank >= kc)
+    int4 v = (tid < kc) ? cs[beg + tid] : pad;
+    const int lane = tid & 31, w = tid >> 5, nr = (p2 + 31) >> 5;
+    for (int k = 2; k <= 32; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const int4 o = shfl_xor4(v, j);
+        const bool up = (lane & k) == 0;
+        const bool sw = ((lane & j) == 0) ? (cand_less(o, v) == up) : (cand_less(v, o) == up);
+        if (sw) v = o;
+      }
+    }
+    int4* runs = B.c + bd;
+    runs[tid] = v;
+    __syncthreads();
+    if (w < nr) {
+      int rank = lane;
+      for (int r = 0; r < nr; ++r) {
+        if (r == w) continue;
+        const int4* rr = runs + r * 32;
+        int lo = 0, hi = 32;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (cand_less(rr[mid], v)) lo = mid + 1; else hi = mid;
+        }
+        rank += lo;
+      }
+      if (rank < kc) B.c[rank] = v;
+    }
+    __syncthreads();
+#else
   if (p2 <= bd) {
     // one element per thread in registers: partners closer than 32 by
     // shuffles, farther ones through two alternating shared-memory buffers
@@ -470,6 +515,7 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
     __syncthreads();   // the last exchange buffer's reads are done
     if (tid < p2) B.c[tid] = v;
     __syncthreads();
+#endif
   } else {
   for (int i = tid; i < p2; i += bd) B.c[i] = (i < kc) ? cs[beg + i] : pad;
   __syncthreads();
@@ -489,6 +535,7 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
     }
   }
   }
+  MERGE_MARK(0);
   // 2. survivors: prefix min of h and equal-cost group starts
   int4 cq[EC];
   float lmin = __int_as_float(0x7f800000);
@@ -535,6 +582,7 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
   for (int r = 0; r < EC; ++r)
     if (surv[r]) B.c[spos++] = cq[r];
   __syncthreads();
+  MERGE_MARK(1);
   // 3. kills of old entries
   bool alive[EM];
   int aloc = 0;
@@ -576,6 +624,7 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
     B.bc[0] = atomicAdd(&S->nlabels, ns);
   }
   __syncthreads();
+  MERGE_MARK(2);
   // 4. merged staircase in the other buffer; survivors get labels
 #pragma unroll
   for (int r = 0; r < EM; ++r) {
@@ -622,6 +671,7 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
       }
     }
   }
+  MERGE_MARK(3);
   if (tid == 0) {
     const int newm = na + ns;
     if (newm > C.K) atomicOr(&S->overflow, OVF_STAIR);
@@ -629,6 +679,8 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
     my_ins += (unsigned long long)ns;
   }
   __syncthreads();   // B is reused by the CTA's next large node
+  MERGE_MARK(4);
+  if (MPAP_DEBUG_CHECKS && tid == 0) atomicAdd(&g_merge_cyc[5], 1ull);
 }
 
 // Warp merge of a node with <= 32 candidates and a staircase of up to kBigM
@@ -1847,6 +1899,13 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
               (ph[w][6] - ph[w][5]) * 1e-3, pst[w][0], pst[w][1], pst[w][2], pst[w][3]);
     std::memset(pst, 0, sizeof(pst));
     CKS(cudaMemcpyToSymbol(g_phase_stat, pst, sizeof(pst)));
+    unsigned long long mc[6];
+    CKS(cudaMemcpyFromSymbol(mc, g_merge_cyc, sizeof(mc)));
+    const double nn = (double)std::max(mc[5], 1ull);
+    fprintf(stderr, "[merge] large nodes %llu, cycles per node: load+sort %.0f survivors %.0f kills %.0f "
+            "order+labels %.0f tail %.0f\n", mc[5], mc[0] / nn, mc[1] / nn, mc[2] / nn, mc[3] / nn, mc[4] / nn);
+    std::memset(mc, 0, sizeof(mc));
+    CKS(cudaMemcpyToSymbol(g_merge_cyc, mc, sizeof(mc)));
   }
   if (MPAP_DEBUG_CHECKS) {
     unsigned long long fails = 0;
