@@ -47,6 +47,9 @@
 
 #include "mpap_internal.cuh"
 
+#ifndef MPAP_MERGE_MONO
+#define MPAP_MERGE_MONO 1   // CTA merge: per-thread bounds advance over consecutive old entries
+#endif
 #ifndef MPAP_MERGE_RANKSORT
 #define MPAP_MERGE_RANKSORT 1   // CTA merge: warp sorts + rank merge (else one bitonic network)
 #endif
@@ -586,17 +589,35 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
   // 3. kills of old entries
   bool alive[EM];
   int aloc = 0;
+#if MPAP_MERGE_MONO
+  int lo3 = -1;   // this thread's entries are consecutive and sorted: the bound only moves forward
+#endif
 #pragma unroll
   for (int r = 0; r < EM; ++r) {
     const int j = tid * EM + r;
     alive[r] = false;
     if (j < m) {
       const float2 o = st[j];
+#if MPAP_MERGE_MONO
+      int lo = lo3;   // first survivor with cost >= o.x
+      if (lo < 0) {
+        int hi = ns;
+        lo = 0;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (__int_as_float(B.c[mid].y) < o.x) lo = mid + 1; else hi = mid;
+        }
+      } else {
+        while (lo < ns && __int_as_float(B.c[lo].y) < o.x) ++lo;
+      }
+      lo3 = lo;
+#else
       int lo = 0, hi = ns;   // first survivor with cost >= o.x
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
         if (__int_as_float(B.c[mid].y) < o.x) lo = mid + 1; else hi = mid;
       }
+#endif
       const bool dead = lo > 0 && __int_as_float(B.c[lo - 1].z) <= o.y;
       alive[r] = !dead;
       aloc += alive[r] ? 1 : 0;
@@ -626,16 +647,34 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
   __syncthreads();
   MERGE_MARK(2);
   // 4. merged staircase in the other buffer; survivors get labels
+#if MPAP_MERGE_MONO
+  int lo4 = -1;
+#endif
 #pragma unroll
   for (int r = 0; r < EM; ++r) {
     const int j = tid * EM + r;
     if (j < m && alive[r]) {
       const float2 o = st[j];
+#if MPAP_MERGE_MONO
+      int lo = lo4;   // survivors with key < o (non-decreasing over the thread's entries)
+      if (lo < 0) {
+        int hi = ns;
+        lo = 0;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (key_less(__int_as_float(B.c[mid].y), __int_as_float(B.c[mid].z), o.x, o.y)) lo = mid + 1; else hi = mid;
+        }
+      } else {
+        while (lo < ns && key_less(__int_as_float(B.c[lo].y), __int_as_float(B.c[lo].z), o.x, o.y)) ++lo;
+      }
+      lo4 = lo;
+#else
       int lo = 0, hi = ns;   // survivors with key < o
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
         if (key_less(__int_as_float(B.c[mid].y), __int_as_float(B.c[mid].z), o.x, o.y)) lo = mid + 1; else hi = mid;
       }
+#endif
       const int pos = B.ap[j] + lo;
       if (pos < C.K) {
         nst[pos] = o;
