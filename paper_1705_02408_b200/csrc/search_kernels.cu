@@ -47,6 +47,9 @@
 
 #include "mpap_internal.cuh"
 
+#ifndef MPAP_EXPAND_BATCH_META
+#define MPAP_EXPAND_BATCH_META 1   // expand: plan metadata loaded 32 plans per warp at a time
+#endif
 #ifndef MPAP_MERGE_MONO
 #define MPAP_MERGE_MONO 1   // CTA merge: per-thread bounds advance over consecutive old entries
 #endif
@@ -1000,6 +1003,108 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
     // ---- a7 expand (A3.6-A3.11): warp per plan of G_i, 32 edges per step ----
     {
       unsigned long long my_relax = 0, my_bpass = 0, my_t = 0, my_ss = 0;
+#if MPAP_EXPAND_BATCH_META
+      // the warp's plans k = warp, warp + nw, ... (the same sequence), their
+      // labels and CSR row bounds loaded 32 plans at a time (lane i: plan i of
+      // the batch) so the label -> row-pointer load chain is paid once per 32
+      for (int kb = warp; kb < gsize; kb += 32 * nw) {
+        const int kk = kb + lane * nw;
+        int p_l = 0;
+        int4 lb_l = make_int4(0, 0, 0, 0);
+        int64_t e0_l = 0, e1_l = 0;
+        if (kk < gsize) {
+          p_l = Gc[kk];
+          lb_l = labels[p_l];
+          e0_l = rp[lb_l.x];
+          e1_l = rp[lb_l.x + 1];
+        }
+        const int nbat = min(32, (gsize - kb + nw - 1) / nw);
+        for (int ib = 0; ib < nbat; ++ib) {
+          const int p = __shfl_sync(FULLM, p_l, ib);
+          const float pc = __int_as_float(__shfl_sync(FULLM, lb_l.z, ib));
+          const float ph = __int_as_float(__shfl_sync(FULLM, lb_l.w, ib));
+          const int64_t e0 = __shfl_sync(FULLM, e0_l, ib), e1 = __shfl_sync(FULLM, e1_l, ib);
+          for (int64_t eb = e0; eb < e1; eb += 32) {
+            const int64_t e = eb + lane;
+            bool fr = false, emit = false;
+            int x = 0;
+            float qc = 0.f, qh = 0.f;
+            if (e < e1) {
+              const uint4 raw = __ldg(reinterpret_cast<const uint4*>(A.edges) + e);
+              fr = (raw.x >> 31) == 0u;
+              if (fr) {
+                x = (int)(raw.x & 0x7fffffffu);
+                qc = pc + __uint_as_float(raw.y);
+                const float t = ph + __uint_as_float(raw.z);
+                const float cc = __uint_as_float(raw.w);
+                qh = (t > cc) ? t : cc;
+                bool ok = (double)qh <= beta;                      // A3.9 cutoff
+                if (forall_t && ok) {                              // every step of the edge
+                  const float2 pk = __ldg(A.peak + e);
+                  const float t2 = ph + pk.x;
+                  ok = (double)((t2 > pk.y) ? t2 : pk.y) <= beta;
+                }
+                if (ok) {
+                  ++my_bpass;
+                  const int snx = sn[x];
+                  const int m = snx & kStairCountMask;
+                  if (TRACE) {
+                    if (atomicExch(&stamp[x], wave) != wave) { ++my_t; my_ss += (unsigned long long)m; }
+                  }
+                  // dominated by the node's non-dominated staircase?  Such a
+                  // candidate cannot survive RemoveDominated (transitivity).  With
+                  // the staircase sorted, only the last entry of cost < qc matters.
+                  const float2* st = sch + stair_base(snx, x, n, C.K);
+                  // first index with cost >= qc; the wavefront's candidates are
+                  // usually costlier than the whole staircase, so its last entry
+                  // is checked first (one load instead of a log2(m)-deep search)
+                  int lo = 0, hi = m;
+                  float2 prev = make_float2(0.0f, __int_as_float(0x7f800000));
+                  if (m > 0) {
+                    const float2 last = st[m - 1];
+                    if (last.x < qc) {
+                      lo = m;
+                      prev = last;
+                    } else {
+                      hi = m - 1;
+                    }
+                  }
+                  while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (st[mid].x < qc) lo = mid + 1; else hi = mid;
+                  }
+                  if (lo > 0 && lo < m) prev = st[lo - 1];
+                  const bool dom = lo > 0 && prev.y <= qh;
+                  emit = !dom;
+                }
+              }
+            }
+            my_relax += __popc(__ballot_sync(FULLM, fr)) * (lane == 0 ? 1u : 0u);
+            const unsigned em = __ballot_sync(FULLM, emit);
+            if (em) {
+              int base = 0;
+              if (lane == 0) base = atomicAdd(&S->ncand, __popc(em));
+              base = __shfl_sync(FULLM, base, 0);
+              if (emit) {
+                const int idx = base + __popc(em & lt);
+                if (idx < C.C) {
+                  DCHECK(x >= 0 && x < n);
+                  cand[idx] = make_int4(x, __float_as_int(qc), __float_as_int(qh), p);
+                  if (atomicAdd(&ccnt[x], 1) == 0) {
+                    const int tpos = atomicAdd(&S->ntouched, 1);
+                    DCHECK(tpos < n);
+                    touched[tpos] = x;
+                  }
+                } else {
+                  atomicOr(&S->overflow, OVF_CAND);
+                }
+              }
+            }
+          }
+
+        }
+      }
+#else
       for (int k = warp; k < gsize; k += nw) {
         const int p = Gc[k];
         const int4 lb = labels[p];
@@ -1084,6 +1189,7 @@ __device__ void run_query(const Team& team, const SearchArgs& A, Ctl* S, int slo
           }
         }
       }
+#endif
       if (my_relax) atomicAdd(&S->relax, my_relax);
       if (my_bpass) atomicAdd(&S->bpass, my_bpass);
       if (TRACE) {
