@@ -1695,6 +1695,7 @@ struct CapHint {
 };
 constexpr int kMaxDevices = 64;
 constexpr size_t kHintArenaBytes = size_t(4) << 30;
+constexpr int kHintMaxSlots = 64;
 CapHint g_cap_hint[kMaxDevices];
 std::mutex g_cap_mu;
 
@@ -1839,7 +1840,10 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     while (csize > 2 && nrun * csize > nsm * occ) csize >>= 1;
     const bool cluster_mode = !grid_mode && use_cluster && (nrun * csize <= nsm * occ || rm->lazy);
     const int nslots = grid_mode ? 1 : cluster_mode ? nrun : std::min(nrun, nsm * occ);
-    if (round == 0 && dev >= 0 && dev < kMaxDevices && getenv("MPAP_SEARCH_NO_HINT") == nullptr) {
+    // (only for up to kHintMaxSlots slots: a many-slot arena seeded from a
+    // smaller batch's maxima kept growing the workspace step after step)
+    if (round == 0 && nslots <= kHintMaxSlots && dev >= 0 && dev < kMaxDevices &&
+        getenv("MPAP_SEARCH_NO_HINT") == nullptr) {
       CapHint h;
       {
         std::lock_guard<std::mutex> lk(g_cap_mu);
