@@ -1699,6 +1699,45 @@ constexpr int kHintMaxSlots = 64;
 CapHint g_cap_hint[kMaxDevices];
 std::mutex g_cap_mu;
 
+// Stream access-policy window (persisting hits) over [base, base + bytes),
+// clamped to the device's window and persisting-L2 limits; removed (and the
+// persisting lines released) when the object goes out of scope.
+struct L2Window {
+  cudaStream_t st;
+  bool on = false;
+  L2Window(cudaStream_t s, int dev, const void* base, size_t bytes, bool enable) : st(s) {
+    if (!enable || !base || bytes == 0) return;
+    int max_win = 0, max_persist = 0;
+    if (cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess ||
+        max_win <= 0 || max_persist <= 0) {
+      cudaGetLastError();
+      return;
+    }
+    const size_t win = std::min(bytes, (size_t)max_win);
+    const size_t persist = std::min(win, (size_t)max_persist);
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    v.accessPolicyWindow.num_bytes = win;
+    v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)persist / (double)win);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    on = cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
+    if (!on) cudaGetLastError();
+  }
+  ~L2Window() {
+    if (!on) return;
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaCtxResetPersistingL2Cache();
+  }
+};
+
 size_t carve(SearchArgs* A, const SlotCaps& c, int nslots, char* base) {
   size_t off = 0;
   auto take = [&](size_t per_slot) -> void* {
@@ -1825,6 +1864,11 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
   std::vector<int32_t> retries(nq, 0);
   std::vector<mpap_result> hres(nq);
   mpap_status status = MPAP_OK;
+  // L2 persistence for the CSR edge records (read by every expansion, the
+  // search's streamed data): an access-policy window on the stream for the
+  // duration of this call (MPAP_SEARCH_L2_PERSIST=1; measured)
+  L2Window l2w(st, dev, rm->d_edges, (size_t)rm->nnz_total * sizeof(EdgeRec),
+               getenv("MPAP_SEARCH_L2_PERSIST") != nullptr);
   for (int round = 0; round < 12 && !todo.empty(); ++round) {
     const int nrun = (int)todo.size();
     // one query: the whole grid works on it (cooperative launch); otherwise one
