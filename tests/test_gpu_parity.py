@@ -180,7 +180,13 @@ def _golden_check(mp, rm, prob, gold, env=0):
             assert np.float32(g["h_peak"]).tobytes().hex() == s["h_peak"]
 
 
-def test_search_full_size_c3_golden(mp):
+@pytest.mark.parametrize("l2_persist", [False, True])
+def test_search_full_size_c3_golden(mp, monkeypatch, l2_persist):
+    """C3 full size against the oracle's stored run; with l2_persist the
+    search runs under the optional L2 access-policy window over the CSR
+    (MPAP_SEARCH_L2_PERSIST), which must not change anything."""
+    if l2_persist:
+        monkeypatch.setenv("MPAP_SEARCH_L2_PERSIST", "1")
     prob = make_problem(load_config("c3"))
     rm = mp.pb.build_problem(prob)
     _golden_check(mp, rm, prob, json.load(open(os.path.join(GOLDEN, "c3_full.json"))))
