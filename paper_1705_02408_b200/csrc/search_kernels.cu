@@ -470,7 +470,9 @@ __device__ void cta_merge(Ctl* S, const SlotCaps& C, int x, int n, const int4* c
     const int lane = tid & 31, w = tid >> 5, nr = (p2 + 31) >> 5;
     for (int k = 2; k <= 32; k <<= 1) {
       for (int j = k >> 1; j > 0; j >>= 1) {
-        const int4 o = shfl_xor4(v, j);
+        // every candidate of the node has the same .x (the node): 3 shuffles
+        const int4 o = make_int4(v.x, __shfl_xor_sync(FULLM, v.y, j), __shfl_xor_sync(FULLM, v.z, j),
+                                 __shfl_xor_sync(FULLM, v.w, j));
         const bool up = (lane & k) == 0;
         const bool sw = ((lane & j) == 0) ? (cand_less(o, v) == up) : (cand_less(v, o) == up);
         if (sw) v = o;
