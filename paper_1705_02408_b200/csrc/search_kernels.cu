@@ -1698,6 +1698,7 @@ struct CapHint {
 constexpr int kMaxDevices = 64;
 constexpr size_t kHintArenaBytes = size_t(4) << 30;
 constexpr int kHintMaxSlots = 64;
+constexpr int64_t kGridHalfNnz = 256 * 1024;
 CapHint g_cap_hint[kMaxDevices];
 std::mutex g_cap_mu;
 
@@ -1886,6 +1887,16 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     while (csize > 2 && nrun * csize > nsm * occ) csize >>= 1;
     const bool cluster_mode = !grid_mode && use_cluster && (nrun * csize <= nsm * occ || rm->lazy);
     const int nslots = grid_mode ? 1 : cluster_mode ? nrun : std::min(nrun, nsm * occ);
+    // whole-grid team: one block per SM; half the SMs for a roadmap of at
+    // most kGridHalfNnz edges, whose waves are too small to pay for the
+    // wider barriers (measured: C1-C3 single queries 10-20 % faster on 74
+    // blocks, C4 1.5x slower)
+    int grid_ctas = nsm * occ_grid;
+    if (grid_mode) {
+      const int env0 = h_queries[todo[0]].env;
+      if (rm->edge_base[env0 + 1] - rm->edge_base[env0] <= kGridHalfNnz) grid_ctas = std::max(1, grid_ctas / 2);
+    }
+    if (const char* gc = getenv("MPAP_SEARCH_GRID_CTAS")) grid_ctas = std::max(1, std::min(nsm * occ_grid, atoi(gc)));
     // (only for up to kHintMaxSlots slots: a many-slot arena seeded from a
     // smaller batch's maxima kept growing the workspace step after step)
     if (round == 0 && nslots <= kHintMaxSlots && dev >= 0 && dev < kMaxDevices &&
@@ -1964,7 +1975,7 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
           if (grid_mode) {
             void* args[] = {&A, &d_ctl};
             const void* fn = trace ? (const void*)k_search_grid<true> : (const void*)k_search_grid<false>;
-            CKS(cudaLaunchCooperativeKernel(fn, dim3(nsm * occ_grid), dim3(kST), args, kBigSmem, st));
+            CKS(cudaLaunchCooperativeKernel(fn, dim3(grid_ctas), dim3(kST), args, kBigSmem, st));
           } else {
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(nslots * csize);
@@ -2000,7 +2011,7 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
       if (grid_mode) {
         void* args[] = {&A, &d_ctl};
         const void* fn = trace ? (const void*)k_search_grid<true> : (const void*)k_search_grid<false>;
-        CKS(cudaLaunchCooperativeKernel(fn, dim3(nsm * occ_grid), dim3(kST), args, kBigSmem, st));
+        CKS(cudaLaunchCooperativeKernel(fn, dim3(grid_ctas), dim3(kST), args, kBigSmem, st));
       } else if (cluster_mode) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(nslots * csize);
