@@ -1884,6 +1884,10 @@ mpap_status search_batch_device(const mpap_roadmap* rm, int32_t nq, const QueryD
     // runs batches in cluster mode, one static slot per query, so suspended
     // queries resume in place.)
     int csize = kCluster;
+    if (const char* cs = getenv("MPAP_SEARCH_CLUSTER")) {   // tuning: largest cluster size (2, 4 or 8)
+      const int c = atoi(cs);
+      if (c == 2 || c == 4 || c == 8) csize = c;
+    }
     while (csize > 2 && nrun * csize > nsm * occ) csize >>= 1;
     const bool cluster_mode = !grid_mode && use_cluster && (nrun * csize <= nsm * occ || rm->lazy);
     const int nslots = grid_mode ? 1 : cluster_mode ? nrun : std::min(nrun, nsm * occ);
